@@ -1,0 +1,191 @@
+/*
+ * ebv.h — C ABI of libebv.so, the B200 (sm_100a) implementation of the hot
+ * path of the "Equal bi-Vectorized" (EbV) method, arXiv 1907.05767.
+ *
+ * Citations: P:<line> = PAPER.md (the paper text), DESIGN.md = this repo's
+ * design notes (readings R1..R16 of the garbled passages).
+ *
+ * The problem statement followed by every call (Eq 1):
+ *     AX = B  <=>  (LU)X = B  <=>  L(UX) = B  <=>  LY = B, then UX = Y.
+ * A is factored without pivoting into a unit lower triangular L and an upper
+ * triangular U (Doolittle; Eq 3, reading R1) by the per-step
+ * recurrences of Eq 6:
+ *     l_ik = a_ik / a_kk            (Eq 6-a, the L_(k) column vector)
+ *     u_kj = a_kj                   (Eq 6-b, the U_(k) row vector, reading R1)
+ *     a_ij <- a_ij - l_ik u_kj      (Eq 6-c, the rank-1 update of A^(k))
+ * for a diagonally dominant A ("diagonal dominant shape").  Every
+ * entry is produced as the fma chain over ascending k followed (for L) by a
+ * correctly rounded division — the canonical order of DESIGN.md, which makes
+ * the results bitwise identical to the serial oracle.
+ *
+ * Conventions shared by all calls
+ *   - Matrices are column-major: a(i, j) = A[i + j*lda], lda >= n.  The
+ *     factorization is packed in place: strict lower triangle = L multipliers
+ *     (unit diagonal implicit), diagonal + upper triangle = U.
+ *   - All matrix / vector / info pointers are DEVICE pointers owned by the
+ *     caller; the library never frees them.  The library owns only its
+ *     context (workspace, streams, events).
+ *   - Calls are asynchronous on the caller's `stream` (a cudaStream_t passed
+ *     as void*; NULL = legacy default stream).  The library never
+ *     synchronizes the caller's stream.
+ *   - Host-detectable argument errors return EBV_ERR_INVALID_VALUE before
+ *     anything is launched.  CUDA launch / runtime failures return
+ *     EBV_ERR_CUDA; ebv_last_error() gives a one-line description.
+ *   - A singular / small pivot is never a return code: it is reported through
+ *     the device-side info word(s) (LAPACK getrf convention): 0, or the first
+ *     1-based step r with |u_rr| <= tau.  The factorization always runs to
+ *     completion; outputs are unspecified (may hold Inf/NaN) when info != 0.
+ *   - tau: pivot floor.  tau >= 0 is used as is (0 = exact-zero check only);
+ *     tau < 0 selects the default n * DBL_EPSILON * ||A||_inf (reading R9),
+ *     computed on the device by a norm pre-pass.
+ */
+#ifndef EBV_H_
+#define EBV_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  EBV_SUCCESS = 0,
+  EBV_ERR_INVALID_VALUE = 1,  /* bad size / stride / NULL pointer            */
+  EBV_ERR_SINGULAR_PIVOT = 2, /* never returned by the async calls; for
+                                 callers that map a nonzero info word        */
+  EBV_ERR_CUDA = 3,           /* a CUDA runtime error (see ebv_last_error)    */
+  EBV_ERR_NCCL = 4,           /* reserved for the multi-GPU context           */
+  EBV_ERR_NOT_SUPPORTED = 5,  /* valid but unsupported (e.g. batched n > 32)  */
+  EBV_ERR_ALLOC = 6           /* workspace allocation failed                  */
+} ebv_status_t;
+
+/* Opaque context: device, workspace, auxiliary streams/events, options. */
+typedef struct ebv_context* ebv_context_t;
+
+/* Which factorization path ebv_lu_factor takes.
+ *   EBV_PATH_VECTOR  — the paper's vector-level elimination (Eq 6 step by
+ *                      step) as one persistent kernel: each CTA owns
+ *                      EbV-paired columns (j, n-1-j) (Eq 7) resident
+ *                      in shared memory; per step the owner of column k
+ *                      publishes L_(k) and every CTA applies the rank-1 update
+ *                      to its columns.  n <= EBV_VECTOR_MAX_N.
+ *   EBV_PATH_BLOCKED — recursive blocked form of the same recurrences: the
+ *                      trailing rank-k updates run as FP64 tensor-core (DMMA)
+ *                      contractions, triangular blocks by row/column-parallel
+ *                      substitution.  Any n.
+ *   EBV_PATH_AUTO    — VECTOR for n <= 256... see ebv_lu_factor.           */
+typedef enum { EBV_PATH_AUTO = 0, EBV_PATH_VECTOR = 1, EBV_PATH_BLOCKED = 2 } ebv_path_t;
+
+#define EBV_VECTOR_MAX_N 2048
+#define EBV_BATCHED_MAX_N 32
+
+/* Column-block -> rank layouts for a 1D distribution:
+ * CYCLIC = J mod P; EBVPAIR = block pairs (J, N-1-J) dealt round-robin
+ * (the paper's first-with-last equalization, Eq 7, applied to blocks);
+ * SNAKE = reflective (boustrophedon) order. */
+typedef enum { EBV_LAYOUT_CYCLIC = 0, EBV_LAYOUT_EBVPAIR = 1, EBV_LAYOUT_SNAKE = 2 } ebv_layout_t;
+
+/* ---- context ------------------------------------------------------------ */
+
+/* Create a context on CUDA device `device` (made current for the call).
+ * *ctx receives the handle.  Errors: INVALID_VALUE (ctx NULL, bad device),
+ * CUDA, ALLOC. */
+ebv_status_t ebv_create(ebv_context_t* ctx, int device);
+
+/* Destroy a context (synchronizes the context's own resources only). */
+ebv_status_t ebv_destroy(ebv_context_t ctx);
+
+/* Static description of a status code (never NULL). */
+const char* ebv_status_string(ebv_status_t s);
+
+/* Description of the last error on the calling thread ("" if none). */
+const char* ebv_last_error(void);
+
+/* Select the factorization path (default EBV_PATH_AUTO). */
+ebv_status_t ebv_set_path(ebv_context_t ctx, ebv_path_t path);
+
+/* Blocked path leaf size (the diagonal blocks factored inside one CTA);
+ * 0 restores the default.  Must be a multiple of 8 in [8, 64]. */
+ebv_status_t ebv_set_leaf(ebv_context_t ctx, int64_t leaf);
+
+/* ---- the hot path (Eq 1, Eq 6) ------------------------------------------ */
+
+/* A = LU in place, no pivoting (Eq 6-a..c).
+ *   n      order of A (n >= 0; n == 0 is a no-op that sets *d_info = 0)
+ *   A      device, column-major n x n with leading dimension lda >= max(1,n);
+ *          overwritten by the packed L\U factors
+ *   tau    pivot floor (see the conventions above)
+ *   d_info device int64: written with 0 or the first failing 1-based step
+ *   stream cudaStream_t
+ * Errors (synchronous, nothing launched): INVALID_VALUE for n < 0,
+ * lda < max(1,n), A or d_info NULL (when n > 0), or PATH_VECTOR with
+ * n > EBV_VECTOR_MAX_N. */
+ebv_status_t ebv_lu_factor(ebv_context_t ctx, int64_t n, double* A, int64_t lda, double tau,
+                           int64_t* d_info, void* stream);
+
+/* X from LY = B then UX = Y (Eq 1; "UX = B" read as UX = Y, R6).
+ *   LU     device, the packed output of ebv_lu_factor (column-major, lda)
+ *   B      device, n x nrhs column-major (ldb >= max(1,n)), overwritten by X
+ * Each right-hand side column is processed in the canonical order (forward:
+ * y_i = fma chain over ascending k of -l_ik y_k from b_i; backward: x_k =
+ * y_k / u_kk, then y_i -= u_ik x_k for i < k, k descending).
+ * Errors: INVALID_VALUE for n < 0, nrhs < 0, lda/ldb < max(1,n), NULL
+ * pointers when n > 0 and nrhs > 0. */
+ebv_status_t ebv_lu_solve(ebv_context_t ctx, int64_t n, const double* LU, int64_t lda, double* B,
+                          int64_t ldb, int64_t nrhs, void* stream);
+
+/* Batched independent systems (BASELINE.json configs[4]; reading R16):
+ * system s has A_s = A + s*strideA (n x n column-major, lda) and, if B is not
+ * NULL, right-hand sides B_s = B + s*strideB (n x nrhs, ldb), solved in place
+ * (fused factor + solve).  Each system is factored exactly like
+ * ebv_lu_factor (bitwise).  d_info[s] (device int32) receives each system's
+ * info.  One warp holds two systems; lane t owns rows t and n-1-t of its
+ * system (the paper's first-with-last pairing, Eq 7, at lane granularity).
+ * Sharding across GPUs = the caller passes its shard's pointers.
+ * Errors: INVALID_VALUE (n < 0, batch < 0, lda < n, strides too small,
+ * NULL pointers); NOT_SUPPORTED for n > EBV_BATCHED_MAX_N or nrhs > 16. */
+ebv_status_t ebv_lu_factor_batched(ebv_context_t ctx, int64_t n, double* A, int64_t lda,
+                                   int64_t strideA, int64_t batch, double* B, int64_t ldb,
+                                   int64_t strideB, int64_t nrhs, double tau, int32_t* d_info,
+                                   void* stream);
+
+/* ---- EbV plan (host, pure; Eq 7) -------------------------- */
+
+/* Owner map over n indices (columns, rows or blocks): index j is paired with
+ * n-1-j (first with last), pairs p = 0,1,... dealt round-robin to `workers`
+ * (reading R12).  owner: host array of n int32.  Errors: INVALID_VALUE. */
+ebv_status_t ebv_plan_owner_map(int64_t n, int64_t workers, int32_t* owner);
+
+/* The paper's equal-length units (Eq 7; SPEC equalize): for n >= 2 exactly
+ * n-1 units.  Unit u is written as (tri0[u], k0[u], tri1[u], k1[u]) with
+ * tri = 0 for an L vector, 1 for a U vector, k 1-based, and tri1 = -1 for a
+ * single-member unit (never produced: every unit has two members), plus its
+ * round-robin owner.  Arrays have n-1 entries.  Errors: INVALID_VALUE. */
+ebv_status_t ebv_plan_units(int64_t n, int64_t workers, int32_t* tri0, int32_t* k0, int32_t* tri1,
+                            int32_t* k1, int32_t* owner);
+
+/* Owner rank of column block J of N blocks over nranks under `layout`
+ * (-1 on invalid arguments). */
+int64_t ebv_block_owner(int64_t J, int64_t N, int64_t nranks, ebv_layout_t layout);
+
+/* ---- measurement --------------------------------------------------------- */
+
+/* Per-kernel-class statistics, recorded with CUDA events on the launching
+ * stream while enabled (off by default).  Classes: 0 = DMMA trailing update
+ * (GEMM), 1 = diagonal-block LU, 2 = TRSM, 3 = solve, 4 = batched,
+ * 5 = vector path, 6 = other.  ebv_stats_get synchronizes the events and
+ * returns for class c: launches, total milliseconds, algorithmic flops and
+ * algorithmic bytes. */
+#define EBV_NUM_KCLASSES 7
+ebv_status_t ebv_stats_enable(ebv_context_t ctx, int enable);
+ebv_status_t ebv_stats_reset(ebv_context_t ctx);
+ebv_status_t ebv_stats_get(ebv_context_t ctx, int kclass, int64_t* launches, double* ms,
+                           double* flops, double* bytes);
+
+/* Number of kernels this context launched since creation (all classes). */
+int64_t ebv_launch_count(ebv_context_t ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EBV_H_ */
