@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""bench.py — EbV LU factor + solve on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[3] at N=1, the configuration the metric is
+quoted on): one dense diagonally dominant fp64 system, n = 32768, 1 RHS,
+generated on the device by ebv_inputs (seeded, synthetic).  One step = one
+ebv_lu_factor (A = LU, Eq 6) + one ebv_lu_solve (LY = B, UX = Y, Eq 1) on a
+fresh copy of A (the copy from a pristine device buffer is inside the timed
+region and counted against the step).
+
+value = nominal factor flops (2/3 n^3) per step * steps / timed seconds, in
+GFLOP/s — the "LU factor GFLOP/s" of the metric, charged with the solve and
+the restore copy; factor_ms / solve_ms are reported beside it ("solve ms").
+
+--impl reference runs the serial CPU oracle (oracle/, the test
+infrastructure) on a bounded sample of the same workload: the leading
+m x m principal submatrix of the same n = 32768 matrix (bit-identical
+entries), per step one oracle factor + solve.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_DEFAULT = 32768
+CPU_SAMPLE_M = 2048
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ebv", choices=["ebv", "reference"])
+    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--nrhs", type=int, default=1)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE_M)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() in ("active", "1", "yes"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    """The serial oracle, as it stands, on the host cores (1 thread)."""
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import ebv_inputs
+    import oracle
+
+    m = args.cpu_sample
+    d = ebv_inputs.generate_leading(args.n, m, seed=args.seed, nrhs=args.nrhs)
+    a = d["At"].T.numpy().copy()
+    b = d["B"].numpy().copy()
+    oracle.build()
+    times = []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        lu, info = oracle.lu_factor(a)
+        x = oracle.lu_solve(lu, b)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    assert info == 0 and np.max(np.abs(x - d["X"].numpy())) <= 1e-10
+    tot = sum(times)
+    fl = 2.0 / 3.0 * m ** 3
+    value = fl * len(times) / tot / 1e9
+    sample = (f"leading {m}x{m} principal submatrix of the n={args.n} seed={args.seed} matrix "
+              f"(bit-identical entries); per step one serial oracle factor + {args.nrhs}-rhs solve; "
+              f"GFLOP/s = (2/3) m^3 / step time")
+    line = {
+        "impl": "reference", "metric": "LU factor GFLOP/s + solve ms at n=32768 fp64 (oracle on a bounded sample)",
+        "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"dense DD fp64 n={args.n}, {args.nrhs} rhs (sample m={m})", "n": args.n,
+                   "sample_m": m, "nrhs": args.nrhs, "seed": args.seed},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------- CPU baseline leg
+def cpu_baseline(args):
+    import numpy as np
+
+    import ebv_inputs
+    import oracle
+
+    m = args.cpu_sample
+    d = ebv_inputs.generate_leading(args.n, m, seed=args.seed, nrhs=args.nrhs)
+    a = d["At"].T.numpy().copy()
+    b = d["B"].numpy().copy()
+    oracle.build()
+    t0 = time.perf_counter()
+    lu, info = oracle.lu_factor(a)
+    x = oracle.lu_solve(lu, b)
+    dt = time.perf_counter() - t0
+    ok = info == 0 and float(np.max(np.abs(x - d["X"].numpy()))) <= 1e-10
+    return {"value": 2.0 / 3.0 * m ** 3 / dt / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
+            "sample": (f"leading {m}x{m} principal submatrix of the n={args.n} matrix (same entries), one serial "
+                       f"oracle factor + solve, {dt:.2f} s, GFLOP/s = (2/3) m^3 / t; correct={ok}"),
+            "seconds": dt}
+
+
+def dmma_peak_tflops():
+    """Measured FP64 DMMA peak (probe M2, profiles/r01_probe_dmma.jsonl)."""
+    best = None
+    p = os.path.join(ROOT, "profiles", "r01_probe_dmma.jsonl")
+    try:
+        with open(p) as f:
+            for ln in f:
+                r = json.loads(ln)
+                if str(r.get("probe", "")).startswith("M2_dmma"):
+                    best = max(best or 0.0, float(r["tflops"]))
+    except OSError:
+        pass
+    return best or 37.2
+
+
+def ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_gemm_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except OSError:
+        return None
+
+
+# --------------------------------------------------------------------- product arm
+def run_ebv(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    import ebv_inputs
+    import paper_1907_05767_b200 as ebv
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n, nrhs = args.n, args.nrhs
+    # inputs resident in HBM before the timed region (generated on the device)
+    d = ebv_inputs.generate(n, seed=args.seed + rank, nrhs=nrhs, device=dev)
+    A0 = d["At"]                       # pristine column-major storage (row j = column j)
+    B0 = d["B"].T.contiguous()         # (nrhs, n): column-major storage of B
+    Xtrue = d["X"]
+    del d
+    Aw = torch.empty_like(A0)
+    Bw = torch.empty_like(B0)
+    info = torch.zeros((), dtype=torch.int64, device=dev)
+    ctx = ebv.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+
+    def step(ev=None):
+        Aw.copy_(A0)
+        Bw.copy_(B0)
+        if ev:
+            ev[0].record(stream)
+        s = ebv.ebv_lu_factor(ctx.handle, n, Aw.data_ptr(), n, 0.0, info.data_ptr(), sh)
+        if ev:
+            ev[1].record(stream)
+        s |= ebv.ebv_lu_solve(ctx.handle, n, Aw.data_ptr(), n, Bw.data_ptr(), n, nrhs, sh)
+        if ev:
+            ev[2].record(stream)
+        if s:
+            raise RuntimeError(ebv.ebv_last_error())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ok = int(info) == 0
+    err = (Bw.T - Xtrue).abs().max().item()
+    ok = ok and err <= 1e-10
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk.start()
+    ctx.stats_reset()
+    ctx.stats_enable(True)
+    l0 = ctx.launch_count()
+    t_start.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    ctx.stats_enable(False)
+    launches = ctx.launch_count() - l0
+    clocks = clk.stop()
+    if world > 1:
+        dist.barrier()
+    region_ms = t_start.elapsed_time(t_end)
+    f_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    s_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    st = ctx.stats()
+    if world > 1:
+        t = torch.tensor([region_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        region_ms = t.item()
+    fl = 2.0 / 3.0 * n ** 3
+    value = fl * args.steps * world / (region_ms / 1e3) / 1e9
+    g = st["gemm_dmma"]
+    peak = dmma_peak_tflops()
+    achieved = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else None
+    traffic = ncu_traffic()
+    total_kernel_ms = sum(v["ms"] for v in st.values())
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": (achieved / peak) if achieved else None,
+                "traffic": (traffic or {}).get("bytes_per_launch"),
+                "kernel": "gemm_sub_kernel (DMMA.8x8x4 trailing update, Eq 6-c)",
+                "launches": g["launches"], "kernel_ms_per_step": g["ms"] / args.steps,
+                "share_of_step": g["ms"] / max(total_kernel_ms, 1e-9),
+                "algorithmic_flops_per_launch": g["flops"] / max(g["launches"], 1),
+                "peak_source": "measured: sm_100a DMMA.8x8x4 issue-rate probe M2 (profiles/r01_probe_dmma.jsonl); "
+                               "cuBLAS DGEMM 16384^3 = 36.2 TF (profiles/r01_probe_torch.jsonl)"}
+
+    # ---- end to end through the public API from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        hA = torch.empty(A0.shape, dtype=torch.float64, pin_memory=True)
+        hB = torch.empty(B0.shape, dtype=torch.float64, pin_memory=True)
+        hX = torch.empty(B0.shape, dtype=torch.float64, pin_memory=True)
+        hA.copy_(A0)
+        hB.copy_(B0)
+        torch.cuda.synchronize()
+
+        def e2e_step():
+            Aw.copy_(hA, non_blocking=True)
+            Bw.copy_(hB, non_blocking=True)
+            s = ebv.ebv_lu_factor(ctx.handle, n, Aw.data_ptr(), n, 0.0, info.data_ptr(), sh)
+            s |= ebv.ebv_lu_solve(ctx.handle, n, Aw.data_ptr(), n, Bw.data_ptr(), n, nrhs, sh)
+            hX.copy_(Bw, non_blocking=True)
+            if s:
+                raise RuntimeError(ebv.ebv_last_error())
+
+        e2e_step()
+        torch.cuda.synchronize()
+        ksteps = max(1, min(args.steps, 3))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        e0.record(stream)
+        for _ in range(ksteps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = t.item()
+        e2e_ok = (hX.T - Xtrue.cpu()).abs().max().item() <= 1e-10
+        e2e = {"value": fl * ksteps * world / (ems / 1e3) / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(hA.numel() * 8 + hB.numel() * 8), "d2h_bytes_per_step": int(hX.numel() * 8),
+               "ms_per_step": ems / ksteps, "steps": ksteps, "correct": bool(e2e_ok)}
+        del hA, hB, hX
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            cpu = cpu_baseline(args)
+        out = {
+            "metric": "LU factor GFLOP/s + solve ms at n=32768 fp64, 1/2/4/8 B200, % FP64 peak",
+            "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": region_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak" if world > 1 else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (ebv_inputs counter-hash DD generator, on device)",
+            "config": {"workload": f"dense diagonally dominant fp64 n={n}, {nrhs} rhs (BASELINE configs[3])",
+                       "n": n, "nrhs": nrhs, "seed": args.seed, "path": "blocked (recursive, DMMA)",
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs (8.6 GB) larger than L2 (126 MB); no flush needed"},
+            "factor_ms": statistics.median(f_ms), "solve_ms": statistics.median(s_ms),
+            "factor_gflops": fl / (statistics.median(f_ms) / 1e3) / 1e9,
+            "factor_frac_of_peak": fl / (statistics.median(f_ms) / 1e3) / 1e12 / peak,
+            "solve_gbs": 8.0 * n * n / (statistics.median(s_ms) / 1e3) / 1e9,
+            "correct": bool(ok), "max_abs_err_x": err,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks, "kernel_stats": st,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ebv(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

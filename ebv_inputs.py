@@ -161,3 +161,32 @@ def closed_form_inputs(n: int, seed: int = 1, alpha: float | None = None, beta: 
     At = beta * torch.outer(sf, sf)
     At[rows, rows] += alpha
     return At, s
+
+
+def generate_leading(n: int, m: int, seed: int = 1, nrhs: int = 1, device="cpu", system: int = 0):
+    """The leading m x m principal submatrix of generate(n, seed) (same
+    entries bit for bit: the diagonal uses the full-row sums over all n
+    columns), plus an exact right-hand side B_m = A_m X_m for the first m
+    entries of x_true.  Cost O(m n) hashes — a bounded sample of the
+    n x n workload for the CPU baseline."""
+    dev = torch.device(device)
+    base = system_base(seed, system)
+    rows = torch.arange(m, dtype=torch.int64, device=dev)
+    rowsum = torch.zeros(m, dtype=torch.int64, device=dev)
+    chunk = max(1, (1 << 24) // max(m, 1))
+    for j0 in range(0, n, chunk):
+        j1 = min(n, j0 + chunk)
+        jj = torch.arange(j0, j1, dtype=torch.int64, device=dev)
+        K = offdiag_units(base, rows[None, :], jj[:, None])
+        K = torch.where(rows[None, :] == jj[:, None], torch.zeros_like(K), K)
+        rowsum += K.abs().sum(0)
+    jj = torch.arange(m, dtype=torch.int64, device=dev)
+    K = offdiag_units(base, rows[None, :], jj[:, None])
+    K = torch.where(rows[None, :] == jj[:, None], torch.zeros_like(K), K)
+    dunits = rowsum + ONE_UNITS
+    rr = torch.arange(nrhs, dtype=torch.int64, device=dev)
+    X_u = xtrue_units(base, rows[:, None], rr[None, :], n)
+    B_u = (K.t() @ X_u if dev.type == "cpu" else _int_matmul(K.t(), X_u)) + dunits[:, None] * X_u
+    At = K.to(torch.float64) * SCALE
+    At[jj, jj] = dunits.to(torch.float64) * SCALE
+    return {"At": At, "X": X_u.to(torch.float64), "B": B_u.to(torch.float64) * SCALE, "n": m}

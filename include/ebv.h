@@ -73,10 +73,11 @@ typedef struct ebv_context* ebv_context_t;
  *                      trailing rank-k updates run as FP64 tensor-core (DMMA)
  *                      contractions, triangular blocks by row/column-parallel
  *                      substitution.  Any n.
- *   EBV_PATH_AUTO    — VECTOR for n <= 256... see ebv_lu_factor.           */
+ *   EBV_PATH_AUTO    — the blocked path (the faster one at every n measured;
+ *                      DESIGN.md §Paths).                                    */
 typedef enum { EBV_PATH_AUTO = 0, EBV_PATH_VECTOR = 1, EBV_PATH_BLOCKED = 2 } ebv_path_t;
 
-#define EBV_VECTOR_MAX_N 2048
+#define EBV_VECTOR_MAX_N 1536
 #define EBV_BATCHED_MAX_N 32
 
 /* Column-block -> rank layouts for a 1D distribution:
@@ -107,6 +108,18 @@ ebv_status_t ebv_set_path(ebv_context_t ctx, ebv_path_t path);
 /* Blocked path leaf size (the diagonal blocks factored inside one CTA);
  * 0 restores the default.  Must be a multiple of 8 in [8, 64]. */
 ebv_status_t ebv_set_leaf(ebv_context_t ctx, int64_t leaf);
+
+/* Blocked path schedule: nb > 0 = right-looking with column blocks of nb
+ * (a multiple of the leaf; default 256) — panel LU, U12 substitution, DMMA
+ * trailing update per block; nb = -1 = fully recursive 2 x 2 splitting;
+ * nb = 0 restores the default.  Both are bitwise identical. */
+ebv_status_t ebv_set_block(ebv_context_t ctx, int64_t nb);
+
+/* Vector path CTA count: 0 = automatic (one CTA per SM, preferring a count
+ * that divides the number of column pairs); > 0 = that many CTAs with the EbV
+ * paired owner map; < 0 = |ctas| CTAs with the plain cyclic map j mod C (the
+ * comparison baseline for the pairing). */
+ebv_status_t ebv_set_vector_ctas(ebv_context_t ctx, int64_t ctas);
 
 /* ---- the hot path (Eq 1, Eq 6) ------------------------------------------ */
 
@@ -148,6 +161,17 @@ ebv_status_t ebv_lu_factor_batched(ebv_context_t ctx, int64_t n, double* A, int6
                                    int64_t strideA, int64_t batch, double* B, int64_t ldb,
                                    int64_t strideB, int64_t nrhs, double tau, int32_t* d_info,
                                    void* stream);
+
+/* The trailing rank-k update of Eq 6-c on its own — the DMMA
+ * contraction every blocked / distributed schedule is built from:
+ *     C <- C - A * B      A: M x K (lda), B: K x N (ldb), C: M x N (ldc),
+ * all device, column-major.  Each entry of C is the fma chain
+ * c <- fma(-a_ik, b_kj, c) over k = 0..K-1 ascending starting from its input
+ * value (bitwise the oracle's order for those k).  Errors: INVALID_VALUE for
+ * negative sizes, leading dimensions below the row counts, NULL pointers
+ * when the product is non-empty. */
+ebv_status_t ebv_update(ebv_context_t ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                        const double* B, int64_t ldb, double* C, int64_t ldc, void* stream);
 
 /* ---- EbV plan (host, pure; Eq 7) -------------------------- */
 

@@ -1,0 +1,332 @@
+"""paper_1907_05767_b200 — B200 (sm_100a) implementation of the hot path of the
+"Equal bi-Vectorized" (EbV) method (arXiv 1907.05767): no-pivot LU factor
+A = LU of diagonally dominant fp64 matrices followed by forward (LY = B) and
+backward (UX = Y) substitution (Eq 1, Eq 6 of the paper).
+
+This module is a thin binding over the C ABI of ``libebv.so``
+(include/ebv.h): argument marshalling only — every step of the path runs in
+the library's CUDA kernels.  PyTorch is used for device memory and streams.
+There is no CPU fallback: if the library is missing, every call raises.
+
+Two layers:
+  * the C-ABI mirror, same names as include/ebv.h (``ebv_lu_factor(ctx, n,
+    A_ptr, lda, tau, info_ptr, stream)`` ...), taking raw device pointers;
+  * tensor helpers (``lu_factor``, ``lu_solve``, ``lu_factor_batched``,
+    ``Context``) that take torch CUDA float64 tensors in logical [i, j]
+    indexing and pass column-major storage to the library.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libebv.so")
+
+EBV_SUCCESS = 0
+EBV_PATH_AUTO, EBV_PATH_VECTOR, EBV_PATH_BLOCKED = 0, 1, 2
+EBV_LAYOUT_CYCLIC, EBV_LAYOUT_EBVPAIR, EBV_LAYOUT_SNAKE = 0, 1, 2
+KCLASSES = ["gemm_dmma", "leaf_lu", "trsm", "solve", "batched", "vector", "other"]
+
+# every exported symbol of include/ebv.h with its ctypes signature
+_i64, _i32, _vp, _d, _int = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_double, ctypes.c_int
+SIGNATURES = {
+    "ebv_create": (_int, [ctypes.POINTER(_vp), _int]),
+    "ebv_destroy": (_int, [_vp]),
+    "ebv_status_string": (ctypes.c_char_p, [_int]),
+    "ebv_last_error": (ctypes.c_char_p, []),
+    "ebv_set_path": (_int, [_vp, _int]),
+    "ebv_set_leaf": (_int, [_vp, _i64]),
+    "ebv_set_vector_ctas": (_int, [_vp, _i64]),
+    "ebv_set_block": (_int, [_vp, _i64]),
+    "ebv_lu_factor": (_int, [_vp, _i64, _vp, _i64, _d, _vp, _vp]),
+    "ebv_lu_solve": (_int, [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp]),
+    "ebv_lu_factor_batched": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _d, _vp, _vp]),
+    "ebv_update": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp]),
+    "ebv_plan_owner_map": (_int, [_i64, _i64, _vp]),
+    "ebv_plan_units": (_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "ebv_block_owner": (_i64, [_i64, _i64, _i64, _int]),
+    "ebv_stats_enable": (_int, [_vp, _int]),
+    "ebv_stats_reset": (_int, [_vp]),
+    "ebv_stats_get": (_int, [_vp, _int, ctypes.POINTER(_i64), ctypes.POINTER(_d), ctypes.POINTER(_d),
+                             ctypes.POINTER(_d)]),
+    "ebv_launch_count": (_i64, [_vp]),
+}
+
+_lib = None
+
+
+class EbvError(RuntimeError):
+    pass
+
+
+def lib():
+    """Load libebv.so (raises if it has not been built — no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise EbvError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int, what: str):
+    if status != EBV_SUCCESS:
+        L = lib()
+        raise EbvError(f"{what}: {L.ebv_status_string(status).decode()} ({L.ebv_last_error().decode()})")
+
+
+# ------------------------------------------------------------------ C-ABI mirror
+def ebv_create(device: int = 0) -> int:
+    h = _vp()
+    _check(lib().ebv_create(ctypes.byref(h), device), "ebv_create")
+    return h.value
+
+
+def ebv_destroy(ctx: int) -> int:
+    return lib().ebv_destroy(ctx)
+
+
+def ebv_status_string(s: int) -> str:
+    return lib().ebv_status_string(s).decode()
+
+
+def ebv_last_error() -> str:
+    return lib().ebv_last_error().decode()
+
+
+def ebv_set_path(ctx, path):
+    return lib().ebv_set_path(ctx, path)
+
+
+def ebv_set_leaf(ctx, leaf):
+    return lib().ebv_set_leaf(ctx, leaf)
+
+
+def ebv_set_block(ctx, nb):
+    return lib().ebv_set_block(ctx, nb)
+
+
+def ebv_set_vector_ctas(ctx, ctas):
+    return lib().ebv_set_vector_ctas(ctx, ctas)
+
+
+def ebv_lu_factor(ctx, n, A, lda, tau, d_info, stream):
+    return lib().ebv_lu_factor(ctx, n, A, lda, tau, d_info, stream)
+
+
+def ebv_lu_solve(ctx, n, LU, lda, B, ldb, nrhs, stream):
+    return lib().ebv_lu_solve(ctx, n, LU, lda, B, ldb, nrhs, stream)
+
+
+def ebv_lu_factor_batched(ctx, n, A, lda, strideA, batch, B, ldb, strideB, nrhs, tau, d_info, stream):
+    return lib().ebv_lu_factor_batched(ctx, n, A, lda, strideA, batch, B, ldb, strideB, nrhs, tau, d_info, stream)
+
+
+def ebv_update(ctx, M, N, K, A, lda, B, ldb, C, ldc, stream):
+    return lib().ebv_update(ctx, M, N, K, A, lda, B, ldb, C, ldc, stream)
+
+
+def update(C: torch.Tensor, A: torch.Tensor, B: torch.Tensor, ctx: Context | None = None):
+    """C <- C - A @ B in place (Eq 6-c rank-k update); all column-major CUDA float64."""
+    for t, nm in ((C, "C"), (A, "A"), (B, "B")):
+        _require(t, nm)
+        if _colmajor_ld(t) < 0:
+            raise EbvError(f"{nm} must be column-major")
+    M, N = C.shape
+    K = A.shape[1]
+    ctx = ctx or default_context(C.device.index or 0)
+    _check(ebv_update(ctx.handle, M, N, K, A.data_ptr(), max(_colmajor_ld(A), 1), B.data_ptr(),
+                      max(_colmajor_ld(B), 1), C.data_ptr(), max(_colmajor_ld(C), 1), _stream_handle(C.device)),
+           "ebv_update")
+    return C
+
+
+def ebv_plan_owner_map(n: int, workers: int):
+    out = (ctypes.c_int32 * max(n, 1))()
+    _check(lib().ebv_plan_owner_map(n, workers, out), "ebv_plan_owner_map")
+    return list(out)[:n]
+
+
+def ebv_plan_units(n: int, workers: int):
+    m = max(n - 1, 1)
+    arrs = [(ctypes.c_int32 * m)() for _ in range(5)]
+    _check(lib().ebv_plan_units(n, workers, *arrs), "ebv_plan_units")
+    t0, k0, t1, k1, own = (list(a)[: n - 1] for a in arrs)
+    tri = "LU"
+    units = [((tri[a], b), (tri[c], d)) for a, b, c, d in zip(t0, k0, t1, k1)]
+    return units, own
+
+
+def ebv_block_owner(J, N, nranks, layout=EBV_LAYOUT_CYCLIC) -> int:
+    return lib().ebv_block_owner(J, N, nranks, layout)
+
+
+def ebv_launch_count(ctx) -> int:
+    return lib().ebv_launch_count(ctx)
+
+
+# ------------------------------------------------------------------ tensor helpers
+def _stream_handle(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class Context:
+    """Owns an ebv_context_t on one CUDA device."""
+
+    def __init__(self, device: int | torch.device = 0, path: int = EBV_PATH_AUTO, leaf: int = 0):
+        if isinstance(device, torch.device):
+            device = device.index or 0
+        if not torch.cuda.is_available():
+            raise EbvError("paper_1907_05767_b200 needs a CUDA device (no CPU fallback)")
+        self.device = int(device)
+        self.handle = ebv_create(self.device)
+        _check(ebv_set_path(self.handle, path), "ebv_set_path")
+        _check(ebv_set_leaf(self.handle, leaf), "ebv_set_leaf")
+
+    def set_path(self, path: int):
+        _check(ebv_set_path(self.handle, path), "ebv_set_path")
+
+    def set_leaf(self, leaf: int):
+        _check(ebv_set_leaf(self.handle, leaf), "ebv_set_leaf")
+
+    def set_block(self, nb: int):
+        _check(ebv_set_block(self.handle, nb), "ebv_set_block")
+
+    def set_vector_ctas(self, ctas: int):
+        _check(ebv_set_vector_ctas(self.handle, ctas), "ebv_set_vector_ctas")
+
+    def stats_enable(self, on: bool = True):
+        _check(lib().ebv_stats_enable(self.handle, 1 if on else 0), "ebv_stats_enable")
+
+    def stats_reset(self):
+        _check(lib().ebv_stats_reset(self.handle), "ebv_stats_reset")
+
+    def stats(self) -> dict:
+        out = {}
+        for c, name in enumerate(KCLASSES):
+            n, ms, fl, by = _i64(), _d(), _d(), _d()
+            _check(lib().ebv_stats_get(self.handle, c, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(fl),
+                                       ctypes.byref(by)), "ebv_stats_get")
+            out[name] = {"launches": n.value, "ms": ms.value, "flops": fl.value, "bytes": by.value}
+        return out
+
+    def launch_count(self) -> int:
+        return ebv_launch_count(self.handle)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            ebv_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+_default_ctx: dict[int, Context] = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default_ctx:
+        _default_ctx[device] = Context(device)
+    return _default_ctx[device]
+
+
+def _colmajor_ld(t: torch.Tensor) -> int:
+    """Leading dimension if t (logical [rows, cols]) is column-major-strided
+    with ld >= rows, else -1."""
+    if t.dim() != 2:
+        return -1
+    rows, cols = t.shape
+    if cols <= 1:
+        return max(rows, 1) if (t.stride(0) == 1 or rows <= 1) else -1
+    if t.stride(0) != 1 and rows > 1:
+        return -1
+    return t.stride(1) if t.stride(1) >= max(rows, 1) else -1
+
+
+def colmajor_copy(t: torch.Tensor) -> torch.Tensor:
+    """A fresh column-major (Fortran-ordered) copy of a 2-D tensor."""
+    return t.mT.clone(memory_format=torch.contiguous_format).mT
+
+
+def _require(t: torch.Tensor, what: str):
+    if not t.is_cuda or t.dtype != torch.float64:
+        raise EbvError(f"{what} must be a CUDA float64 tensor")
+
+
+def lu_factor(A: torch.Tensor, tau: float = 0.0, ctx: Context | None = None, inplace: bool = False):
+    """A = LU without pivoting (Eq 6).  A: (n, n) CUDA float64, logical
+    indexing.  Returns (LU, info): LU is the column-major packed L\\U (A
+    itself when inplace=True, which needs column-major A), info a 0-dim int64
+    CUDA tensor (0 or the first failing 1-based step)."""
+    _require(A, "A")
+    n = A.shape[0]
+    if A.dim() != 2 or A.shape[1] != n:
+        raise EbvError("A must be square")
+    ctx = ctx or default_context(A.device.index or 0)
+    if inplace:
+        if _colmajor_ld(A) < 0:
+            raise EbvError("inplace lu_factor needs a column-major A (A.mT contiguous)")
+        LU = A
+    else:
+        LU = colmajor_copy(A)
+    info = torch.zeros((), dtype=torch.int64, device=A.device)
+    _check(ebv_lu_factor(ctx.handle, n, LU.data_ptr(), max(_colmajor_ld(LU), 1), float(tau), info.data_ptr(),
+                         _stream_handle(A.device)), "ebv_lu_factor")
+    return LU, info
+
+
+def lu_solve(LU: torch.Tensor, B: torch.Tensor, ctx: Context | None = None, inplace: bool = False):
+    """X from LY = B then UX = Y (Eq 1).  B: (n,) or (n, nrhs) CUDA float64.
+    Returns X (B itself when inplace=True and B is column-major)."""
+    _require(LU, "LU")
+    _require(B, "B")
+    n = LU.shape[0]
+    ctx = ctx or default_context(LU.device.index or 0)
+    vec = B.dim() == 1
+    B2 = B.reshape(n, 1) if vec else B
+    if inplace and _colmajor_ld(B2) > 0:
+        X = B2
+    else:
+        X = colmajor_copy(B2)
+    LUc = LU if _colmajor_ld(LU) > 0 else colmajor_copy(LU)
+    _check(ebv_lu_solve(ctx.handle, n, LUc.data_ptr(), max(_colmajor_ld(LUc), 1), X.data_ptr(),
+                        max(_colmajor_ld(X), 1), X.shape[1], _stream_handle(LU.device)), "ebv_lu_solve")
+    if vec:
+        return X.reshape(n)
+    return X
+
+
+def lu_factor_batched(At: torch.Tensor, Bt: torch.Tensor | None = None, tau: float = 0.0,
+                      ctx: Context | None = None):
+    """In place on per-system column-major storage: At (batch, n, n) with
+    At[s, j, i] = a^(s)_ij (contiguous), Bt (batch, nrhs, n) with Bt[s, r, i]
+    = b^(s)_i,r (contiguous) or None.  Returns the int32 info tensor."""
+    _require(At, "At")
+    if not At.is_contiguous():
+        raise EbvError("At must be contiguous (batch, n, n) column-major storage")
+    batch, n, _ = At.shape
+    ctx = ctx or default_context(At.device.index or 0)
+    info = torch.zeros(batch, dtype=torch.int32, device=At.device)
+    if Bt is not None:
+        _require(Bt, "Bt")
+        if not Bt.is_contiguous():
+            raise EbvError("Bt must be contiguous (batch, nrhs, n)")
+        nrhs = Bt.shape[1]
+        bptr, ldb, sb = Bt.data_ptr(), max(n, 1), n * nrhs
+    else:
+        nrhs, bptr, ldb, sb = 0, None, max(n, 1), 0
+    _check(ebv_lu_factor_batched(ctx.handle, n, At.data_ptr(), max(n, 1), n * n, batch, bptr, ldb, sb, nrhs,
+                                 float(tau), info.data_ptr(), _stream_handle(At.device)), "ebv_lu_factor_batched")
+    return info

@@ -1,0 +1,520 @@
+// ebv_api.cu — the C ABI of libebv.so (include/ebv.h): argument validation,
+// context / workspace management, the recursive blocked schedule and the
+// measurement hooks.  All arithmetic happens in the kernels (k_*.cu).
+//
+// Blocked schedule (EBV_PATH_BLOCKED): the Eq 6 recurrences applied
+// to a 2 x 2 block partition, recursively:
+//     LU(A11);  L21 = A21 U11^-1;  U12 = L11^-1 A12;  A22 -= L21 U12;  LU(A22)
+// The triangular solves recurse the same way (X2 -= X1 U12 between the two
+// halves), so every flop outside the <= 64 x 64 leaves is a DMMA contraction
+// with a long k range, and every entry still sees its updates in ascending k
+// followed by its division (bitwise equal to the serial oracle).
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "ebv_internal.cuh"
+
+struct ebv_context {
+  int device = 0;
+  ebv_path_t path = EBV_PATH_AUTO;
+  int64_t leaf = 64;
+  int64_t nb = 256;         // right-looking block width; -1 = fully recursive schedule
+  double* d_tau = nullptr;
+  unsigned long long* d_norm = nullptr;
+  double* d_scratch = nullptr;
+  int* d_ticket = nullptr;
+  int* d_flags = nullptr;
+  int64_t flags_cap = 0;
+  int* d_vflags = nullptr;
+  int64_t vflags_cap = 0;
+  int64_t solve_epoch = 0;
+  int64_t launches = 0;
+  int vector_ctas = 0;      // 0 = auto; < 0 = cyclic map with |value| CTAs (for comparison)
+  bool stats = false;
+  struct Rec {
+    int cls;
+    cudaEvent_t e0, e1;
+    double flops, bytes;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  int64_t st_launch[EBV_NUM_KCLASSES] = {0};
+  double st_ms[EBV_NUM_KCLASSES] = {0}, st_flops[EBV_NUM_KCLASSES] = {0}, st_bytes[EBV_NUM_KCLASSES] = {0};
+};
+
+namespace ebv {
+namespace {
+thread_local std::string g_last_error;
+}
+void set_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace ebv
+
+using namespace ebv;
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+ebv_status_t cuda_fail(cudaError_t e, const char* where) {
+  set_error(std::string(where) + ": " + cudaGetErrorString(e));
+  return EBV_ERR_CUDA;
+}
+
+ebv_status_t invalid(const char* msg) {
+  set_error(msg);
+  return EBV_ERR_INVALID_VALUE;
+}
+
+cudaEvent_t get_event(ebv_context* c) {
+  if (!c->pool.empty()) {
+    cudaEvent_t e = c->pool.back();
+    c->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Launch wrapper: counts launches and (when enabled) brackets the launch with
+// CUDA events on the launching stream for the per-class statistics.
+template <class F>
+cudaError_t timed(ebv_context* c, int cls, double flops, double bytes, cudaStream_t s, int nlaunch, F&& f) {
+  c->launches += nlaunch;
+  if (!c->stats) return f();
+  ebv_context::Rec r{cls, get_event(c), get_event(c), flops, bytes};
+  cudaEventRecord(r.e0, s);
+  cudaError_t e = f();
+  cudaEventRecord(r.e1, s);
+  c->recs.push_back(r);
+  return e;
+}
+
+cudaError_t gemm(ebv_context* c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                 int64_t ldb, double* C, int64_t ldc, bool rev, cudaStream_t s) {
+  if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
+  double fl = 2.0 * M * N * K, by = 8.0 * (M * K + K * N + 2.0 * M * N);
+  return timed(c, KC_GEMM, fl, by, s, 1, [&] { return launch_gemm_sub(M, N, K, A, lda, B, ldb, C, ldc, rev, s); });
+}
+
+int64_t split_point(int64_t n, int64_t leaf) {
+  int64_t h = ((n / 2 + leaf - 1) / leaf) * leaf;
+  if (h >= n) h = n - leaf;
+  if (h <= 0) h = n / 2;
+  return h;
+}
+
+// X (m x k) <- X U^-1, U upper k x k
+cudaError_t trsm_r(ebv_context* c, int64_t m, int64_t k, double* X, int64_t ldx, const double* U, int64_t ldu,
+                   cudaStream_t s) {
+  if (m <= 0 || k <= 0) return cudaSuccess;
+  if (k <= c->leaf) {
+    double fl = (double)m * k * k, by = 16.0 * m * k + 8.0 * k * k / 2;
+    return timed(c, KC_TRSM, fl, by, s, 1, [&] { return launch_trsm_right_upper(m, k, X, ldx, U, ldu, s); });
+  }
+  int64_t h = split_point(k, c->leaf);
+  cudaError_t e = trsm_r(c, m, h, X, ldx, U, ldu, s);
+  if (e != cudaSuccess) return e;
+  e = gemm(c, m, k - h, h, X, ldx, U + h * ldu, ldu, X + h * ldx, ldx, false, s);
+  if (e != cudaSuccess) return e;
+  return trsm_r(c, m, k - h, X + h * ldx, ldx, U + h + h * ldu, ldu, s);
+}
+
+// X (k x m) <- L^-1 X, L unit lower k x k
+cudaError_t trsm_l(ebv_context* c, int64_t k, int64_t m, const double* L, int64_t ldl, double* X, int64_t ldx,
+                   cudaStream_t s) {
+  if (m <= 0 || k <= 0) return cudaSuccess;
+  if (k <= c->leaf) {
+    double fl = (double)m * k * k, by = 16.0 * m * k + 8.0 * k * k / 2;
+    return timed(c, KC_TRSM, fl, by, s, 1, [&] { return launch_trsm_left_lower_unit(k, m, L, ldl, X, ldx, s); });
+  }
+  int64_t h = split_point(k, c->leaf);
+  cudaError_t e = trsm_l(c, h, m, L, ldl, X, ldx, s);
+  if (e != cudaSuccess) return e;
+  e = gemm(c, k - h, m, h, L + h, ldl, X, ldx, X + h, ldx, false, s);
+  if (e != cudaSuccess) return e;
+  return trsm_l(c, k - h, m, L + h + h * ldl, ldl, X + h, ldx, s);
+}
+
+// Fully recursive schedule (EBV_BLOCK_RECURSIVE):
+//     LU(A11);  L21 = A21 U11^-1;  U12 = L11^-1 A12;  A22 -= L21 U12;  LU(A22)
+cudaError_t lu_rec(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t koff, int64_t* info, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  if (n <= c->leaf) {
+    double fl = 2.0 / 3.0 * n * n * n, by = 16.0 * n * n;
+    return timed(c, KC_LEAF, fl, by, s, 1, [&] { return launch_leaf_lu(n, A, lda, c->d_tau, info, koff, s); });
+  }
+  int64_t h = split_point(n, c->leaf);
+  cudaError_t e = lu_rec(c, h, A, lda, koff, info, s);
+  if (e != cudaSuccess) return e;
+  e = trsm_r(c, n - h, h, A + h, lda, A, lda, s);                      // L21 = A21 U11^-1
+  if (e != cudaSuccess) return e;
+  e = trsm_l(c, h, n - h, A, lda, A + h * lda, lda, s);                // U12 = L11^-1 A12
+  if (e != cudaSuccess) return e;
+  e = gemm(c, n - h, n - h, h, A + h, lda, A + h * lda, lda, A + h + h * lda, lda, false, s);  // A22 -= L21 U12
+  if (e != cudaSuccess) return e;
+  return lu_rec(c, n - h, A + h + h * lda, lda, koff + h, info, s);
+}
+
+// LU of a tall panel P (M x w, M >= w) in place: its w x w top block becomes
+// L11\U11 and the rows below become L21 (Eq 6 restricted to the w steps of
+// the panel).  Recursive on the panel width; the leaves fuse nothing but are
+// a diagonal-block LU (one CTA) + a row-parallel L21 = A21 U11^-1.
+cudaError_t panel_rec(ebv_context* c, int64_t M, int64_t w, double* P, int64_t lda, int64_t koff, int64_t* info,
+                      cudaStream_t s) {
+  if (w <= 0) return cudaSuccess;
+  if (w <= c->leaf) {
+    double fl = 2.0 / 3.0 * w * w * w, by = 16.0 * w * w;
+    cudaError_t e = timed(c, KC_LEAF, fl, by, s, 1, [&] { return launch_leaf_lu(w, P, lda, c->d_tau, info, koff, s); });
+    if (e != cudaSuccess) return e;
+    return trsm_r(c, M - w, w, P + w, lda, P, lda, s);
+  }
+  int64_t h = split_point(w, c->leaf);
+  cudaError_t e = panel_rec(c, M, h, P, lda, koff, info, s);
+  if (e != cudaSuccess) return e;
+  e = trsm_l(c, h, w - h, P, lda, P + h * lda, lda, s);
+  if (e != cudaSuccess) return e;
+  e = gemm(c, M - h, w - h, h, P + h, lda, P + h * lda, lda, P + h + h * lda, lda, false, s);
+  if (e != cudaSuccess) return e;
+  return panel_rec(c, M - h, w - h, P + h + h * lda, lda, koff + h, info, s);
+}
+
+// Right-looking blocked schedule (default): for each column block K of width
+// nb — the block form of the step-k recurrences of Eq 6:
+//     panel LU of A[K:, K]          (L_(k), U_(k) vectors of the block's steps)
+//     U12 = L11^-1 A[K, K+1:]        (the U_(k) rows to the right)
+//     A[K+1:, K+1:] -= L21 U12       (Eq 6-c for the nb steps at once, DMMA)
+// This is also the per-step structure of the 1D block-cyclic multi-GPU
+// schedule (only the owner of block K factors the panel).
+cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s) {
+  const int64_t nb = c->nb;
+  for (int64_t c0 = 0; c0 < n; c0 += nb) {
+    const int64_t w = (n - c0) < nb ? (n - c0) : nb;
+    double* P = A + c0 + c0 * lda;
+    cudaError_t e = panel_rec(c, n - c0, w, P, lda, c0, info, s);
+    if (e != cudaSuccess) return e;
+    const int64_t rest = n - c0 - w;
+    if (rest <= 0) break;
+    e = trsm_l(c, w, rest, P, lda, P + w * lda, lda, s);
+    if (e != cudaSuccess) return e;
+    e = gemm(c, rest, rest, w, P + w, lda, P + w * lda, lda, P + w + w * lda, lda, false, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+ebv_status_t ensure_flags(ebv_context* c, int64_t need) {
+  if (need <= c->flags_cap) return EBV_SUCCESS;
+  if (c->d_flags) cudaFree(c->d_flags);
+  c->d_flags = nullptr;
+  cudaError_t e = cudaMalloc(&c->d_flags, need * sizeof(int));
+  if (e != cudaSuccess) { c->flags_cap = 0; set_error("workspace alloc failed"); return EBV_ERR_ALLOC; }
+  e = cudaMemset(c->d_flags, 0, need * sizeof(int));
+  if (e != cudaSuccess) return cuda_fail(e, "memset");
+  c->flags_cap = need;
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ensure_vflags(ebv_context* c, int64_t need) {
+  if (need <= c->vflags_cap) return EBV_SUCCESS;
+  if (c->d_vflags) cudaFree(c->d_vflags);
+  c->d_vflags = nullptr;
+  cudaError_t e = cudaMalloc(&c->d_vflags, need * sizeof(int));
+  if (e != cudaSuccess) { c->vflags_cap = 0; set_error("workspace alloc failed"); return EBV_ERR_ALLOC; }
+  e = cudaMemset(c->d_vflags, 0, need * sizeof(int));
+  if (e != cudaSuccess) return cuda_fail(e, "memset");
+  c->vflags_cap = need;
+  return EBV_SUCCESS;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ebv_status_string(ebv_status_t s) {
+  switch (s) {
+    case EBV_SUCCESS: return "success";
+    case EBV_ERR_INVALID_VALUE: return "invalid value";
+    case EBV_ERR_SINGULAR_PIVOT: return "singular pivot";
+    case EBV_ERR_CUDA: return "CUDA error";
+    case EBV_ERR_NCCL: return "NCCL error";
+    case EBV_ERR_NOT_SUPPORTED: return "not supported";
+    case EBV_ERR_ALLOC: return "allocation failed";
+  }
+  return "unknown status";
+}
+
+const char* ebv_last_error(void) { return g_last_error.c_str(); }
+
+ebv_status_t ebv_create(ebv_context_t* ctx, int device) {
+  if (!ctx) return invalid("ebv_create: ctx is NULL");
+  *ctx = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (device < 0 || device >= count) return invalid("ebv_create: bad device");
+  DeviceGuard g(device);
+  ebv_context* c = new ebv_context();
+  c->device = device;
+  // one allocation for the small scalars: tau, norm, scratch, tickets
+  char* base = nullptr;
+  e = cudaMalloc(&base, 256);
+  if (e != cudaSuccess) { delete c; return cuda_fail(e, "cudaMalloc"); }
+  cudaMemset(base, 0, 256);
+  c->d_tau = reinterpret_cast<double*>(base);
+  c->d_norm = reinterpret_cast<unsigned long long*>(base + 8);
+  c->d_scratch = reinterpret_cast<double*>(base + 16);
+  c->d_ticket = reinterpret_cast<int*>(base + 64);
+  *ctx = c;
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_destroy(ebv_context_t c) {
+  if (!c) return invalid("ebv_destroy: NULL");
+  DeviceGuard g(c->device);
+  for (auto& r : c->recs) { cudaEventDestroy(r.e0); cudaEventDestroy(r.e1); }
+  for (auto e : c->pool) cudaEventDestroy(e);
+  if (c->d_flags) cudaFree(c->d_flags);
+  if (c->d_vflags) cudaFree(c->d_vflags);
+  cudaFree(c->d_tau);
+  delete c;
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_set_path(ebv_context_t c, ebv_path_t path) {
+  if (!c) return invalid("ebv_set_path: NULL ctx");
+  if (path != EBV_PATH_AUTO && path != EBV_PATH_VECTOR && path != EBV_PATH_BLOCKED) return invalid("bad path");
+  c->path = path;
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_set_leaf(ebv_context_t c, int64_t leaf) {
+  if (!c) return invalid("ebv_set_leaf: NULL ctx");
+  if (leaf == 0) leaf = 64;
+  if (leaf < 8 || leaf > 64 || leaf % 8) return invalid("leaf must be a multiple of 8 in [8, 64]");
+  c->leaf = leaf;
+  if (c->nb > 0 && c->nb % leaf) c->nb = ((c->nb + leaf - 1) / leaf) * leaf;
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_set_block(ebv_context_t c, int64_t nb) {
+  if (!c) return invalid("ebv_set_block: NULL ctx");
+  if (nb == 0) nb = ((256 + c->leaf - 1) / c->leaf) * c->leaf;
+  if (nb != -1 && (nb < c->leaf || nb % c->leaf)) return invalid("block must be -1 or a multiple of the leaf size");
+  c->nb = nb;
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_set_vector_ctas(ebv_context_t c, int64_t ctas) {
+  if (!c) return invalid("ebv_set_vector_ctas: NULL ctx");
+  c->vector_ctas = (int)ctas;
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_lu_factor(ebv_context_t c, int64_t n, double* A, int64_t lda, double tau, int64_t* d_info,
+                           void* stream) {
+  if (!c) return invalid("ebv_lu_factor: NULL ctx");
+  if (n < 0) return invalid("ebv_lu_factor: n < 0");
+  if (lda < (n > 1 ? n : 1)) return invalid("ebv_lu_factor: lda < max(1, n)");
+  if (!d_info) return invalid("ebv_lu_factor: d_info is NULL");
+  if (n > 0 && !A) return invalid("ebv_lu_factor: A is NULL");
+  if (c->path == EBV_PATH_VECTOR && n > EBV_VECTOR_MAX_N) return invalid("ebv_lu_factor: n too large for PATH_VECTOR");
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = timed(c, KC_OTHER, 0, 0, s, 1, [&] { return launch_set_info0(d_info, s); });
+  if (e != cudaSuccess) return cuda_fail(e, "info init");
+  if (n == 0) return EBV_SUCCESS;
+  e = timed(c, KC_OTHER, 0, 8.0 * n * n, s, tau < 0 ? 3 : 1,
+            [&] { return launch_tau(n, A, lda, tau, c->d_tau, c->d_norm, s); });
+  if (e != cudaSuccess) return cuda_fail(e, "tau");
+  if (c->path == EBV_PATH_VECTOR) {
+    ebv_status_t st = ensure_vflags(c, n);
+    if (st != EBV_SUCCESS) return st;
+    int C = c->vector_ctas ? c->vector_ctas : vector_max_ctas(c->device, n);
+    int smem_max = 0, sms = 0;
+    cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    if (vector_smem_bytes(n, C) + 4096 > (size_t)smem_max || (C < 0 ? -C : C) > sms) {
+      set_error("vector path: owned columns do not fit in shared memory (or more CTAs than SMs)");
+      return EBV_ERR_NOT_SUPPORTED;
+    }
+    double fl = 2.0 / 3.0 * n * n * n, by = 16.0 * n * n;
+    e = timed(c, KC_VECTOR, fl, by, s, 2, [&] {
+      return launch_vector_lu(n, A, lda, c->d_tau, d_info, c->d_vflags, c->d_scratch, C, s);
+    });
+    if (e != cudaSuccess) return cuda_fail(e, "vector path");
+    return EBV_SUCCESS;
+  }
+  e = (c->nb > 0) ? lu_blocked(c, n, A, lda, d_info, s) : lu_rec(c, n, A, lda, 0, d_info, s);
+  if (e != cudaSuccess) return cuda_fail(e, "blocked factor");
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_lu_solve(ebv_context_t c, int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb,
+                          int64_t nrhs, void* stream) {
+  if (!c) return invalid("ebv_lu_solve: NULL ctx");
+  if (n < 0 || nrhs < 0) return invalid("ebv_lu_solve: negative size");
+  if (lda < (n > 1 ? n : 1) || ldb < (n > 1 ? n : 1)) return invalid("ebv_lu_solve: leading dimension too small");
+  if (n == 0 || nrhs == 0) return EBV_SUCCESS;
+  if (!LU || !B) return invalid("ebv_lu_solve: NULL pointer");
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t NB = (n + solve_block_rows() - 1) / solve_block_rows();
+  ebv_status_t st = ensure_flags(c, 2 * NB);
+  if (st != EBV_SUCCESS) return st;
+  c->solve_epoch++;
+  const int64_t groups = (nrhs + 15) / 16;
+  double by = (8.0 * n * n + 4.0 * 8.0 * n * nrhs), fl = 2.0 * n * n * nrhs;
+  cudaError_t e = timed(c, KC_SOLVE, fl, by, s, (int)(4 * groups), [&] {
+    return launch_solve(n, LU, lda, B, ldb, nrhs, c->d_ticket, c->d_flags, c->solve_epoch, s);
+  });
+  if (e != cudaSuccess) return cuda_fail(e, "solve");
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_lu_factor_batched(ebv_context_t c, int64_t n, double* A, int64_t lda, int64_t strideA,
+                                   int64_t batch, double* B, int64_t ldb, int64_t strideB, int64_t nrhs,
+                                   double tau, int32_t* d_info, void* stream) {
+  if (!c) return invalid("ebv_lu_factor_batched: NULL ctx");
+  if (n < 0 || batch < 0 || nrhs < 0) return invalid("ebv_lu_factor_batched: negative size");
+  if (lda < (n > 1 ? n : 1)) return invalid("ebv_lu_factor_batched: lda too small");
+  if (batch > 1 && strideA < lda * n) return invalid("ebv_lu_factor_batched: strideA < lda*n");
+  if (B && nrhs > 0) {
+    if (ldb < (n > 1 ? n : 1)) return invalid("ebv_lu_factor_batched: ldb too small");
+    if (batch > 1 && strideB < ldb * nrhs) return invalid("ebv_lu_factor_batched: strideB < ldb*nrhs");
+  }
+  if (n == 0 || batch == 0) return EBV_SUCCESS;
+  if (!A || !d_info) return invalid("ebv_lu_factor_batched: NULL pointer");
+  if (n > EBV_BATCHED_MAX_N) { set_error("batched path supports n <= 32"); return EBV_ERR_NOT_SUPPORTED; }
+  if (nrhs > 16) { set_error("batched path supports nrhs <= 16"); return EBV_ERR_NOT_SUPPORTED; }
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  double* Bp = (nrhs > 0) ? B : nullptr;
+  double fl = batch * (2.0 / 3.0 * n * n * n + 2.0 * n * n * (Bp ? nrhs : 0));
+  double by = batch * (16.0 * n * n + (Bp ? 16.0 * n * nrhs : 0) + 4.0);
+  cudaError_t e = timed(c, KC_BATCHED, fl, by, s, 1, [&] {
+    return launch_batched(n, A, lda, strideA, batch, Bp, ldb, strideB, nrhs, nullptr, tau < 0, tau < 0 ? 0.0 : tau,
+                          d_info, s);
+  });
+  if (e != cudaSuccess) return cuda_fail(e, "batched");
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_update(ebv_context_t c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                        const double* B, int64_t ldb, double* C, int64_t ldc, void* stream) {
+  if (!c) return invalid("ebv_update: NULL ctx");
+  if (M < 0 || N < 0 || K < 0) return invalid("ebv_update: negative size");
+  if (lda < (M > 1 ? M : 1) || ldb < (K > 1 ? K : 1) || ldc < (M > 1 ? M : 1))
+    return invalid("ebv_update: leading dimension too small");
+  if (M == 0 || N == 0 || K == 0) return EBV_SUCCESS;
+  if (!A || !B || !C) return invalid("ebv_update: NULL pointer");
+  DeviceGuard g(c->device);
+  cudaError_t e = gemm(c, M, N, K, A, lda, B, ldb, C, ldc, false, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "update");
+  return EBV_SUCCESS;
+}
+
+// ---- EbV plan ----------------------------------------------------------------
+
+ebv_status_t ebv_plan_owner_map(int64_t n, int64_t workers, int32_t* owner) {
+  if (n < 0 || workers < 1 || (n > 0 && !owner)) return invalid("ebv_plan_owner_map: bad arguments");
+  for (int64_t j = 0; j < n; j++) {
+    int64_t p = j < n - 1 - j ? j : n - 1 - j;
+    owner[j] = (int32_t)(p % workers);
+  }
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_plan_units(int64_t n, int64_t workers, int32_t* tri0, int32_t* k0, int32_t* tri1, int32_t* k1,
+                            int32_t* owner) {
+  if (n < 2 || workers < 1 || !tri0 || !k0 || !tri1 || !k1 || !owner) return invalid("ebv_plan_units: bad arguments");
+  int64_t u = 0;
+  // within each triangle pair k with n-k (first with last), k = 1..floor((n-1)/2)
+  for (int t = 0; t < 2; t++)
+    for (int64_t k = 1; k <= (n - 1) / 2; k++) {
+      tri0[u] = t; k0[u] = (int32_t)k; tri1[u] = t; k1[u] = (int32_t)(n - k);
+      u++;
+    }
+  if (n % 2 == 0) {   // merge the two middle vectors across triangles
+    tri0[u] = 0; k0[u] = (int32_t)(n / 2); tri1[u] = 1; k1[u] = (int32_t)(n / 2);
+    u++;
+  }
+  for (int64_t i = 0; i < u; i++) owner[i] = (int32_t)(i % workers);
+  return EBV_SUCCESS;
+}
+
+int64_t ebv_block_owner(int64_t J, int64_t N, int64_t nranks, ebv_layout_t layout) {
+  if (J < 0 || J >= N || nranks < 1) return -1;
+  switch (layout) {
+    case EBV_LAYOUT_CYCLIC: return J % nranks;
+    case EBV_LAYOUT_EBVPAIR: {
+      int64_t p = J < N - 1 - J ? J : N - 1 - J;
+      return p % nranks;
+    }
+    case EBV_LAYOUT_SNAKE: {
+      int64_t r = J % (2 * nranks);
+      return r < nranks ? r : 2 * nranks - 1 - r;
+    }
+  }
+  return -1;
+}
+
+// ---- measurement ---------------------------------------------------------------
+
+ebv_status_t ebv_stats_enable(ebv_context_t c, int enable) {
+  if (!c) return invalid("ebv_stats_enable: NULL ctx");
+  c->stats = enable != 0;
+  return EBV_SUCCESS;
+}
+
+static void drain(ebv_context* c) {
+  for (auto& r : c->recs) {
+    cudaEventSynchronize(r.e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, r.e0, r.e1);
+    c->st_launch[r.cls]++;
+    c->st_ms[r.cls] += ms;
+    c->st_flops[r.cls] += r.flops;
+    c->st_bytes[r.cls] += r.bytes;
+    c->pool.push_back(r.e0);
+    c->pool.push_back(r.e1);
+  }
+  c->recs.clear();
+}
+
+ebv_status_t ebv_stats_reset(ebv_context_t c) {
+  if (!c) return invalid("ebv_stats_reset: NULL ctx");
+  DeviceGuard g(c->device);
+  drain(c);
+  for (int i = 0; i < EBV_NUM_KCLASSES; i++) c->st_launch[i] = 0, c->st_ms[i] = c->st_flops[i] = c->st_bytes[i] = 0;
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_stats_get(ebv_context_t c, int kclass, int64_t* launches, double* ms, double* flops, double* bytes) {
+  if (!c || kclass < 0 || kclass >= EBV_NUM_KCLASSES) return invalid("ebv_stats_get: bad arguments");
+  DeviceGuard g(c->device);
+  drain(c);
+  if (launches) *launches = c->st_launch[kclass];
+  if (ms) *ms = c->st_ms[kclass];
+  if (flops) *flops = c->st_flops[kclass];
+  if (bytes) *bytes = c->st_bytes[kclass];
+  return EBV_SUCCESS;
+}
+
+int64_t ebv_launch_count(ebv_context_t c) { return c ? c->launches : -1; }
+
+}  // extern "C"

@@ -1,0 +1,72 @@
+// ebv_internal.cuh — internal declarations shared by the libebv translation
+// units (kernels + host dispatch).  Not part of the public C ABI (include/ebv.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+
+#include "../../include/ebv.h"
+
+namespace ebv {
+
+// Kernel classes for the measurement hooks (ebv_stats_*).
+enum KClass { KC_GEMM = 0, KC_LEAF = 1, KC_TRSM = 2, KC_SOLVE = 3, KC_BATCHED = 4, KC_VECTOR = 5,
+              KC_OTHER = 6 };
+
+void set_error(const std::string& msg);
+
+// ---- launchers (all asynchronous on `s`; return cudaGetLastError()) -------
+
+// C <- C - A*B  (A: M x K col-major lda, B: K x N col-major ldb, C: M x N ldc).
+// Every entry of C is the fma chain c <- fma(-a_ik, b_kj, c) over k ascending
+// (or descending when reverse_k), starting from its input value: the FP64
+// tensor-core (DMMA) contraction of the Eq 6-c rank-k update.
+cudaError_t launch_gemm_sub(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                            const double* B, int64_t ldb, double* C, int64_t ldc, bool reverse_k,
+                            cudaStream_t s);
+
+// TMA-fed variant (k_gemm_tma.cu); eligible for 16-byte aligned bases and
+// even leading dimensions.
+bool gemm_tma_eligible(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb);
+cudaError_t launch_gemm_sub_tma(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                                int64_t ldb, double* C, int64_t ldc, int variant, cudaStream_t s);
+
+// Unblocked LU of one diagonal block (n <= 64) inside one CTA (Eq 6-a..c).
+// Pivot check against *tau (device); the first failing step (1-based,
+// global index koff + k + 1) is written to *info if *info is still 0.
+cudaError_t launch_leaf_lu(int64_t n, double* A, int64_t lda, const double* tau, int64_t* info,
+                           int64_t koff, cudaStream_t s);
+
+// X <- X U^-1, U upper triangular k x k (k <= 64, non-unit), X m x k:
+// row-parallel substitution (the L21 panel of the blocked form).
+cudaError_t launch_trsm_right_upper(int64_t m, int64_t k, double* X, int64_t ldx, const double* U,
+                                    int64_t ldu, cudaStream_t s);
+
+// X <- L^-1 X, L unit lower triangular k x k (k <= 64), X k x m:
+// column-parallel substitution (the U12 panel of the blocked form).
+cudaError_t launch_trsm_left_lower_unit(int64_t k, int64_t m, const double* L, int64_t ldl, double* X,
+                                        int64_t ldx, cudaStream_t s);
+
+// Forward (LY = B) then backward (UX = Y) wavefront substitution (Eq 1).
+cudaError_t launch_solve(int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb, int64_t nrhs,
+                         int* ticket_ws, int* flags_ws, int64_t epoch, cudaStream_t s);
+int64_t solve_block_rows();
+
+// Batched n <= 32 fused factor + solve.
+cudaError_t launch_batched(int64_t n, double* A, int64_t lda, int64_t strideA, int64_t batch, double* B,
+                           int64_t ldb, int64_t strideB, int64_t nrhs, const double* tau, bool tau_default,
+                           double tau_value, int32_t* info, cudaStream_t s);
+
+// Vector-level EbV path (persistent cooperative kernel).
+cudaError_t launch_vector_lu(int64_t n, double* A, int64_t lda, const double* tau, int64_t* info,
+                             int* flags_ws, double* lbuf_ws, int num_ctas, cudaStream_t s);
+int vector_max_ctas(int device, int64_t n);
+size_t vector_smem_bytes(int64_t n, int num_ctas);
+
+// Utilities.
+cudaError_t launch_set_info0(int64_t* info, cudaStream_t s);
+// tau_out = (tau >= 0) ? tau : n * eps * ||A||_inf  (norm pre-pass)
+cudaError_t launch_tau(int64_t n, const double* A, int64_t lda, double tau, double* tau_out,
+                       unsigned long long* norm_ws, cudaStream_t s);
+
+}  // namespace ebv

@@ -1,0 +1,46 @@
+// k_util.cu — small device utilities of the dispatch layer: info reset and
+// the default pivot floor tau = n * DBL_EPSILON * ||A||_inf (reading R9).
+#include "ebv_internal.cuh"
+
+namespace ebv {
+namespace {
+
+__global__ void set_info0_kernel(int64_t* info) { *info = 0; }
+
+// row absolute sums (thread per row, coalesced over a column) -> max via
+// atomicMax on the IEEE bits (non-negative doubles order like uint64)
+__global__ void norm_inf_kernel(int64_t n, const double* __restrict__ A, int64_t lda, unsigned long long* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int64_t j = 0; j < n; j++) s += fabs(A[i + j * lda]);
+  atomicMax(out, (unsigned long long)__double_as_longlong(s));
+}
+
+__global__ void tau_kernel(int64_t n, const unsigned long long* nrm, double* tau_out) {
+  *tau_out = (double)n * 2.220446049250313e-16 * __longlong_as_double((long long)*nrm);
+}
+
+__global__ void set_tau_kernel(double tau, double* tau_out) { *tau_out = tau; }
+
+}  // namespace
+
+cudaError_t launch_set_info0(int64_t* info, cudaStream_t s) {
+  set_info0_kernel<<<1, 1, 0, s>>>(info);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tau(int64_t n, const double* A, int64_t lda, double tau, double* tau_out,
+                       unsigned long long* norm_ws, cudaStream_t s) {
+  if (tau >= 0.0 || n <= 0) {
+    set_tau_kernel<<<1, 1, 0, s>>>(tau >= 0.0 ? tau : 0.0, tau_out);
+    return cudaGetLastError();
+  }
+  cudaError_t e = cudaMemsetAsync(norm_ws, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  norm_inf_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, A, lda, norm_ws);
+  tau_kernel<<<1, 1, 0, s>>>(n, norm_ws, tau_out);
+  return cudaGetLastError();
+}
+
+}  // namespace ebv

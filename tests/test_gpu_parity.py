@@ -1,0 +1,319 @@
+"""GPU parity: the CUDA path through the C ABI against the serial oracle.
+
+Bar: the path keeps the oracle's per-entry operation
+order, so factor, solve and batched results are compared BITWISE
+(np.array_equal) at sizes the oracle finishes in seconds — spanning several
+leaves / tiles and ragged tails — and at the full BASELINE.json sizes via
+properties that hold at any size (closed form, leading principal submatrix,
+backward error).  The north_star tolerance (1e-10 relative, backward error
+<= 1e-12) is asserted as well, as the documented fallback bar.
+"""
+import numpy as np
+import pytest
+import torch
+
+import ebv_inputs
+import oracle
+from oracle import closed_form
+
+pytestmark = pytest.mark.gpu
+
+ebv = pytest.importorskip("paper_1907_05767_b200")
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda:0")
+
+
+@pytest.fixture(scope="module")
+def ctx(dev):
+    return ebv.Context(0)
+
+
+def run_factor(ctx, A, tau=0.0, path=ebv.EBV_PATH_BLOCKED, leaf=0, vector_ctas=0, nb=0):
+    ctx.set_path(path)
+    ctx.set_leaf(leaf)
+    ctx.set_block(nb)
+    ctx.set_vector_ctas(vector_ctas)
+    LU, info = ebv.lu_factor(A, tau=tau, ctx=ctx)
+    torch.cuda.synchronize()
+    ctx.set_path(ebv.EBV_PATH_AUTO)
+    ctx.set_leaf(0)
+    ctx.set_block(0)
+    ctx.set_vector_ctas(0)
+    return LU.cpu().numpy(), int(info)
+
+
+def tol_ok(g, o, rel=1e-10):
+    m = np.max(np.abs(o)) if o.size else 0.0
+    return np.max(np.abs(g - o)) <= rel * m if o.size else True
+
+
+# ------------------------------------------------------------------ generator
+def test_generator_device_equals_host(dev):
+    c = ebv_inputs.generate(333, seed=4, nrhs=2)
+    g = ebv_inputs.generate(333, seed=4, nrhs=2, device=dev)
+    for k in ("At", "X", "B"):
+        assert torch.equal(c[k], g[k].cpu())
+    cb = ebv_inputs.generate_batched(50, 32, seed=4)
+    gb = ebv_inputs.generate_batched(50, 32, seed=4, device=dev)
+    for k in ("At", "X", "B"):
+        assert torch.equal(cb[k], gb[k].cpu())
+
+
+# ------------------------------------------------------------------ blocked factor
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 17, 33, 64, 65, 100, 129, 200, 257, 511, 1000, 1536])
+def test_blocked_factor_bitwise(dev, ctx, n):
+    d = ebv_inputs.generate(n, seed=n, device=dev)
+    A = d["At"].T
+    lu_g, info = run_factor(ctx, A)
+    lu_o, info_o = oracle.lu_factor(A.cpu().numpy())
+    assert info == info_o == 0
+    assert np.array_equal(lu_g, lu_o)
+
+
+@pytest.mark.parametrize("nb", [64, 128, 192, 512, -1])
+def test_blocked_schedules_bitwise(dev, ctx, nb):
+    n = 700
+    d = ebv_inputs.generate(n, seed=nb + 1000, device=dev)
+    A = d["At"].T
+    lu_g, _ = run_factor(ctx, A, nb=nb)
+    lu_o, _ = oracle.lu_factor(A.cpu().numpy())
+    assert np.array_equal(lu_g, lu_o)
+
+
+@pytest.mark.parametrize("leaf", [8, 16, 24, 32, 48])
+def test_blocked_factor_leaf_sizes_bitwise(dev, ctx, leaf):
+    n = 300
+    d = ebv_inputs.generate(n, seed=leaf, device=dev)
+    A = d["At"].T
+    lu_g, _ = run_factor(ctx, A, leaf=leaf)
+    lu_o, _ = oracle.lu_factor(A.cpu().numpy())
+    assert np.array_equal(lu_g, lu_o)
+
+
+def test_blocked_factor_2048_bitwise_and_tolerance(dev, ctx):
+    n = 2048
+    d = ebv_inputs.generate(n, seed=21, device=dev)
+    A = d["At"].T
+    lu_g, _ = run_factor(ctx, A)
+    lu_o, _ = oracle.lu_factor(A.cpu().numpy())
+    assert tol_ok(lu_g, lu_o)
+    assert np.array_equal(lu_g, lu_o)
+
+
+def test_leading_dimension_and_odd_strides(dev, ctx):
+    n, lda = 150, 173
+    d = ebv_inputs.generate(n, seed=3, device=dev)
+    store = torch.zeros(n, lda, dtype=torch.float64, device=dev)   # row j = column j, padded
+    store[:, :n] = d["At"]
+    A = store.T[:n, :]      # logical (n, n) with stride (1, lda)
+    assert A.stride() == (1, lda)
+    LU, info = ebv.lu_factor(A, ctx=ctx, inplace=True)
+    torch.cuda.synchronize()
+    lu_o, _ = oracle.lu_factor(d["At"].T.cpu().numpy())
+    assert np.array_equal(store.T[:n, :].cpu().numpy(), lu_o)
+    assert not store[:, n:].any()      # padding untouched
+
+
+def test_determinism(dev, ctx):
+    d = ebv_inputs.generate(777, seed=5, device=dev)
+    a, _ = run_factor(ctx, d["At"].T)
+    b, _ = run_factor(ctx, d["At"].T)
+    assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------------ pivots / info
+def test_info_zero_pivot_and_tau(dev, ctx):
+    n = 130
+    for k0 in (0, 63, 64, 100, 129):
+        A = torch.eye(n, dtype=torch.float64, device=dev) * 2.0
+        A[k0, k0] = 0.0
+        _, info = run_factor(ctx, A)
+        assert info == k0 + 1
+        _, info_v = run_factor(ctx, A, path=ebv.EBV_PATH_VECTOR)
+        assert info_v == k0 + 1
+    A = torch.eye(n, dtype=torch.float64, device=dev)
+    A[5, 5] = 1e-30
+    assert run_factor(ctx, A, tau=0.0)[1] == 0
+    assert run_factor(ctx, A, tau=1e-20)[1] == 6
+    assert run_factor(ctx, A, tau=-1.0)[1] == 6      # default n*eps*||A||_inf
+    # first failing step wins, the factorization continues
+    A = torch.eye(n, dtype=torch.float64, device=dev)
+    A[70, 70] = 0.0
+    A[3, 3] = 0.0
+    assert run_factor(ctx, A)[1] == 4
+
+
+def test_argument_errors(dev, ctx):
+    L = ebv.lib()
+    info = torch.zeros((), dtype=torch.int64, device=dev)
+    A = torch.zeros(4, 4, dtype=torch.float64, device=dev)
+    assert L.ebv_lu_factor(ctx.handle, -1, A.data_ptr(), 4, 0.0, info.data_ptr(), None) == 1
+    assert L.ebv_lu_factor(ctx.handle, 4, A.data_ptr(), 3, 0.0, info.data_ptr(), None) == 1
+    assert L.ebv_lu_factor(ctx.handle, 4, None, 4, 0.0, info.data_ptr(), None) == 1
+    assert L.ebv_lu_factor(ctx.handle, 0, None, 1, 0.0, info.data_ptr(), None) == 0
+    assert L.ebv_lu_solve(ctx.handle, 4, A.data_ptr(), 4, None, 4, 1, None) == 1
+    assert L.ebv_lu_factor_batched(ctx.handle, 33, A.data_ptr(), 33, 33 * 33, 1, None, 33, 0, 0, 0.0,
+                                   info.data_ptr(), None) == 5
+    torch.cuda.synchronize()
+
+
+# ------------------------------------------------------------------ solve
+@pytest.mark.parametrize("n,nrhs", [(1, 1), (5, 2), (64, 1), (65, 3), (200, 16), (333, 17), (1000, 1), (1536, 5)])
+def test_solve_bitwise(dev, ctx, n, nrhs):
+    d = ebv_inputs.generate(n, seed=100 + n, nrhs=nrhs, device=dev)
+    A = d["At"].T
+    LU, _ = ebv.lu_factor(A, ctx=ctx)
+    X = ebv.lu_solve(LU, d["B"], ctx=ctx)
+    torch.cuda.synchronize()
+    lu_o, _ = oracle.lu_factor(A.cpu().numpy())
+    x_o = oracle.lu_solve(lu_o, d["B"].cpu().numpy())
+    assert np.array_equal(X.cpu().numpy(), x_o)
+    assert np.max(np.abs(X.cpu().numpy() - d["X"].cpu().numpy())) <= 1e-10
+
+
+def test_solve_vector_rhs_and_backward_error(dev, ctx):
+    n = 4096
+    d = ebv_inputs.generate(n, seed=9, nrhs=1, device=dev)
+    A = d["At"].T
+    LU, _ = ebv.lu_factor(A, ctx=ctx)
+    x = ebv.lu_solve(LU, d["B"][:, 0], ctx=ctx)
+    torch.cuda.synchronize()
+    r = (A @ x - d["B"][:, 0]).abs().max() / (A.abs().sum(1).max() * x.abs().max())
+    assert float(r) <= 1e-12
+
+
+# ------------------------------------------------------------------ vector path (EbV owner map)
+@pytest.mark.parametrize("n,ctas", [(1, 0), (2, 0), (3, 0), (64, 0), (255, 0), (1024, 0), (1024, 128), (1024, -128),
+                                    (1000, 100), (1536, 0)])
+def test_vector_path_bitwise(dev, ctx, n, ctas):
+    d = ebv_inputs.generate(n, seed=3 * n + 1, device=dev)
+    A = d["At"].T
+    lu_g, info = run_factor(ctx, A, path=ebv.EBV_PATH_VECTOR, vector_ctas=ctas)
+    lu_o, info_o = oracle.lu_factor(A.cpu().numpy())
+    assert info == info_o
+    assert np.array_equal(lu_g, lu_o)
+
+
+# ------------------------------------------------------------------ batched
+@pytest.mark.parametrize("n,batch,nrhs", [(32, 1000, 1), (32, 1, 1), (32, 7, 2), (1, 5, 1), (7, 33, 3),
+                                          (31, 64, 16), (32, 257, 0)])
+def test_batched_bitwise(dev, ctx, n, batch, nrhs):
+    db = ebv_inputs.generate_batched(batch, n, seed=n + batch, nrhs=max(nrhs, 1), device=dev)
+    At = db["At"].clone()
+    Bt = db["B"].transpose(1, 2).clone(memory_format=torch.contiguous_format)[:, :nrhs] if nrhs else None
+    if Bt is not None:
+        Bt = Bt.contiguous()
+    info = ebv.lu_factor_batched(At, Bt, ctx=ctx)
+    torch.cuda.synchronize()
+    a = db["At"].transpose(1, 2).cpu().numpy()
+    b = db["B"][:, :, :nrhs].cpu().numpy() if nrhs else None
+    lu_o, x_o, info_o = oracle.lu_factor_batched(a, b)
+    assert np.array_equal(info.cpu().numpy(), info_o)
+    assert np.array_equal(At.transpose(1, 2).cpu().numpy(), lu_o)
+    if nrhs:
+        assert np.array_equal(Bt.transpose(1, 2).cpu().numpy(), x_o)
+
+
+def test_batched_full_size_c5(dev, ctx):
+    """BASELINE.json configs[4]: 100k systems of n = 32, every system bitwise."""
+    batch = 100_000
+    db = ebv_inputs.generate_batched(batch, 32, seed=1, nrhs=1, device=dev)
+    At = db["At"].clone()
+    Bt = db["B"].transpose(1, 2).clone(memory_format=torch.contiguous_format)
+    info = ebv.lu_factor_batched(At, Bt, ctx=ctx)
+    torch.cuda.synchronize()
+    lu_o, x_o, info_o = oracle.lu_factor_batched(db["At"].transpose(1, 2).cpu().numpy(), db["B"].cpu().numpy())
+    assert not info.any().item()
+    assert np.array_equal(At.transpose(1, 2).cpu().numpy(), lu_o)
+    assert np.array_equal(Bt.transpose(1, 2).cpu().numpy(), x_o)
+
+
+def test_batched_singular_systems(dev, ctx):
+    db = ebv_inputs.generate_batched(10, 32, seed=2, device=dev)
+    At = db["At"].clone()
+    At[3, 5, :] = 0.0            # column 5 of system 3 zero -> u_55 == 0 exactly
+    At[7, 0, 0] = 0.0            # first pivot of system 7
+    ref = At.transpose(1, 2).cpu().numpy().copy()
+    info = ebv.lu_factor_batched(At, None, ctx=ctx)
+    torch.cuda.synchronize()
+    _, _, info_o = oracle.lu_factor_batched(ref, None)
+    assert info.cpu().tolist() == info_o.tolist()
+    assert info_o[3] == 6 and info_o[7] == 1
+
+
+# ------------------------------------------------------------------ full-size properties (C3 / C4)
+def test_closed_form_full_size(dev, ctx):
+    """A = n I + s s^T at BASELINE's n = 32768: every one of the n^2 entries
+    of the GPU factor against the closed form (oracle/closed_form.py)."""
+    n = 32768
+    At, s = ebv_inputs.closed_form_inputs(n, seed=1, device=dev)
+    A = At.T  # symmetric anyway
+    LU, info = ebv.lu_factor(A, ctx=ctx, inplace=False)
+    torch.cuda.synchronize()
+    assert int(info) == 0
+    del A, At
+    d, cl, cu = closed_form.factors_exact(n, n, 1, s.cpu().numpy())
+    dv = torch.tensor([float(x) for x in d], dtype=torch.float64, device=dev)
+    clv = torch.tensor([float(x) for x in cl], dtype=torch.float64, device=dev)
+    cuv = torch.tensor([float(x) for x in cu], dtype=torch.float64, device=dev)
+    sf = s.to(torch.float64)
+    worst = 0.0
+    for j0 in range(0, n, 2048):
+        j1 = j0 + 2048
+        blk = LU[:, j0:j1]                                  # (n, 2048)
+        rows = torch.arange(n, device=dev)[:, None]
+        cols = torch.arange(j0, j1, device=dev)[None, :]
+        ss = sf[:, None] * sf[None, j0:j1]
+        ref = torch.where(rows > cols, ss * clv[None, j0:j1],
+                          torch.where(rows < cols, ss * cuv[:, None], dv[None, j0:j1].expand(n, -1)))
+        rel = ((blk - ref).abs() / ref.abs()).max().item()
+        worst = max(worst, rel)
+    assert worst <= 1e-12, worst
+
+
+def test_c3_n8192_leading_submatrix_and_backward_error(dev, ctx):
+    """configs[2]: n = 8192, 16 right-hand sides.  LU of the leading 1536 x 1536
+    principal submatrix equals the oracle bitwise (it is the same computation);
+    full solve: x vs the exact x_true and the backward error bound."""
+    n, m = 8192, 1536
+    d = ebv_inputs.generate(n, seed=2, nrhs=16, device=dev)
+    A = d["At"].T
+    LU, info = ebv.lu_factor(A, ctx=ctx)
+    X = ebv.lu_solve(LU, d["B"], ctx=ctx)
+    torch.cuda.synchronize()
+    lu_o, _ = oracle.lu_factor(A[:m, :m].cpu().numpy())
+    assert np.array_equal(LU[:m, :m].cpu().numpy(), lu_o)
+    assert (X - d["X"]).abs().max().item() <= 1e-10
+    r = ((A @ X - d["B"]).abs().max() / (A.abs().sum(1).max() * X.abs().max())).item()
+    assert r <= 1e-12
+
+
+def test_c4_n32768_properties(dev, ctx):
+    """configs[3] size on one GPU: leading principal 1024 block bitwise vs the
+    oracle, sampled reconstruction (LU)_ij == a_ij within the backward-error
+    bound, and x vs the exact solution."""
+    n, m = 32768, 1024
+    d = ebv_inputs.generate(n, seed=1, nrhs=1, device=dev)
+    A = d["At"].T
+    LU, info = ebv.lu_factor(A, ctx=ctx)
+    x = ebv.lu_solve(LU, d["B"][:, 0], ctx=ctx)
+    torch.cuda.synchronize()
+    assert int(info) == 0
+    lu_o, _ = oracle.lu_factor(A[:m, :m].cpu().numpy())
+    assert np.array_equal(LU[:m, :m].cpu().numpy(), lu_o)
+    assert (x - d["X"][:, 0]).abs().max().item() <= 1e-10
+    g = torch.Generator(device="cpu").manual_seed(0)
+    ii = torch.randint(0, n, (2000,), generator=g).tolist()
+    jj = torch.randint(0, n, (2000,), generator=g).tolist()
+    amax = A.abs().max().item()
+    for i, j in zip(ii, jj):
+        if i <= j:   # (LU)_ij = sum_{p<i} l_ip u_pj + u_ij
+            v = (LU[i, :i] * LU[:i, j]).sum() + LU[i, j]
+        else:        # (LU)_ij = sum_{p<j} l_ip u_pj + l_ij u_jj
+            v = (LU[i, :j] * LU[:j, j]).sum() + LU[i, j] * LU[j, j]
+        assert abs(v.item() - A[i, j].item()) <= 1e-12 * amax
