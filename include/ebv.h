@@ -115,6 +115,12 @@ ebv_status_t ebv_set_leaf(ebv_context_t ctx, int64_t leaf);
  * nb = 0 restores the default.  Both are bitwise identical. */
 ebv_status_t ebv_set_block(ebv_context_t ctx, int64_t nb);
 
+/* Lookahead (default on): in the blocked schedule, panel K+1 is factored
+ * on a high-priority side stream of the context while step K's update of
+ * the remaining columns runs; ordering is by CUDA events, results are
+ * bitwise identical either way. */
+ebv_status_t ebv_set_lookahead(ebv_context_t ctx, int enable);
+
 /* Vector path CTA count: 0 = automatic (one CTA per SM, preferring a count
  * that divides the number of column pairs); > 0 = that many CTAs with the EbV
  * paired owner map; < 0 = |ctas| CTAs with the plain cyclic map j mod C (the

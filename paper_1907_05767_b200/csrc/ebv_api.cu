@@ -33,6 +33,9 @@ struct ebv_context {
   int64_t solve_epoch = 0;
   int64_t launches = 0;
   int vector_ctas = 0;      // 0 = auto; < 0 = cyclic map with |value| CTAs (for comparison)
+  bool lookahead = true;    // factor panel K+1 on a side stream under the update of step K
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_a = nullptr, ev_p = nullptr;
   bool stats = false;
   struct Rec {
     int cls;
@@ -202,19 +205,57 @@ cudaError_t panel_rec(ebv_context* c, int64_t M, int64_t w, double* P, int64_t l
 // schedule (only the owner of block K factors the panel).
 cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s) {
   const int64_t nb = c->nb;
+  const bool la = c->lookahead && n > 2 * nb;
+  cudaError_t e = cudaSuccess;
+  if (la) {
+    // the side stream starts after everything already queued on the caller's
+    e = cudaEventRecord(c->ev_start, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_start, 0);
+    if (e != cudaSuccess) return e;
+  }
+  e = panel_rec(c, n, (n < nb ? n : nb), A, lda, 0, info, s);
+  if (e != cudaSuccess) return e;
   for (int64_t c0 = 0; c0 < n; c0 += nb) {
     const int64_t w = (n - c0) < nb ? (n - c0) : nb;
     double* P = A + c0 + c0 * lda;
-    cudaError_t e = panel_rec(c, n - c0, w, P, lda, c0, info, s);
-    if (e != cudaSuccess) return e;
     const int64_t rest = n - c0 - w;
     if (rest <= 0) break;
+    if (la && c0 > 0) {   // panel K (factored on the side stream) must be complete
+      e = cudaStreamWaitEvent(s, c->ev_p, 0);
+      if (e != cudaSuccess) return e;
+    }
     e = trsm_l(c, w, rest, P, lda, P + w * lda, lda, s);
     if (e != cudaSuccess) return e;
-    e = gemm(c, rest, rest, w, P + w, lda, P + w * lda, lda, P + w + w * lda, lda, false, s);
-    if (e != cudaSuccess) return e;
+    const int64_t w1 = rest < nb ? rest : nb;        // width of panel K+1
+    double* P1 = P + w + w * lda;
+    if (la && rest > w1) {
+      // lookahead: update panel K+1's columns first, factor it on the side
+      // stream while the rest of the trailing matrix is updated
+      e = gemm(c, rest, w1, w, P + w, lda, P + w * lda, lda, P1, lda, false, s);
+      if (e == cudaSuccess) e = cudaEventRecord(c->ev_a, s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_a, 0);
+      if (e == cudaSuccess) e = panel_rec(c, rest, w1, P1, lda, c0 + w, info, c->side);
+      if (e == cudaSuccess) e = cudaEventRecord(c->ev_p, c->side);
+      if (e == cudaSuccess)
+        e = gemm(c, rest, rest - w1, w, P + w, lda, P + (w + w1) * lda, lda, P1 + w1 * lda, lda, false, s);
+      if (e != cudaSuccess) return e;
+    } else {
+      e = gemm(c, rest, rest, w, P + w, lda, P + w * lda, lda, P1, lda, false, s);
+      if (e != cudaSuccess) return e;
+      if (la) {   // keep the event protocol: the next panel is factored in order
+        e = panel_rec(c, rest, w1, P1, lda, c0 + w, info, s);
+        if (e == cudaSuccess) e = cudaEventRecord(c->ev_p, s);
+      } else {
+        e = panel_rec(c, rest, w1, P1, lda, c0 + w, info, s);
+      }
+      if (e != cudaSuccess) return e;
+    }
   }
-  return cudaSuccess;
+  if (la) {   // the caller's stream sees the last side-stream work
+    e = cudaEventRecord(c->ev_p, c->side);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, c->ev_p, 0);
+  }
+  return e;
 }
 
 ebv_status_t ensure_flags(ebv_context* c, int64_t need) {
@@ -279,6 +320,13 @@ ebv_status_t ebv_create(ebv_context_t* ctx, int device) {
   c->d_norm = reinterpret_cast<unsigned long long*>(base + 8);
   c->d_scratch = reinterpret_cast<double*>(base + 16);
   c->d_ticket = reinterpret_cast<int*>(base + 64);
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  e = cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_p, cudaEventDisableTiming);
+  if (e != cudaSuccess) { cudaFree(base); delete c; *ctx = nullptr; return cuda_fail(e, "stream/event create"); }
   *ctx = c;
   return EBV_SUCCESS;
 }
@@ -291,6 +339,10 @@ ebv_status_t ebv_destroy(ebv_context_t c) {
   if (c->d_flags) cudaFree(c->d_flags);
   if (c->d_vflags) cudaFree(c->d_vflags);
   cudaFree(c->d_tau);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_start) cudaEventDestroy(c->ev_start);
+  if (c->ev_a) cudaEventDestroy(c->ev_a);
+  if (c->ev_p) cudaEventDestroy(c->ev_p);
   delete c;
   return EBV_SUCCESS;
 }
@@ -316,6 +368,12 @@ ebv_status_t ebv_set_block(ebv_context_t c, int64_t nb) {
   if (nb == 0) nb = ((256 + c->leaf - 1) / c->leaf) * c->leaf;
   if (nb != -1 && (nb < c->leaf || nb % c->leaf)) return invalid("block must be -1 or a multiple of the leaf size");
   c->nb = nb;
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_set_lookahead(ebv_context_t c, int enable) {
+  if (!c) return invalid("ebv_set_lookahead: NULL ctx");
+  c->lookahead = enable != 0;
   return EBV_SUCCESS;
 }
 

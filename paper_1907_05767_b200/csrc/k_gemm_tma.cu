@@ -136,19 +136,38 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   }
 
   // -------------------------------------------------------------- consumers
+  // The accumulators hold the TRANSPOSED tile: the mma computes
+  // D' = (-B^T) A^T + C^T, i.e. D'[n][m] = c_mn + sum_k (-b_kn) a_mk, the very
+  // same products and the same ascending-k fma chain as C - A B (bitwise).
+  // Lane (g, t) then owns C[m = 2t, 2t+1][n = g]: two consecutive rows of a
+  // column-major column, one 16-byte load / store per fragment.
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % C::WM, wn = warp / C::WM;
+  const int64_t mb = (int64_t)m0 + wm * (C::MT * 8) + 2 * t;   // + mt*8 (+q)
+  const int64_t nb = (int64_t)n0 + wn * (C::NT * 8) + g;       // + nt*8
+  const bool vec_c = ((ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(Cm) & 15) == 0) &&
+                     (m0 + C::BM <= M) && (n0 + C::BN <= N);
   double acc[C::MT][C::NT][2];
+  if (vec_c) {
 #pragma unroll
-  for (int mt = 0; mt < C::MT; mt++)
+    for (int mt = 0; mt < C::MT; mt++)
 #pragma unroll
-    for (int nt = 0; nt < C::NT; nt++)
-#pragma unroll
-      for (int q = 0; q < 2; q++) {
-        int64_t m = m0 + wm * (C::MT * 8) + mt * 8 + g;
-        int64_t n = n0 + wn * (C::NT * 8) + nt * 8 + 2 * t + q;
-        acc[mt][nt][q] = (m < M && n < N) ? Cm[m + n * ldc] : 0.0;
+      for (int nt = 0; nt < C::NT; nt++) {
+        const double2 v = *reinterpret_cast<const double2*>(Cm + (mb + mt * 8) + (nb + nt * 8) * ldc);
+        acc[mt][nt][0] = v.x;
+        acc[mt][nt][1] = v.y;
       }
+  } else {
+#pragma unroll
+    for (int mt = 0; mt < C::MT; mt++)
+#pragma unroll
+      for (int nt = 0; nt < C::NT; nt++)
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+          const int64_t m = mb + mt * 8 + q, n = nb + nt * 8;
+          acc[mt][nt][q] = (m < M && n < N) ? Cm[m + n * ldc] : 0.0;
+        }
+  }
 
   for (int kt = 0; kt < nk; kt++) {
     const int s = kt % C::STAGES;
@@ -161,13 +180,13 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     for (int ks = 0; ks < C::KC / 4; ks++) {
       double af[C::MT], bf[C::NT];
 #pragma unroll
-      for (int mt = 0; mt < C::MT; mt++) af[mt] = -a[(ks * 4 + t) * C::AST + mt * 8];
+      for (int mt = 0; mt < C::MT; mt++) af[mt] = a[(ks * 4 + t) * C::AST + mt * 8];
 #pragma unroll
-      for (int nt = 0; nt < C::NT; nt++) bf[nt] = b[nt * 8 * C::BSTR + ks * 4];
+      for (int nt = 0; nt < C::NT; nt++) bf[nt] = -b[nt * 8 * C::BSTR + ks * 4];
 #pragma unroll
       for (int mt = 0; mt < C::MT; mt++)
 #pragma unroll
-        for (int nt = 0; nt < C::NT; nt++) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+        for (int nt = 0; nt < C::NT; nt++) dmma(acc[mt][nt][0], acc[mt][nt][1], bf[nt], af[mt]);
     }
     // all lanes' (generic-proxy) shared-memory reads of this stage are
     // ordered before the TMA (async-proxy) writes that may refill the slot
@@ -176,16 +195,24 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 
+  if (vec_c) {
 #pragma unroll
-  for (int mt = 0; mt < C::MT; mt++)
+    for (int mt = 0; mt < C::MT; mt++)
 #pragma unroll
-    for (int nt = 0; nt < C::NT; nt++)
+      for (int nt = 0; nt < C::NT; nt++)
+        *reinterpret_cast<double2*>(Cm + (mb + mt * 8) + (nb + nt * 8) * ldc) =
+            make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+  } else {
 #pragma unroll
-      for (int q = 0; q < 2; q++) {
-        int64_t m = m0 + wm * (C::MT * 8) + mt * 8 + g;
-        int64_t n = n0 + wn * (C::NT * 8) + nt * 8 + 2 * t + q;
-        if (m < M && n < N) Cm[m + n * ldc] = acc[mt][nt][q];
-      }
+    for (int mt = 0; mt < C::MT; mt++)
+#pragma unroll
+      for (int nt = 0; nt < C::NT; nt++)
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+          const int64_t m = mb + mt * 8 + q, n = nb + nt * 8;
+          if (m < M && n < N) Cm[m + n * ldc] = acc[mt][nt][q];
+        }
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
