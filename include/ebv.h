@@ -179,6 +179,58 @@ ebv_status_t ebv_lu_factor_batched(ebv_context_t ctx, int64_t n, double* A, int6
 ebv_status_t ebv_update(ebv_context_t ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                         const double* B, int64_t ldb, double* C, int64_t ldc, void* stream);
 
+/* ---- multi-GPU: one system over P GPUs -------- */
+/* 1D block-cyclic columns: column block J (width nb, the last one ragged)
+ * lives on rank ebv_block_owner(J, N, P, layout); a rank stores its blocks
+ * in ascending J as a column-major n x local_cols slab (ld >= n).  Per step K
+ * the owner factors the panel and broadcasts it over NCCL (in place, on the
+ * caller's stream); every rank substitutes and updates its blocks J > K.
+ * For a fixed nb the results are bitwise identical for every P and equal to
+ * ebv_lu_factor with ebv_set_block(nb) (and to the serial oracle).
+ * NCCL is loaded at run time (libnccl.so.2; EBV_NCCL_LIB overrides the
+ * path); all ranks must make the same calls in the same order. */
+
+/* 128-byte NCCL unique id for ebv_create_dist (call on one rank, share the
+ * bytes with the others, e.g. through torch.distributed).  Errors: NCCL. */
+ebv_status_t ebv_get_unique_id(void* uid);
+
+/* Context for rank `rank` of `nranks` on `device`, with its own NCCL
+ * communicator; nb: column block width (positive multiple of 64).
+ * Collective: every rank must call it.  Errors: INVALID_VALUE, NCCL, CUDA. */
+ebv_status_t ebv_create_dist(ebv_context_t* ctx, int device, const void* uid, int rank, int nranks, int64_t nb,
+                             ebv_layout_t layout);
+
+/* Host, pure: the column blocks rank `rank` owns (ascending J; blocks may be
+ * NULL to query the count), their count and the slab width local_cols. */
+ebv_status_t ebv_dist_local_blocks(int64_t n, int64_t nb, int rank, int nranks, ebv_layout_t layout, int64_t* blocks,
+                                   int64_t cap, int64_t* nblocks, int64_t* local_cols);
+
+/* Distributed A = LU (Eq 6): A_local is this rank's slab (device, column-
+ * major, lda >= n), factored in place; d_info (device int64) receives the
+ * global first failing step on every rank.  tau must be >= 0 (the default
+ * floor would need a global norm: NOT_SUPPORTED).  Collective. */
+ebv_status_t ebv_lu_factor_dist(ebv_context_t ctx, int64_t n, double* A_local, int64_t lda, double tau,
+                                int64_t* d_info, void* stream);
+
+/* Distributed solve (Eq 1) with the factors of ebv_lu_factor_dist: B (device,
+ * n x nrhs, ldb >= n) holds the same right-hand sides on every rank and is
+ * overwritten with X on every rank.  Forward / backward substitution pass B
+ * through the block owners in order (ncclSend / ncclRecv), so every entry is
+ * computed in the canonical order.  Collective. */
+ebv_status_t ebv_lu_solve_dist(ebv_context_t ctx, int64_t n, const double* LU_local, int64_t lda, double* B,
+                               int64_t ldb, int64_t nrhs, void* stream);
+
+/* Single-GPU emulation of the P-rank schedule (validation on one device):
+ * slabs is a HOST array of nranks device pointers, slab r laid out exactly as
+ * rank r's A_local; ctx is an ordinary context.  Same results as the real
+ * distributed calls. */
+ebv_status_t ebv_lu_factor_dist_emulated(ebv_context_t ctx, int64_t n, int nranks, int64_t nb, ebv_layout_t layout,
+                                         double* const* slabs, int64_t lda, double tau, int64_t* d_info,
+                                         void* stream);
+ebv_status_t ebv_lu_solve_dist_emulated(ebv_context_t ctx, int64_t n, int nranks, int64_t nb, ebv_layout_t layout,
+                                        double* const* slabs, int64_t lda, double* B, int64_t ldb, int64_t nrhs,
+                                        void* stream);
+
 /* ---- EbV plan (host, pure; Eq 7) -------------------------- */
 
 /* Owner map over n indices (columns, rows or blocks): index j is paired with

@@ -46,6 +46,14 @@ SIGNATURES = {
     "ebv_lu_solve": (_int, [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp]),
     "ebv_lu_factor_batched": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _d, _vp, _vp]),
     "ebv_update": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp]),
+    "ebv_get_unique_id": (_int, [_vp]),
+    "ebv_create_dist": (_int, [ctypes.POINTER(_vp), _int, _vp, _int, _int, _i64, _int]),
+    "ebv_dist_local_blocks": (_int, [_i64, _i64, _int, _int, _int, _vp, _i64, ctypes.POINTER(_i64),
+                                     ctypes.POINTER(_i64)]),
+    "ebv_lu_factor_dist": (_int, [_vp, _i64, _vp, _i64, _d, _vp, _vp]),
+    "ebv_lu_solve_dist": (_int, [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp]),
+    "ebv_lu_factor_dist_emulated": (_int, [_vp, _i64, _int, _i64, _int, _vp, _i64, _d, _vp, _vp]),
+    "ebv_lu_solve_dist_emulated": (_int, [_vp, _i64, _int, _i64, _int, _vp, _i64, _vp, _i64, _i64, _vp]),
     "ebv_plan_owner_map": (_int, [_i64, _i64, _vp]),
     "ebv_plan_units": (_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "ebv_block_owner": (_i64, [_i64, _i64, _i64, _int]),
@@ -176,6 +184,73 @@ def ebv_block_owner(J, N, nranks, layout=EBV_LAYOUT_CYCLIC) -> int:
 
 def ebv_launch_count(ctx) -> int:
     return lib().ebv_launch_count(ctx)
+
+
+def load_nccl():
+    """Make the NCCL that torch ships visible to libebv's dlopen (global)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    for d in (spec.submodule_search_locations if spec else []) or []:
+        p = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(p):
+            os.environ.setdefault("EBV_NCCL_LIB", p)
+            ctypes.CDLL(p, mode=ctypes.RTLD_GLOBAL)
+            return p
+    return None
+
+
+def ebv_get_unique_id() -> bytes:
+    load_nccl()
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().ebv_get_unique_id(buf), "ebv_get_unique_id")
+    return buf.raw
+
+
+def ebv_create_dist(device: int, uid: bytes, rank: int, nranks: int, nb: int = 256,
+                    layout: int = EBV_LAYOUT_CYCLIC) -> int:
+    load_nccl()
+    h = _vp()
+    _check(lib().ebv_create_dist(ctypes.byref(h), device, ctypes.create_string_buffer(uid, 128), rank, nranks,
+                                 nb, layout), "ebv_create_dist")
+    return h.value
+
+
+def ebv_dist_local_blocks(n: int, nb: int, rank: int, nranks: int, layout: int = EBV_LAYOUT_CYCLIC):
+    """(blocks owned by `rank` in ascending order, local slab width)."""
+    nbk, cols = _i64(), _i64()
+    _check(lib().ebv_dist_local_blocks(n, nb, rank, nranks, layout, None, 0, ctypes.byref(nbk),
+                                       ctypes.byref(cols)), "ebv_dist_local_blocks")
+    arr = (ctypes.c_int64 * max(nbk.value, 1))()
+    _check(lib().ebv_dist_local_blocks(n, nb, rank, nranks, layout, arr, nbk.value, ctypes.byref(nbk),
+                                       ctypes.byref(cols)), "ebv_dist_local_blocks")
+    return list(arr)[: nbk.value], cols.value
+
+
+def dist_local_columns(n: int, nb: int, rank: int, nranks: int, layout: int = EBV_LAYOUT_CYCLIC):
+    """Global column indices of rank's slab, in slab order."""
+    blocks, _ = ebv_dist_local_blocks(n, nb, rank, nranks, layout)
+    cols = []
+    for J in blocks:
+        cols.extend(range(J * nb, min(n, (J + 1) * nb)))
+    return cols
+
+
+def ebv_lu_factor_dist(ctx, n, A_local, lda, tau, d_info, stream):
+    return lib().ebv_lu_factor_dist(ctx, n, A_local, lda, tau, d_info, stream)
+
+
+def ebv_lu_solve_dist(ctx, n, LU_local, lda, B, ldb, nrhs, stream):
+    return lib().ebv_lu_solve_dist(ctx, n, LU_local, lda, B, ldb, nrhs, stream)
+
+
+def ebv_lu_factor_dist_emulated(ctx, n, nranks, nb, layout, slab_ptrs, lda, tau, d_info, stream):
+    arr = (ctypes.c_void_p * nranks)(*slab_ptrs)
+    return lib().ebv_lu_factor_dist_emulated(ctx, n, nranks, nb, layout, arr, lda, tau, d_info, stream)
+
+
+def ebv_lu_solve_dist_emulated(ctx, n, nranks, nb, layout, slab_ptrs, lda, B, ldb, nrhs, stream):
+    arr = (ctypes.c_void_p * nranks)(*slab_ptrs)
+    return lib().ebv_lu_solve_dist_emulated(ctx, n, nranks, nb, layout, arr, lda, B, ldb, nrhs, stream)
 
 
 # ------------------------------------------------------------------ tensor helpers

@@ -18,6 +18,23 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-li
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"]
 
 
+def nccl_include() -> str:
+    """nccl.h of the NCCL that torch ships (types only: libnccl.so.2 is
+    dlopen'ed at run time, never linked)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec and spec.submodule_search_locations:
+        for d in spec.submodule_search_locations:
+            inc = os.path.join(d, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    raise RuntimeError("nccl.h not found (nvidia-nccl wheel)")
+
+
+def nccl_library() -> str:
+    return os.path.join(os.path.dirname(nccl_include()), "lib", "libnccl.so.2")
+
+
 def _sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -40,7 +57,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def one(src):
         obj = os.path.join(OBJ, os.path.basename(src) + ".o")
-        cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, *FLAGS, "-I", nccl_include(), "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
@@ -51,7 +68,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         objs = list(ex.map(one, _sources()))
     tmp = LIB + ".tmp"
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", tmp, *objs]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", tmp, *objs,
+           "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

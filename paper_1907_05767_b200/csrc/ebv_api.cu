@@ -15,38 +15,7 @@
 #include <string>
 #include <vector>
 
-#include "ebv_internal.cuh"
-
-struct ebv_context {
-  int device = 0;
-  ebv_path_t path = EBV_PATH_AUTO;
-  int64_t leaf = 64;
-  int64_t nb = 256;         // right-looking block width; -1 = fully recursive schedule
-  double* d_tau = nullptr;
-  unsigned long long* d_norm = nullptr;
-  double* d_scratch = nullptr;
-  int* d_ticket = nullptr;
-  int* d_flags = nullptr;
-  int64_t flags_cap = 0;
-  int* d_vflags = nullptr;
-  int64_t vflags_cap = 0;
-  int64_t solve_epoch = 0;
-  int64_t launches = 0;
-  int vector_ctas = 0;      // 0 = auto; < 0 = cyclic map with |value| CTAs (for comparison)
-  bool lookahead = true;    // factor panel K+1 on a side stream under the update of step K
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_start = nullptr, ev_a = nullptr, ev_p = nullptr;
-  bool stats = false;
-  struct Rec {
-    int cls;
-    cudaEvent_t e0, e1;
-    double flops, bytes;
-  };
-  std::vector<Rec> recs;
-  std::vector<cudaEvent_t> pool;
-  int64_t st_launch[EBV_NUM_KCLASSES] = {0};
-  double st_ms[EBV_NUM_KCLASSES] = {0}, st_flops[EBV_NUM_KCLASSES] = {0}, st_bytes[EBV_NUM_KCLASSES] = {0};
-};
+#include "ebv_sched.cuh"
 
 namespace ebv {
 namespace {
@@ -56,21 +25,11 @@ void set_error(const std::string& msg) { g_last_error = msg; }
 }  // namespace ebv
 
 using namespace ebv;
+using namespace ebv::sched;
 
-namespace {
+namespace ebv {
+namespace sched {
 
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    cudaGetDevice(&cur);
-    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-  }
-};
 
 ebv_status_t cuda_fail(cudaError_t e, const char* where) {
   set_error(std::string(where) + ": " + cudaGetErrorString(e));
@@ -90,20 +49,6 @@ cudaEvent_t get_event(ebv_context* c) {
   }
   cudaEvent_t e;
   cudaEventCreate(&e);
-  return e;
-}
-
-// Launch wrapper: counts launches and (when enabled) brackets the launch with
-// CUDA events on the launching stream for the per-class statistics.
-template <class F>
-cudaError_t timed(ebv_context* c, int cls, double flops, double bytes, cudaStream_t s, int nlaunch, F&& f) {
-  c->launches += nlaunch;
-  if (!c->stats) return f();
-  ebv_context::Rec r{cls, get_event(c), get_event(c), flops, bytes};
-  cudaEventRecord(r.e0, s);
-  cudaError_t e = f();
-  cudaEventRecord(r.e1, s);
-  c->recs.push_back(r);
   return e;
 }
 
@@ -151,6 +96,24 @@ cudaError_t trsm_l(ebv_context* c, int64_t k, int64_t m, const double* L, int64_
   e = gemm(c, k - h, m, h, L + h, ldl, X, ldx, X + h, ldx, false, s);
   if (e != cudaSuccess) return e;
   return trsm_l(c, k - h, m, L + h + h * ldl, ldl, X + h, ldx, s);
+}
+
+// X (k x m) <- U^-1 X, U upper (non-unit) k x k: backward substitution per
+// column, k descending (the bottom block first, then the rows above it are
+// updated by a reverse-k DMMA update).
+cudaError_t trsm_lu(ebv_context* c, int64_t k, int64_t m, const double* U, int64_t ldu, double* X, int64_t ldx,
+                    cudaStream_t s) {
+  if (m <= 0 || k <= 0) return cudaSuccess;
+  if (k <= c->leaf) {
+    double fl = (double)m * k * k, by = 16.0 * m * k + 8.0 * k * k / 2;
+    return timed(c, KC_TRSM, fl, by, s, 1, [&] { return launch_trsm_left_upper(k, m, U, ldu, X, ldx, s); });
+  }
+  int64_t h = split_point(k, c->leaf);
+  cudaError_t e = trsm_lu(c, k - h, m, U + h + h * ldu, ldu, X + h, ldx, s);
+  if (e != cudaSuccess) return e;
+  e = gemm(c, h, m, k - h, U + h * ldu, ldu, X + h, ldx, X, ldx, true, s);
+  if (e != cudaSuccess) return e;
+  return trsm_lu(c, h, m, U, ldu, X, ldx, s);
 }
 
 // Fully recursive schedule (EBV_BLOCK_RECURSIVE):
@@ -258,6 +221,11 @@ cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_
   return e;
 }
 
+}  // namespace sched
+}  // namespace ebv
+
+namespace {
+
 ebv_status_t ensure_flags(ebv_context* c, int64_t need) {
   if (need <= c->flags_cap) return EBV_SUCCESS;
   if (c->d_flags) cudaFree(c->d_flags);
@@ -334,6 +302,7 @@ ebv_status_t ebv_create(ebv_context_t* ctx, int device) {
 ebv_status_t ebv_destroy(ebv_context_t c) {
   if (!c) return invalid("ebv_destroy: NULL");
   DeviceGuard g(c->device);
+  dist_release(c);
   for (auto& r : c->recs) { cudaEventDestroy(r.e0); cudaEventDestroy(r.e1); }
   for (auto e : c->pool) cudaEventDestroy(e);
   if (c->d_flags) cudaFree(c->d_flags);

@@ -1,0 +1,415 @@
+// ebv_dist.cu — the multi-GPU schedule: one large
+// system factored over P GPUs with a 1D block-cyclic column layout and an
+// NCCL broadcast of each factored panel over NVLink / NVSwitch; the solve is
+// a ring that carries the right-hand side through the block owners in order.
+//
+// Paper: the method is "convenient for ... multi devices"; the
+// per-step structure is Eq 6 in block form.  For a fixed block
+// width nb every entry sees exactly the operation sequence of the one-GPU
+// blocked schedule (panel LU, U12 substitution, DMMA update with k ascending),
+// so the factors and the solution are bitwise identical for every P and
+// equal to the serial oracle.
+//
+// Step K (owner = ebv_block_owner(K, N, P, layout)):
+//   owner   : panel LU of its block K (rows K*nb..n) in place, pack the panel
+//             (L11\U11 over L21, contiguous M x w) into the panel buffer
+//   all     : ncclBroadcast of the panel buffer from the owner (in place)
+//   all     : U12 = L11^-1 A12 and A22 -= L21 U12 on their local blocks J > K
+//             (a contiguous suffix of the local slab: blocks are stored in
+//             ascending J)
+// Solve, forward (K ascending) then backward (K descending): owner(K) solves
+// its diagonal block against the current right-hand side, applies its block
+// column to the rows below (above, with the reverse-k update), and passes
+// the right-hand side to owner(K+1) (owner(K-1)) with ncclSend / ncclRecv;
+// the result is broadcast from owner(0).
+//
+// The same driver runs in an emulation mode: one process, one GPU, all P
+// virtual ranks' slabs; the "broadcast" is the shared panel buffer and the
+// ring is the shared right-hand side.  It validates the multi-rank schedule
+// (ownership, local offsets, packing) bitwise on a single GPU.
+//
+// NCCL is loaded at run time (dlopen of libnccl.so.2, the copy torch ships),
+// so libebv.so has no link-time NCCL dependency.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "ebv_sched.cuh"
+
+using namespace ebv;
+using namespace ebv::sched;
+
+namespace {
+
+struct NcclApi {
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclBroadcast) Broadcast = nullptr;
+  decltype(&ncclAllReduce) AllReduce = nullptr;
+  decltype(&ncclSend) Send = nullptr;
+  decltype(&ncclRecv) Recv = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+  bool ok = false;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* env = getenv("EBV_NCCL_LIB");
+    void* h = nullptr;
+    if (env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+#define EBV_SYM(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(h, "nccl" #f))
+    EBV_SYM(GetUniqueId);
+    EBV_SYM(CommInitRank);
+    EBV_SYM(CommDestroy);
+    EBV_SYM(Broadcast);
+    EBV_SYM(AllReduce);
+    EBV_SYM(Send);
+    EBV_SYM(Recv);
+    EBV_SYM(GetErrorString);
+#undef EBV_SYM
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Broadcast && api.AllReduce &&
+             api.Send && api.Recv;
+  });
+  return api;
+}
+
+ebv_status_t nccl_fail(ncclResult_t r, const char* where) {
+  const char* m = nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error";
+  set_error(std::string(where) + ": " + m);
+  return EBV_ERR_NCCL;
+}
+
+// local column blocks of `rank` in ascending J, their slab offsets and widths
+struct Plan {
+  int64_t n = 0, nb = 0, N = 0;
+  int P = 1, rank = 0;
+  ebv_layout_t layout = EBV_LAYOUT_CYCLIC;
+  std::vector<int64_t> blocks, off;   // local block list and local column offsets
+  std::vector<int64_t> loc;           // global J -> local offset or -1
+  int64_t cols = 0;
+  int64_t width(int64_t J) const { return (J + 1) * nb <= n ? nb : n - J * nb; }
+  int64_t owner(int64_t J) const { return ebv_block_owner(J, N, P, layout); }
+};
+
+Plan make_plan(int64_t n, int64_t nb, int rank, int P, ebv_layout_t layout) {
+  Plan p;
+  p.n = n; p.nb = nb; p.P = P; p.rank = rank; p.layout = layout;
+  p.N = (n + nb - 1) / nb;
+  p.loc.assign(p.N, -1);
+  for (int64_t J = 0; J < p.N; J++)
+    if (p.owner(J) == rank) {
+      p.blocks.push_back(J);
+      p.off.push_back(p.cols);
+      p.loc[J] = p.cols;
+      p.cols += p.width(J);
+    }
+  return p;
+}
+
+// first local column of a block J' > K, or cols
+int64_t suffix_after(const Plan& p, int64_t K) {
+  for (size_t b = 0; b < p.blocks.size(); b++)
+    if (p.blocks[b] > K) return p.off[b];
+  return p.cols;
+}
+
+struct View {
+  Plan plan;
+  double* A;
+  int64_t lda;
+};
+
+__global__ void info_to_min_kernel(int64_t* info) {
+  if (*info == 0) *info = INT64_MAX;
+}
+__global__ void info_from_min_kernel(int64_t* info) {
+  if (*info == INT64_MAX) *info = 0;
+}
+
+}  // namespace
+
+struct ebv_dist_state {
+  int rank = 0, nranks = 1;
+  int64_t nb = 256;
+  ebv_layout_t layout = EBV_LAYOUT_CYCLIC;
+  ncclComm_t comm = nullptr;
+  double* pbuf = nullptr;
+  size_t pcap = 0;
+};
+
+namespace {
+
+ebv_status_t ensure_pbuf(ebv_context* c, ebv_dist_state* d, size_t elems) {
+  if (elems <= d->pcap) return EBV_SUCCESS;
+  if (d->pbuf) cudaFree(d->pbuf);
+  d->pbuf = nullptr;
+  d->pcap = 0;
+  cudaError_t e = cudaMalloc(&d->pbuf, elems * sizeof(double));
+  if (e != cudaSuccess) { set_error("panel buffer alloc failed"); return EBV_ERR_ALLOC; }
+  d->pcap = elems;
+  (void)c;
+  return EBV_SUCCESS;
+}
+
+// The schedule over the views this process drives (one real rank, or all P
+// virtual ranks in emulation).  comm == nullptr means emulation.
+ebv_status_t dist_factor(ebv_context* c, ebv_dist_state* d, std::vector<View>& views, int64_t n, int64_t* info,
+                         cudaStream_t s) {
+  const Plan& p0 = views[0].plan;
+  const int64_t nb = p0.nb;
+  ebv_status_t st = ensure_pbuf(c, d, (size_t)n * nb);
+  if (st != EBV_SUCCESS) return st;
+  cudaError_t e = cudaSuccess;
+  for (int64_t K = 0; K < p0.N; K++) {
+    const int64_t c0 = K * nb, w = p0.width(K), M = n - c0;
+    const int64_t owner = p0.owner(K);
+    for (auto& v : views) {
+      if (v.plan.rank != owner) continue;
+      double* P = v.A + c0 + v.plan.loc[K] * v.lda;
+      e = panel_rec(c, M, w, P, v.lda, c0, info, s);
+      if (e != cudaSuccess) return cuda_fail(e, "dist panel");
+      e = cudaMemcpy2DAsync(d->pbuf, M * sizeof(double), P, v.lda * sizeof(double), M * sizeof(double), w,
+                            cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return cuda_fail(e, "dist pack");
+    }
+    if (d->comm && d->nranks > 1) {
+      ncclResult_t r = nccl().Broadcast(d->pbuf, d->pbuf, (size_t)(M * w), ncclFloat64, (int)owner, d->comm, s);
+      if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(panel)");
+      c->launches += 1;
+    }
+    for (auto& v : views) {
+      const int64_t lc0 = suffix_after(v.plan, K);
+      const int64_t ncols = v.plan.cols - lc0;
+      if (ncols <= 0 || M - w < 0) continue;
+      double* X = v.A + c0 + lc0 * v.lda;
+      e = trsm_l(c, w, ncols, d->pbuf, M, X, v.lda, s);                                 // U12 = L11^-1 A12
+      if (e == cudaSuccess) e = gemm(c, M - w, ncols, w, d->pbuf + w, M, X, v.lda, X + w, v.lda, false, s);
+      if (e != cudaSuccess) return cuda_fail(e, "dist update");
+    }
+  }
+  if (d->comm && d->nranks > 1) {
+    // first failing step over all owners: min over nonzero info words
+    info_to_min_kernel<<<1, 1, 0, s>>>(info);
+    ncclResult_t r = nccl().AllReduce(info, info, 1, ncclInt64, ncclMin, d->comm, s);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce(info)");
+    info_from_min_kernel<<<1, 1, 0, s>>>(info);
+    c->launches += 3;
+  }
+  return EBV_SUCCESS;
+}
+
+ebv_status_t dist_solve(ebv_context* c, ebv_dist_state* d, std::vector<View>& views, int64_t n, double* B,
+                        int64_t ldb, int64_t nrhs, cudaStream_t s) {
+  const Plan& p0 = views[0].plan;
+  const int64_t nb = p0.nb, N = p0.N;
+  const bool real = d->comm && d->nranks > 1;
+  const size_t cnt = (size_t)(ldb * (nrhs - 1) + n);
+  auto find = [&](int64_t J) -> View* {
+    for (auto& v : views)
+      if (v.plan.rank == p0.owner(J)) return &v;
+    return nullptr;
+  };
+  cudaError_t e = cudaSuccess;
+  ncclResult_t r = ncclSuccess;
+  // forward: LY = B, blocks ascending
+  for (int64_t K = 0; K < N; K++) {
+    View* v = find(K);
+    if (!v) continue;
+    const int64_t c0 = K * nb, w = p0.width(K);
+    if (real && K > 0 && p0.owner(K - 1) != v->plan.rank) {
+      r = nccl().Recv(B, cnt, ncclFloat64, (int)p0.owner(K - 1), d->comm, s);
+      if (r != ncclSuccess) return nccl_fail(r, "ncclRecv(fwd)");
+    }
+    const double* Lk = v->A + v->plan.loc[K] * v->lda;
+    e = trsm_l(c, w, nrhs, Lk + c0, v->lda, B + c0, ldb, s);
+    if (e == cudaSuccess) e = gemm(c, n - c0 - w, nrhs, w, Lk + c0 + w, v->lda, B + c0, ldb, B + c0 + w, ldb, false, s);
+    if (e != cudaSuccess) return cuda_fail(e, "dist forward");
+    if (real && K + 1 < N && p0.owner(K + 1) != v->plan.rank) {
+      r = nccl().Send(B, cnt, ncclFloat64, (int)p0.owner(K + 1), d->comm, s);
+      if (r != ncclSuccess) return nccl_fail(r, "ncclSend(fwd)");
+    }
+  }
+  // backward: UX = Y, blocks descending
+  for (int64_t K = N - 1; K >= 0; K--) {
+    View* v = find(K);
+    if (!v) continue;
+    const int64_t c0 = K * nb, w = p0.width(K);
+    if (real && K + 1 < N && p0.owner(K + 1) != v->plan.rank) {
+      r = nccl().Recv(B, cnt, ncclFloat64, (int)p0.owner(K + 1), d->comm, s);
+      if (r != ncclSuccess) return nccl_fail(r, "ncclRecv(bwd)");
+    }
+    const double* Uk = v->A + v->plan.loc[K] * v->lda;
+    e = trsm_lu(c, w, nrhs, Uk + c0, v->lda, B + c0, ldb, s);
+    if (e == cudaSuccess && c0 > 0) e = gemm(c, c0, nrhs, w, Uk, v->lda, B + c0, ldb, B, ldb, true, s);
+    if (e != cudaSuccess) return cuda_fail(e, "dist backward");
+    if (real && K > 0 && p0.owner(K - 1) != v->plan.rank) {
+      r = nccl().Send(B, cnt, ncclFloat64, (int)p0.owner(K - 1), d->comm, s);
+      if (r != ncclSuccess) return nccl_fail(r, "ncclSend(bwd)");
+    }
+  }
+  if (real) {
+    r = nccl().Broadcast(B, B, cnt, ncclFloat64, (int)p0.owner(0), d->comm, s);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(x)");
+  }
+  return EBV_SUCCESS;
+}
+
+ebv_status_t check_common(ebv_context* c, int64_t n, int64_t lda, double tau, int P) {
+  if (!c) return invalid("dist: NULL ctx");
+  if (n < 0 || P < 1) return invalid("dist: bad size");
+  if (lda < (n > 1 ? n : 1)) return invalid("dist: lda < n");
+  if (tau < 0) {
+    set_error("dist: the default pivot floor (tau < 0) needs a global norm; pass tau >= 0");
+    return EBV_ERR_NOT_SUPPORTED;
+  }
+  return EBV_SUCCESS;
+}
+
+}  // namespace
+
+namespace ebv {
+namespace sched {
+void dist_release(ebv_context* c) {   // called by ebv_destroy
+  if (!c || !c->dist) return;
+  if (c->dist->comm && nccl().ok) nccl().CommDestroy(c->dist->comm);
+  if (c->dist->pbuf) cudaFree(c->dist->pbuf);
+  delete c->dist;
+  c->dist = nullptr;
+}
+}  // namespace sched
+}  // namespace ebv
+
+extern "C" {
+
+ebv_status_t ebv_get_unique_id(void* uid) {
+  if (!uid) return invalid("ebv_get_unique_id: NULL");
+  if (!nccl().ok) { set_error("libnccl.so.2 could not be loaded"); return EBV_ERR_NCCL; }
+  ncclUniqueId id;
+  ncclResult_t r = nccl().GetUniqueId(&id);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+  memcpy(uid, &id, sizeof(id));
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_create_dist(ebv_context_t* ctx, int device, const void* uid, int rank, int nranks, int64_t nb,
+                             ebv_layout_t layout) {
+  if (!ctx || !uid || nranks < 1 || rank < 0 || rank >= nranks) return invalid("ebv_create_dist: bad arguments");
+  if (nb <= 0 || nb % 64) return invalid("ebv_create_dist: nb must be a positive multiple of 64");
+  if (layout != EBV_LAYOUT_CYCLIC && layout != EBV_LAYOUT_EBVPAIR && layout != EBV_LAYOUT_SNAKE)
+    return invalid("ebv_create_dist: bad layout");
+  if (!nccl().ok) { set_error("libnccl.so.2 could not be loaded"); return EBV_ERR_NCCL; }
+  ebv_status_t st = ebv_create(ctx, device);
+  if (st != EBV_SUCCESS) return st;
+  DeviceGuard g(device);
+  ebv_dist_state* d = new ebv_dist_state();
+  d->rank = rank; d->nranks = nranks; d->nb = nb; d->layout = layout;
+  ncclUniqueId id;
+  memcpy(&id, uid, sizeof(id));
+  ncclResult_t r = nccl().CommInitRank(&d->comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    delete d;
+    ebv_destroy(*ctx);
+    *ctx = nullptr;
+    return nccl_fail(r, "ncclCommInitRank");
+  }
+  (*ctx)->dist = d;
+  (*ctx)->nb = nb;
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_dist_local_blocks(int64_t n, int64_t nb, int rank, int nranks, ebv_layout_t layout, int64_t* blocks,
+                                   int64_t cap, int64_t* nblocks, int64_t* local_cols) {
+  if (n < 0 || nb <= 0 || nranks < 1 || rank < 0 || rank >= nranks || !nblocks || !local_cols)
+    return invalid("ebv_dist_local_blocks: bad arguments");
+  Plan p = make_plan(n, nb, rank, nranks, layout);
+  *nblocks = (int64_t)p.blocks.size();
+  *local_cols = p.cols;
+  if (blocks) {
+    if (cap < (int64_t)p.blocks.size()) return invalid("ebv_dist_local_blocks: cap too small");
+    for (size_t i = 0; i < p.blocks.size(); i++) blocks[i] = p.blocks[i];
+  }
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_lu_factor_dist(ebv_context_t c, int64_t n, double* A_local, int64_t lda, double tau, int64_t* d_info,
+                                void* stream) {
+  if (!c || !c->dist) return invalid("ebv_lu_factor_dist: not a distributed context");
+  ebv_dist_state* d = c->dist;
+  ebv_status_t st = check_common(c, n, lda, tau, d->nranks);
+  if (st != EBV_SUCCESS) return st;
+  if (!d_info) return invalid("ebv_lu_factor_dist: d_info NULL");
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = launch_set_info0(d_info, s);
+  if (e == cudaSuccess) e = launch_tau(n, nullptr, lda, tau, c->d_tau, c->d_norm, s);
+  if (e != cudaSuccess) return cuda_fail(e, "dist init");
+  c->launches += 2;
+  if (n == 0) return EBV_SUCCESS;
+  std::vector<View> views{View{make_plan(n, d->nb, d->rank, d->nranks, d->layout), A_local, lda}};
+  if (views[0].plan.cols > 0 && !A_local) return invalid("ebv_lu_factor_dist: A_local NULL");
+  return dist_factor(c, d, views, n, d_info, s);
+}
+
+ebv_status_t ebv_lu_solve_dist(ebv_context_t c, int64_t n, const double* LU_local, int64_t lda, double* B, int64_t ldb,
+                               int64_t nrhs, void* stream) {
+  if (!c || !c->dist) return invalid("ebv_lu_solve_dist: not a distributed context");
+  ebv_dist_state* d = c->dist;
+  ebv_status_t st = check_common(c, n, lda, 0.0, d->nranks);
+  if (st != EBV_SUCCESS) return st;
+  if (nrhs < 0 || ldb < (n > 1 ? n : 1)) return invalid("ebv_lu_solve_dist: bad B");
+  if (n == 0 || nrhs == 0) return EBV_SUCCESS;
+  if (!B) return invalid("ebv_lu_solve_dist: B NULL");
+  DeviceGuard g(c->device);
+  std::vector<View> views{View{make_plan(n, d->nb, d->rank, d->nranks, d->layout), const_cast<double*>(LU_local), lda}};
+  return dist_solve(c, d, views, n, B, ldb, nrhs, (cudaStream_t)stream);
+}
+
+ebv_status_t ebv_lu_factor_dist_emulated(ebv_context_t c, int64_t n, int nranks, int64_t nb, ebv_layout_t layout,
+                                         double* const* slabs, int64_t lda, double tau, int64_t* d_info, void* stream) {
+  ebv_status_t st = check_common(c, n, lda, tau, nranks);
+  if (st != EBV_SUCCESS) return st;
+  if (nb <= 0 || nb % 64) return invalid("emulated: nb must be a positive multiple of 64");
+  if (!d_info || (n > 0 && !slabs)) return invalid("emulated: NULL pointer");
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = launch_set_info0(d_info, s);
+  if (e == cudaSuccess) e = launch_tau(n, nullptr, lda, tau, c->d_tau, c->d_norm, s);
+  if (e != cudaSuccess) return cuda_fail(e, "emulated init");
+  if (n == 0) return EBV_SUCCESS;
+  ebv_dist_state tmp;
+  tmp.nranks = nranks; tmp.nb = nb; tmp.layout = layout;
+  std::vector<View> views;
+  for (int r = 0; r < nranks; r++) views.push_back(View{make_plan(n, nb, r, nranks, layout), slabs[r], lda});
+  st = dist_factor(c, &tmp, views, n, d_info, s);
+  cudaStreamSynchronize(s);   // the temporary panel buffer dies with tmp
+  if (tmp.pbuf) cudaFree(tmp.pbuf);
+  return st;
+}
+
+ebv_status_t ebv_lu_solve_dist_emulated(ebv_context_t c, int64_t n, int nranks, int64_t nb, ebv_layout_t layout,
+                                        double* const* slabs, int64_t lda, double* B, int64_t ldb, int64_t nrhs,
+                                        void* stream) {
+  ebv_status_t st = check_common(c, n, lda, 0.0, nranks);
+  if (st != EBV_SUCCESS) return st;
+  if (nb <= 0 || nb % 64) return invalid("emulated: nb must be a positive multiple of 64");
+  if (nrhs < 0 || ldb < (n > 1 ? n : 1)) return invalid("emulated: bad B");
+  if (n == 0 || nrhs == 0) return EBV_SUCCESS;
+  if (!B || !slabs) return invalid("emulated: NULL pointer");
+  DeviceGuard g(c->device);
+  ebv_dist_state tmp;
+  tmp.nranks = nranks; tmp.nb = nb; tmp.layout = layout;
+  std::vector<View> views;
+  for (int r = 0; r < nranks; r++) views.push_back(View{make_plan(n, nb, r, nranks, layout), slabs[r], lda});
+  return dist_solve(c, &tmp, views, n, B, ldb, nrhs, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -47,6 +47,11 @@ cudaError_t launch_trsm_right_upper(int64_t m, int64_t k, double* X, int64_t ldx
 cudaError_t launch_trsm_left_lower_unit(int64_t k, int64_t m, const double* L, int64_t ldl, double* X,
                                         int64_t ldx, cudaStream_t s);
 
+// X <- U^-1 X, U upper triangular non-unit k x k (k <= 64), X k x m:
+// column-parallel backward substitution, k descending.
+cudaError_t launch_trsm_left_upper(int64_t k, int64_t m, const double* U, int64_t ldu, double* X, int64_t ldx,
+                                   cudaStream_t s);
+
 // Forward (LY = B) then backward (UX = Y) wavefront substitution (Eq 1).
 cudaError_t launch_solve(int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb, int64_t nrhs,
                          int* ticket_ws, int* flags_ws, int64_t epoch, cudaStream_t s);

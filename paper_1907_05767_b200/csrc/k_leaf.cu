@@ -138,7 +138,46 @@ __global__ void __launch_bounds__(128) trsm_llu_kernel(int k, int64_t m, const d
   }
 }
 
+// ---------------------------------------------------------------- X = U11^-1 X
+// Backward substitution per column (thread per column), k descending:
+// x_p = x_p / u_pp, then x_i = fma(-u_ip, x_p, x_i) for i < p — the oracle's
+// backward order (Eq 1, UX = Y).  Padded rows (p >= k) are identity rows and
+// come first in the descending sweep: they change nothing.
+__global__ void __launch_bounds__(128) trsm_luu_kernel(int k, int64_t m, const double* __restrict__ U, int64_t ldu,
+                                                       double* __restrict__ X, int64_t ldx) {
+  __shared__ __align__(16) double sU[W * S];   // sU[p*S + i] = u(i, p), i <= p (column p of U)
+  for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
+    const int i = idx % W, p = idx / W;
+    sU[p * S + i] = (i < k && p < k) ? (i <= p ? U[i + (int64_t)p * ldu] : 0.0) : (i == p ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= m) return;
+  double* col = X + c * ldx;
+  double x[W];
+#pragma unroll
+  for (int r = 0; r < W; r++) x[r] = (r < k) ? col[r] : 0.0;
+#pragma unroll
+  for (int p = W - 1; p >= 0; p--) {
+    const double* up = sU + p * S;
+    x[p] = x[p] / up[p];
+#pragma unroll
+    for (int i = 0; i < p; i++) x[i] = fma(-up[i], x[p], x[i]);
+  }
+#pragma unroll
+  for (int r = 0; r < W; r++)
+    if (r < k) col[r] = x[r];
+}
+
 }  // namespace
+
+cudaError_t launch_trsm_left_upper(int64_t k, int64_t m, const double* U, int64_t ldu, double* X, int64_t ldx,
+                                   cudaStream_t s) {
+  if (m <= 0 || k <= 0) return cudaSuccess;
+  if (k > W) return cudaErrorInvalidValue;
+  trsm_luu_kernel<<<(unsigned)((m + 127) / 128), 128, 0, s>>>((int)k, m, U, ldu, X, ldx);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_leaf_lu(int64_t n, double* A, int64_t lda, const double* tau, int64_t* info, int64_t koff,
                            cudaStream_t s) {

@@ -1,0 +1,125 @@
+"""GPU: the 1D block-cyclic multi-GPU schedule.
+
+On one B200 the P-rank schedule runs in emulation (all virtual ranks' slabs
+in one process) and, for P = 1, through a real NCCL communicator.  Every
+result is compared BITWISE with the serial oracle and with the one-GPU
+blocked schedule of the same block width (the per-entry order does not
+depend on P)."""
+import numpy as np
+import pytest
+import torch
+
+import ebv_inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+ebv = pytest.importorskip("paper_1907_05767_b200")
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda:0")
+
+
+@pytest.fixture(scope="module")
+def ctx(dev):
+    return ebv.Context(0)
+
+
+def slabs_for(d, n, nb, P, layout, dev):
+    """Per-rank column-major slabs (storage (cols, n): row c = column c)."""
+    slabs, colmaps = [], []
+    for r in range(P):
+        cols = ebv.dist_local_columns(n, nb, r, P, layout)
+        st = d["At"][torch.tensor(cols, dtype=torch.long, device=dev)].clone() if cols else \
+            torch.zeros(1, n, dtype=torch.float64, device=dev)
+        slabs.append(st)
+        colmaps.append(cols)
+    return slabs, colmaps
+
+
+def assemble(slabs, colmaps, n):
+    full = np.zeros((n, n))
+    for st, cols in zip(slabs, colmaps):
+        if cols:
+            full[:, cols] = st[: len(cols)].T.cpu().numpy()
+    return full
+
+
+@pytest.mark.parametrize("P,nb,layout,n", [(1, 128, 0, 700), (2, 64, 0, 1000), (3, 128, 0, 1000), (4, 64, 1, 1537),
+                                           (8, 64, 2, 1000), (4, 256, 0, 2100), (2, 128, 1, 64), (8, 64, 0, 300)])
+def test_emulated_dist_factor_and_solve_bitwise(dev, ctx, P, nb, layout, n):
+    d = ebv_inputs.generate(n, seed=P * 1000 + nb + layout, nrhs=2, device=dev)
+    slabs, colmaps = slabs_for(d, n, nb, P, layout, dev)
+    info = torch.zeros((), dtype=torch.int64, device=dev)
+    sh = torch.cuda.current_stream().cuda_stream
+    st = ebv.ebv_lu_factor_dist_emulated(ctx.handle, n, P, nb, layout, [s.data_ptr() for s in slabs], n, 0.0,
+                                         info.data_ptr(), sh)
+    assert st == 0, ebv.ebv_last_error()
+    B = d["B"].T.clone(memory_format=torch.contiguous_format)   # (nrhs, n) = column-major n x nrhs
+    st = ebv.ebv_lu_solve_dist_emulated(ctx.handle, n, P, nb, layout, [s.data_ptr() for s in slabs], n,
+                                        B.data_ptr(), n, 2, sh)
+    assert st == 0, ebv.ebv_last_error()
+    torch.cuda.synchronize()
+    lu_g = assemble(slabs, colmaps, n)
+    lu_o, info_o = oracle.lu_factor(d["At"].T.cpu().numpy())
+    assert int(info) == info_o == 0
+    assert np.array_equal(lu_g, lu_o)
+    x_o = oracle.lu_solve(lu_o, d["B"].cpu().numpy())
+    assert np.array_equal(B.T.cpu().numpy(), x_o)
+    # the one-GPU blocked schedule with the same block width is the same computation
+    ctx.set_block(nb)
+    LU1, _ = ebv.lu_factor(d["At"].T, ctx=ctx)
+    ctx.set_block(0)
+    torch.cuda.synchronize()
+    assert np.array_equal(LU1.cpu().numpy(), lu_g)
+
+
+def test_emulated_dist_info(dev, ctx):
+    n, nb, P = 400, 64, 3
+    A = torch.eye(n, dtype=torch.float64, device=dev) * 3.0
+    A[200, 200] = 0.0
+    A[350, 350] = 0.0
+    d = {"At": A.T.contiguous()}
+    slabs, _ = slabs_for(d, n, nb, P, 0, dev)
+    info = torch.zeros((), dtype=torch.int64, device=dev)
+    st = ebv.ebv_lu_factor_dist_emulated(ctx.handle, n, P, nb, 0, [s.data_ptr() for s in slabs], n, 0.0,
+                                         info.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    assert st == 0
+    torch.cuda.synchronize()
+    assert int(info) == 201
+
+
+def test_real_nccl_single_rank(dev):
+    """ebv_create_dist + ebv_lu_factor_dist / ebv_lu_solve_dist through a real
+    NCCL communicator (1 rank on this GPU)."""
+    n, nb = 900, 128
+    uid = ebv.ebv_get_unique_id()
+    h = ebv.ebv_create_dist(0, uid, 0, 1, nb, 0)
+    try:
+        d = ebv_inputs.generate(n, seed=77, nrhs=1, device=dev)
+        slab = d["At"].clone()
+        info = torch.zeros((), dtype=torch.int64, device=dev)
+        sh = torch.cuda.current_stream().cuda_stream
+        assert ebv.ebv_lu_factor_dist(h, n, slab.data_ptr(), n, 0.0, info.data_ptr(), sh) == 0, ebv.ebv_last_error()
+        B = d["B"].T.clone(memory_format=torch.contiguous_format)
+        assert ebv.ebv_lu_solve_dist(h, n, slab.data_ptr(), n, B.data_ptr(), n, 1, sh) == 0, ebv.ebv_last_error()
+        torch.cuda.synchronize()
+        lu_o, _ = oracle.lu_factor(d["At"].T.cpu().numpy())
+        assert np.array_equal(slab.T.cpu().numpy(), lu_o)
+        assert np.array_equal(B.T.cpu().numpy(), oracle.lu_solve(lu_o, d["B"].cpu().numpy()))
+        assert int(info) == 0
+    finally:
+        ebv.ebv_destroy(h)
+
+
+def test_dist_errors(dev, ctx):
+    L = ebv.lib()
+    info = torch.zeros((), dtype=torch.int64, device=dev)
+    # not a distributed context
+    assert L.ebv_lu_factor_dist(ctx.handle, 4, None, 4, 0.0, info.data_ptr(), None) == 1
+    # default pivot floor is not available in the distributed schedule
+    st = ebv.ebv_lu_factor_dist_emulated(ctx.handle, 4, 2, 64, 0, [0, 0], 4, -1.0, info.data_ptr(), None)
+    assert st == 5
