@@ -21,120 +21,142 @@ namespace {
 constexpr int W = 64;        // block width
 constexpr int S = W + 2;     // smem row stride (doubles): 16-byte aligned rows
 
+// Work split used by the three kernels below: a group of G = 8 consecutive
+// lanes shares one row (or column) of the 64-wide block; lane j of the group
+// owns the entries c = j, j+8, ..., j+56.  Step p is carried out by the
+// owner lane of entry p (division or final value), the value is broadcast
+// to the group with a shuffle, and each lane applies the fma to its entries
+// c > p — per entry exactly the ascending-p chain of the oracle.
+constexpr int G = 8;          // lanes per row / column
+constexpr int Q = W / G;      // entries per lane
+
 // ---------------------------------------------------------------- leaf LU
-// The w x w block lives in shared memory (column-major, padded).  Warp v owns
-// the columns j = v, v+8, ...; lane l owns rows l and l+32.  Step k: the
-// owner warp of column k divides it below the diagonal (Eq 6-a, the L_(k)
-// vector); after a barrier every warp applies the rank-1 update (Eq 6-c) to
-// its columns j > k using the U_(k) entry a_kj (Eq 6-b).  A narrower block is
-// padded with an identity (exactly neutral).
-constexpr int LS = W + 1;
-__global__ void __launch_bounds__(256) leaf_lu_kernel(int w, double* __restrict__ A, int64_t lda,
-                                                      const double* __restrict__ tau, int64_t* info, int64_t koff) {
-  __shared__ double s[W * LS];   // s[j*LS + i] = a(i, j)
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int idx = tid; idx < W * W; idx += 256) {
-    const int i = idx % W, j = idx / W;
-    s[j * LS + i] = (i < w && j < w) ? A[i + (int64_t)j * lda] : (i == j ? 1.0 : 0.0);
+// 512 threads: row i of the block is owned by group i.  Step k: group k
+// publishes its final row (the U_(k) vector, Eq 6-b) to shared memory; every
+// row i > k forms l_ik = a_ik / u_kk (Eq 6-a, owner lane), broadcasts it in
+// the group and updates its row (Eq 6-c).  A narrower block is identity
+// padded (exactly neutral).
+__global__ void __launch_bounds__(W * G) leaf_lu_kernel(int w, double* __restrict__ A, int64_t lda,
+                                                        const double* __restrict__ tau, int64_t* info, int64_t koff) {
+  __shared__ __align__(16) double urow[2][W];
+  __shared__ int smin;
+  const int tid = threadIdx.x, i = tid / G, j = tid % G, lane = tid & 31, base = lane & ~(G - 1);
+  double a[Q];
+#pragma unroll
+  for (int q = 0; q < Q; q++) {
+    const int c = j + G * q;
+    a[q] = (i < w && c < w) ? A[i + (int64_t)c * lda] : (i == c ? 1.0 : 0.0);
+  }
+  if (tid == 0) smin = 0x7fffffff;
+  const double tv = *tau;
+#pragma unroll
+  for (int k = 0; k < W; k++) {
+    const int o = k % G, qk = k / G;
+    double* ur = urow[k & 1];
+    if (i == k) {
+#pragma unroll
+      for (int q = qk; q < Q; q++) ur[j + G * q] = a[q];
+    }
+    __syncthreads();
+    const double piv = ur[k];
+    if (tid == 0 && k < w && fabs(piv) <= tv) atomicMin(&smin, k + 1);
+    if (i > k && j == o) a[qk] = a[qk] / piv;
+    const double l = __shfl_sync(0xffffffffu, a[qk], base + o);
+    if (i > k) {
+#pragma unroll
+      for (int q = qk; q < Q; q++)
+        if (q > qk || j > o) a[q] = fma(-l, ur[j + G * q], a[q]);
+    }
   }
   __syncthreads();
-  const double tv = *tau;
-  int fail = 0;
-  for (int k = 0; k < W; k++) {
-    const double piv = s[k * LS + k];
-    if (tid == 0 && k < w && fabs(piv) <= tv && fail == 0) fail = k + 1;
-    if (warp == (k & 7)) {
-      double* ck = s + k * LS;
-      if (lane > k) ck[lane] = ck[lane] / piv;
-      if (lane + 32 > k) ck[lane + 32] = ck[lane + 32] / piv;
-    }
-    __syncthreads();
-    const double l0 = s[k * LS + lane], l1 = s[k * LS + lane + 32];
-    for (int j = k + 1 + ((warp - k - 1) & 7); j < W; j += 8) {
-      double* cj = s + j * LS;
-      const double u = cj[k];
-      if (lane > k) cj[lane] = fma(-l0, u, cj[lane]);
-      if (lane + 32 > k) cj[lane + 32] = fma(-l1, u, cj[lane + 32]);
-    }
-    __syncthreads();
-  }
-  if (tid == 0 && fail) {
+  if (tid == 0 && smin != 0x7fffffff) {
     volatile int64_t* vi = info;
-    if (*vi == 0) *vi = koff + fail;
+    if (*vi == 0) *vi = koff + smin;
   }
-  for (int idx = tid; idx < w * w; idx += 256) {
-    const int i = idx % w, j = idx / w;
-    A[i + (int64_t)j * lda] = s[j * LS + i];
+  if (i < w) {
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+      const int c = j + G * q;
+      if (c < w) A[i + (int64_t)c * lda] = a[q];
+    }
   }
 }
 
 // ---------------------------------------------------------------- L21 = A21 U11^-1
-// Thread per row; right-looking in registers: x_p /= u_pp, then
-// x_j = fma(-x_p, u_pj, x_j) for j > p — per entry: ascending p, division last.
-__global__ void __launch_bounds__(128) trsm_ru_kernel(int64_t m, int k, double* __restrict__ X, int64_t ldx,
+// Group per row: step p, the owner lane divides x_p by u_pp, broadcasts it,
+// every lane applies x_c = fma(-x_p, u_pc, x_c) to its entries c > p.
+__global__ void __launch_bounds__(256) trsm_ru_kernel(int64_t m, int k, double* __restrict__ X, int64_t ldx,
                                                       const double* __restrict__ U, int64_t ldu) {
-  __shared__ __align__(16) double sU[W * S];   // sU[p*S + j] = u(p, j)
+  __shared__ __align__(16) double sU[W * S];   // sU[p*S + c] = u(p, c), identity padded
   for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
-    const int p = idx % W, j = idx / W;          // consecutive p: coalesced column reads
-    sU[p * S + j] = (p < k && j < k) ? (p <= j ? U[p + (int64_t)j * ldu] : 0.0) : (p == j ? 1.0 : 0.0);
+    const int p = idx % W, c = idx / W;
+    sU[p * S + c] = (p < k && c < k) ? (p <= c ? U[p + (int64_t)c * ldu] : 0.0) : (p == c ? 1.0 : 0.0);
   }
   __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  double x[W];
+  const int tid = threadIdx.x, j = tid % G, lane = tid & 31, base = lane & ~(G - 1);
+  const int64_t i = (int64_t)blockIdx.x * (256 / G) + tid / G;
+  const bool rv = i < m;
+  double x[Q];
 #pragma unroll
-  for (int j = 0; j < W; j++) x[j] = (j < k) ? X[i + (int64_t)j * ldx] : 0.0;
-#pragma unroll
-  for (int p = 0; p < W; p++) {
-    const double* up = sU + p * S;
-    x[p] = x[p] / up[p];
-#pragma unroll
-    for (int j = p + 1; j < W; j++) x[j] = fma(-x[p], up[j], x[j]);
+  for (int q = 0; q < Q; q++) {
+    const int c = j + G * q;
+    x[q] = (rv && c < k) ? X[i + (int64_t)c * ldx] : 0.0;
   }
 #pragma unroll
-  for (int j = 0; j < W; j++)
-    if (j < k) X[i + (int64_t)j * ldx] = x[j];
+  for (int p = 0; p < W; p++) {
+    const int o = p % G, qp = p / G;
+    const double* up = sU + p * S;
+    if (j == o) x[qp] = x[qp] / up[p];
+    const double xp = __shfl_sync(0xffffffffu, x[qp], base + o);
+#pragma unroll
+    for (int q = qp; q < Q; q++)
+      if (q > qp || j > o) x[q] = fma(-xp, up[j + G * q], x[q]);
+  }
+  if (rv) {
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+      const int c = j + G * q;
+      if (c < k) X[i + (int64_t)c * ldx] = x[q];
+    }
+  }
 }
 
 // ---------------------------------------------------------------- U12 = L11^-1 A12
-// Thread per column; x_i = fma(-l_ip, x_p, x_i) for p ascending (unit
-// diagonal, no division).
-__global__ void __launch_bounds__(128) trsm_llu_kernel(int k, int64_t m, const double* __restrict__ L, int64_t ldl,
+// Group per column: step p, x_p is final (owner lane), broadcast; every lane
+// applies x_r = fma(-l_rp, x_p, x_r) to its rows r > p (unit diagonal).
+__global__ void __launch_bounds__(256) trsm_llu_kernel(int k, int64_t m, const double* __restrict__ L, int64_t ldl,
                                                        double* __restrict__ X, int64_t ldx) {
-  __shared__ __align__(16) double sL[W * S];   // sL[p*S + i] = l(i, p), i > p
+  __shared__ __align__(16) double sL[W * S];   // sL[p*S + r] = l(r, p), r > p
   for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
-    const int i = idx % W, p = idx / W;
-    sL[p * S + i] = (i > p && i < k) ? L[i + (int64_t)p * ldl] : 0.0;
+    const int r = idx % W, p = idx / W;
+    sL[p * S + r] = (r > p && r < k) ? L[r + (int64_t)p * ldl] : 0.0;
   }
   __syncthreads();
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= m) return;
-  double* col = X + c * ldx;
-  double x[W];
-  if (k == W && ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0)) {
+  const int tid = threadIdx.x, j = tid % G, lane = tid & 31, base = lane & ~(G - 1);
+  const int64_t cidx = (int64_t)blockIdx.x * (256 / G) + tid / G;
+  const bool cv = cidx < m;
+  double* col = X + (cv ? cidx : 0) * ldx;
+  double x[Q];
 #pragma unroll
-    for (int r = 0; r < W; r += 2) {
-      double2 v = *reinterpret_cast<const double2*>(col + r);
-      x[r] = v.x;
-      x[r + 1] = v.y;
-    }
-  } else {
-#pragma unroll
-    for (int r = 0; r < W; r++) x[r] = (r < k) ? col[r] : 0.0;
+  for (int q = 0; q < Q; q++) {
+    const int r = j + G * q;
+    x[q] = (cv && r < k) ? col[r] : 0.0;
   }
 #pragma unroll
   for (int p = 0; p < W; p++) {
+    const int o = p % G, qp = p / G;
     const double* lp = sL + p * S;
+    const double xp = __shfl_sync(0xffffffffu, x[qp], base + o);
 #pragma unroll
-    for (int i = p + 1; i < W; i++) x[i] = fma(-lp[i], x[p], x[i]);
+    for (int q = qp; q < Q; q++)
+      if (q > qp || j > o) x[q] = fma(-lp[j + G * q], xp, x[q]);
   }
-  if (k == W && ((ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0)) {
+  if (cv) {
 #pragma unroll
-    for (int r = 0; r < W; r += 2) *reinterpret_cast<double2*>(col + r) = make_double2(x[r], x[r + 1]);
-  } else {
-#pragma unroll
-    for (int r = 0; r < W; r++)
-      if (r < k) col[r] = x[r];
+    for (int q = 0; q < Q; q++) {
+      const int r = j + G * q;
+      if (r < k) col[r] = x[q];
+    }
   }
 }
 
@@ -183,7 +205,7 @@ cudaError_t launch_leaf_lu(int64_t n, double* A, int64_t lda, const double* tau,
                            cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   if (n > W) return cudaErrorInvalidValue;
-  leaf_lu_kernel<<<1, 256, 0, s>>>((int)n, A, lda, tau, info, koff);
+  leaf_lu_kernel<<<1, W * G, 0, s>>>((int)n, A, lda, tau, info, koff);
   return cudaGetLastError();
 }
 
@@ -191,7 +213,7 @@ cudaError_t launch_trsm_right_upper(int64_t m, int64_t k, double* X, int64_t ldx
                                     cudaStream_t s) {
   if (m <= 0 || k <= 0) return cudaSuccess;
   if (k > W) return cudaErrorInvalidValue;
-  trsm_ru_kernel<<<(unsigned)((m + 127) / 128), 128, 0, s>>>(m, (int)k, X, ldx, U, ldu);
+  trsm_ru_kernel<<<(unsigned)((m + 31) / 32), 256, 0, s>>>(m, (int)k, X, ldx, U, ldu);
   return cudaGetLastError();
 }
 
@@ -199,7 +221,7 @@ cudaError_t launch_trsm_left_lower_unit(int64_t k, int64_t m, const double* L, i
                                         int64_t ldx, cudaStream_t s) {
   if (m <= 0 || k <= 0) return cudaSuccess;
   if (k > W) return cudaErrorInvalidValue;
-  trsm_llu_kernel<<<(unsigned)((m + 127) / 128), 128, 0, s>>>((int)k, m, L, ldl, X, ldx);
+  trsm_llu_kernel<<<(unsigned)((m + 31) / 32), 256, 0, s>>>((int)k, m, L, ldl, X, ldx);
   return cudaGetLastError();
 }
 

@@ -29,13 +29,70 @@ constexpr int BR = 64;          // rows per block (= threads per CTA)
 constexpr int MAXR = 16;        // max right-hand sides per launch
 constexpr int TSTR = BR + 1;    // diagonal tile column stride in smem
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
+__device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+// Wait for a release flag: relaxed polls (no L1 invalidation per poll, which
+// an acquire load costs on sm_100a: CCTL.IVALL) with a short back-off, then
+// one acquire fence that orders the subsequent reads after the observed
+// release.
+__device__ __forceinline__ void wait_flag(const int* p, int v, bool next_in_chain) {
+  // only the block whose diagonal depends on this flag polls tightly; the
+  // others (accumulating further tiles) back off, keeping the flag's L2
+  // slice free for the release store on the critical path
+  const unsigned ns = next_in_chain ? 32 : 1000;
+  while (ld_relaxed(p) != v) __nanosleep(ns);
+  asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
 }
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+#ifdef EBV_SOLVE_TRACE
+// probes/solve_trace.cu: per-block phase timestamps (%globaltimer, ns)
+__device__ unsigned long long g_trace[2][8192][6];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define EBV_TR(slot)                                                     \
+  do {                                                                   \
+    if (i == 0 && I < 8192) g_trace[FORWARD ? 0 : 1][I][slot] = gtime(); \
+  } while (0)
+#else
+#define EBV_TR(slot) \
+  do {               \
+  } while (0)
+#endif
+
+// y / u from a precomputed reciprocal r = RN(1/u): q = RN(y r), one Newton
+// correction with the exact residual (the divisor-independent tail of the
+// hardware division sequence), so the chained step costs three dependent
+// FP64 ops instead of a full division.  The owner lane verifies that q is
+// the correctly rounded quotient: with rr = y - q u (exact), the true
+// quotient is q + rr/u, and q = RN(y/u) iff |rr| < |u| ulp(q)/2 — or
+// |u| ulp(q)/4 when q is a power of two and the quotient lies below it;
+// ties and non-normal q count as unverified.  The caller redoes the block
+// with true division if any step is unverified, so the result is always
+// RN(y/u), bitwise the oracle's division.
+__device__ __forceinline__ double quot(double y, double u, double r, bool own, bool& ok) {
+  const double q0 = y * r;
+  const double q = fma(r, fma(-u, q0, y), q0);
+  if (own) {
+    const double rr = fma(-u, q, y);                               // exact remainder y - q u
+    const long long qb = __double_as_longlong(q);
+    const long long e = qb & 0x7ff0000000000000LL;
+    const bool normal = e > (54LL << 52) && e < (0x7feLL << 52);
+    double lim = fabs(u) * __longlong_as_double(e - (53LL << 52));   // |u| ulp(q) / 2, exact
+    const bool below = (rr < 0.0) != (u < 0.0);                      // true quotient < |q| side
+    const bool pow2 = (qb & 0x000fffffffffffffLL) == 0;
+    if (pow2 && below == (q > 0.0)) lim *= 0.5;                      // toward zero from 2^e
+    ok = ok && normal && fabs(rr) < lim;
+  }
+  return q;
 }
 
 template <bool FORWARD, int NR>
@@ -60,6 +117,7 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
     const int64_t I = FORWARD ? t : NB - 1 - t;
     const int64_t row = I * BR + i;
     const bool rv = row < n;
+    EBV_TR(0);
 
     // stage the diagonal tile (read-only: no dependence on other blocks)
     for (int c = 0; c < BR; c++) {
@@ -78,8 +136,12 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
       const double* src = LU + (rv ? row : 0) + (J * BR) * lda;
 #pragma unroll
       for (int k = 0; k < BR; k++) l[k] = (rv && J * BR + k < n) ? __ldg(src + k * lda) : 0.0;
-      if (i == 0) {
-        while (ld_acquire(flags + J) != epoch) __nanosleep(20);
+      if (jj + 1 == nJ) {
+        EBV_TR(1);
+      }
+      if (i == 0) wait_flag(flags + J, epoch, jj + 1 == nJ);
+      if (jj + 1 == nJ) {
+        EBV_TR(2);
       }
       __syncthreads();
       for (int idx = i; idx < BR * nr; idx += BR) {
@@ -103,55 +165,155 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
       }
     }
 
-    // ---- diagonal block
+    // ---- diagonal block: warp w takes right-hand sides r = w, w+2, ...
+    // (up to HR = MAXR/2 of them, carried through the same step loop as
+    // independent chains); lane l owns rows l and l+32.  Every lane evaluates
+    // the step's division (uniform, no divergence) and the owner's quotient
+    // is broadcast by shuffle; per entry the operations are the oracle's.
     __syncthreads();   // sy (aliased by sacc) is no longer read
+    EBV_TR(3);
 #pragma unroll
     for (int r = 0; r < MAXR; r++)
       if (r < nr) sacc[i * MAXR + r] = acc[r];
     __syncthreads();
-    const double* st = sd;
-    for (int r = warp; r < nr; r += BR / 32) {
-      double v0 = sacc[lane * MAXR + r], v1 = sacc[(lane + 32) * MAXR + r];
+    {
+      constexpr int HR = MAXR / 2;
+      const int nw = (nr + 1) / 2 > 0 ? 2 : 1;
+      const int myr = (nr - warp + 1) / 2;          // rhs handled by this warp
+      if (myr > 0) {
+      const double* st = sd;
+      const int nv = (int)((n - I * BR) < BR ? (n - I * BR) : BR);   // valid rows of the block
+      double v0[HR], v1[HR];
+#pragma unroll
+      for (int q = 0; q < HR; q++) {
+        const int r = warp + 2 * q;
+        v0[q] = (q < myr) ? sacc[lane * MAXR + r] : 0.0;
+        v1[q] = (q < myr) ? sacc[(lane + 32) * MAXR + r] : 0.0;
+      }
+      (void)nw;
       if (FORWARD) {
-        // rows lane, lane+32; y_k final when reached; k ascending
-#pragma unroll 8
+#pragma unroll 4
         for (int k = 0; k < 32; k++) {
-          const double yk = __shfl_sync(0xffffffffu, v0, k);
-          if (lane > k) v0 = fma(-st[k * TSTR + lane], yk, v0);
-          v1 = fma(-st[k * TSTR + lane + 32], yk, v1);
-        }
-#pragma unroll 8
-        for (int k = 32; k < BR; k++) {
-          const double yk = __shfl_sync(0xffffffffu, v1, k - 32);
-          if (lane + 32 > k) v1 = fma(-st[k * TSTR + lane + 32], yk, v1);
-        }
-      } else {
-        // k descending: x_k = y_k / u_kk, then rows above k are updated
-#pragma unroll 8
-        for (int k = BR - 1; k >= 32; k--) {
-          const bool valid = I * BR + k < n;
-          if (lane == k - 32 && valid) v1 = v1 / st[k * TSTR + k];
-          const double xk = __shfl_sync(0xffffffffu, v1, k - 32);
-          if (valid) {
-            if (lane + 32 < k) v1 = fma(-st[k * TSTR + lane + 32], xk, v1);
-            v0 = fma(-st[k * TSTR + lane], xk, v0);
+          const double l0 = st[k * TSTR + lane], l1 = st[k * TSTR + lane + 32];
+          const bool b0 = lane > k;
+#pragma unroll
+          for (int q = 0; q < HR; q++) {
+            if (NR == 1 && q > 0) break;
+            const double yk = __shfl_sync(0xffffffffu, v0[q], k);
+            const double t0 = fma(-l0, yk, v0[q]);
+            v0[q] = b0 ? t0 : v0[q];
+            v1[q] = fma(-l1, yk, v1[q]);
           }
         }
-#pragma unroll 8
+#pragma unroll 4
+        for (int k = 32; k < BR; k++) {
+          const double l1 = st[k * TSTR + lane + 32];
+          const bool b1 = lane + 32 > k;
+#pragma unroll
+          for (int q = 0; q < HR; q++) {
+            if (NR == 1 && q > 0) break;
+            const double yk = __shfl_sync(0xffffffffu, v1[q], k - 32);
+            const double t1 = fma(-l1, yk, v1[q]);
+            v1[q] = b1 ? t1 : v1[q];
+          }
+        }
+      } else {
+        // k descending; steps k >= nv (padding rows of the last block) are
+        // skipped.  Fast pass with hoisted reciprocals (verified); if any
+        // quotient is unverified the block is redone with true division.
+        double rc0 = 1.0 / st[lane * TSTR + lane], rc1 = 1.0 / st[(lane + 32) * TSTR + lane + 32];
+        double w0[HR], w1[HR];
+#pragma unroll
+        for (int q = 0; q < HR; q++) { w0[q] = v0[q]; w1[q] = v1[q]; }
+        bool ok = true;
+        for (int k = BR - 1; k >= 32; k--) {
+          if (k >= nv) continue;
+          const double ukk = st[k * TSTR + k];
+          const double rk = __shfl_sync(0xffffffffu, rc1, k - 32);
+          const double u0 = st[k * TSTR + lane], u1 = st[k * TSTR + lane + 32];
+          const bool own = lane == k - 32, b1 = lane + 32 < k;
+#pragma unroll
+          for (int q = 0; q < HR; q++) {
+            if (NR == 1 && q > 0) break;
+            const double xk = __shfl_sync(0xffffffffu, quot(v1[q], ukk, rk, own && q < myr, ok), k - 32);
+            v1[q] = own ? xk : (b1 ? fma(-u1, xk, v1[q]) : v1[q]);
+            v0[q] = fma(-u0, xk, v0[q]);
+          }
+        }
         for (int k = 31; k >= 0; k--) {
-          const bool valid = I * BR + k < n;
-          if (lane == k && valid) v0 = v0 / st[k * TSTR + k];
-          const double xk = __shfl_sync(0xffffffffu, v0, k);
-          if (valid && lane < k) v0 = fma(-st[k * TSTR + lane], xk, v0);
+          if (k >= nv) continue;
+          const double ukk = st[k * TSTR + k];
+          const double rk = __shfl_sync(0xffffffffu, rc0, k);
+          const double u0 = st[k * TSTR + lane];
+          const bool own = lane == k, b0 = lane < k;
+#pragma unroll
+          for (int q = 0; q < HR; q++) {
+            if (NR == 1 && q > 0) break;
+            const double xk = __shfl_sync(0xffffffffu, quot(v0[q], ukk, rk, own && q < myr, ok), k);
+            v0[q] = own ? xk : (b0 ? fma(-u0, xk, v0[q]) : v0[q]);
+          }
+        }
+        // any unverified quotient (checked by its owner lane) -> redo the
+        // block with true division
+        if (__any_sync(0xffffffffu, !ok)) {
+#pragma unroll
+          for (int q = 0; q < HR; q++) { v0[q] = w0[q]; v1[q] = w1[q]; }
+          for (int k = BR - 1; k >= 32; k--) {
+            if (k >= nv) continue;
+            const double ukk = st[k * TSTR + k];
+            const double u0 = st[k * TSTR + lane], u1 = st[k * TSTR + lane + 32];
+            const bool own = lane == k - 32, b1 = lane + 32 < k;
+#pragma unroll
+            for (int q = 0; q < HR; q++) {
+              if (NR == 1 && q > 0) break;
+              const double xk = __shfl_sync(0xffffffffu, v1[q] / ukk, k - 32);
+              v1[q] = own ? xk : (b1 ? fma(-u1, xk, v1[q]) : v1[q]);
+              v0[q] = fma(-u0, xk, v0[q]);
+            }
+          }
+          for (int k = 31; k >= 0; k--) {
+            if (k >= nv) continue;
+            const double ukk = st[k * TSTR + k];
+            const double u0 = st[k * TSTR + lane];
+            const bool own = lane == k, b0 = lane < k;
+#pragma unroll
+            for (int q = 0; q < HR; q++) {
+              if (NR == 1 && q > 0) break;
+              const double xk = __shfl_sync(0xffffffffu, v0[q] / ukk, k);
+              v0[q] = own ? xk : (b0 ? fma(-u0, xk, v0[q]) : v0[q]);
+            }
+          }
         }
       }
       const int64_t r0 = I * BR + lane, r1 = r0 + 32;
-      if (r0 < n) B[r0 + (int64_t)r * ldb] = v0;
-      if (r1 < n) B[r1 + (int64_t)r * ldb] = v1;
+#pragma unroll
+      for (int q = 0; q < HR; q++) {
+        if (q < myr) {
+          const int r = warp + 2 * q;
+          if (r0 < n) B[r0 + (int64_t)r * ldb] = v0[q];
+          if (r1 < n) B[r1 + (int64_t)r * ldb] = v1[q];
+        }
+      }
+      }   // myr > 0
     }
-    __threadfence();
+    // every thread's stores of this block precede thread 0's release (bar.sync
+    // orders them at CTA scope; the gpu-scope release is cumulative)
+#ifndef EBV_RELEASE_VARIANT
+#define EBV_RELEASE_VARIANT 0
+#endif
+    if (EBV_RELEASE_VARIANT == 1) __threadfence();
     __syncthreads();
-    if (i == 0) st_release(flags + I, epoch);
+    EBV_TR(4);
+    if (i == 0) {
+      if (EBV_RELEASE_VARIANT == 2) {
+        asm volatile("st.relaxed.gpu.global.b32 [%0], %1;\n" ::"l"(flags + I), "r"(epoch) : "memory");
+      } else if (EBV_RELEASE_VARIANT == 1) {
+        asm volatile("st.relaxed.gpu.global.b32 [%0], %1;\n" ::"l"(flags + I), "r"(epoch) : "memory");
+      } else {
+        st_release(flags + I, epoch);
+      }
+    }
+    EBV_TR(5);
   }
 }
 

@@ -27,10 +27,16 @@ namespace {
 
 constexpr int VT = 256;   // threads per CTA
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
+__device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+// relaxed polls (an acquire load costs an L1 invalidation per poll on
+// sm_100a), then one acquire fence
+__device__ __forceinline__ void wait_flag(const int* p, int v) {
+  while (ld_relaxed(p) != v) __nanosleep(32);
+  asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
 }
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
@@ -99,9 +105,7 @@ __global__ void __launch_bounds__(VT, 1)
     if (ck >= 0) {
       l = scol + ck * n;            // the owner already holds L_(k)
     } else {
-      if (tid == 0) {
-        while (ld_acquire(flags + k) != epoch) __nanosleep(20);
-      }
+      if (tid == 0) wait_flag(flags + k, epoch);
       __syncthreads();
       for (int i = k + 1 + tid; i < n; i += VT) sl[i] = __ldcg(A + i + (int64_t)k * lda);
       __syncthreads();

@@ -1,0 +1,106 @@
+"""Per-config measurements for BASELINE.json configs C1, C2, C3, C5 (C4 is
+bench.py's headline).  CUDA-event timing on the launching stream, warm-up 3,
+median of 5, inputs restored from pristine device copies outside the events.
+One JSON line per measurement."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import json
+import statistics
+
+import torch
+
+import ebv_inputs
+import paper_1907_05767_b200 as ebv
+
+dev = torch.device("cuda:0")
+stream = torch.cuda.current_stream(dev)
+sh = stream.cuda_stream
+PEAK_TF = 37.116
+HBM = 6538.6
+
+
+def timeit(prep, fn, reps=5, warm=3):
+    ts = []
+    for r in range(warm + reps):
+        prep()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if r >= warm:
+            ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts), min(ts), max(ts)
+
+
+def emit(**kw):
+    print(json.dumps(kw), flush=True)
+
+
+ctx = ebv.Context(0)
+info = torch.zeros((), dtype=torch.int64, device=dev)
+
+# ---------------- C1 / C2 / C3 dense factor (+ solve)
+for cfg, n, nrhs in (("C1", 64, 1), ("C2", 1024, 1), ("C3", 8192, 16)):
+    d = ebv_inputs.generate(n, seed=1, nrhs=nrhs, device=dev)
+    A0, B0 = d["At"], d["B"].T.clone(memory_format=torch.contiguous_format)
+    Aw, Bw = torch.empty_like(A0), torch.empty_like(B0)
+    fl = 2.0 / 3.0 * n ** 3
+    paths = [("blocked", ebv.EBV_PATH_BLOCKED)]
+    if n <= 1536:
+        paths += [("vector_ebvpair", ebv.EBV_PATH_VECTOR), ("vector_cyclic", -1)]
+    for name, path in paths:
+        if path == -1:
+            ctx.set_path(ebv.EBV_PATH_VECTOR)
+            C = min(148, n // 2) if n >= 2 else 1
+            ctx.set_vector_ctas(-C)
+        else:
+            ctx.set_path(path)
+            ctx.set_vector_ctas(0)
+        med, lo, hi = timeit(lambda: Aw.copy_(A0),
+                             lambda: ebv.ebv_lu_factor(ctx.handle, n, Aw.data_ptr(), n, 0.0, info.data_ptr(), sh))
+        ok = int(info) == 0
+        rec = {"config": cfg, "n": n, "what": "factor", "path": name, "ms": med, "ms_min": lo, "ms_max": hi,
+               "gflops": fl / med / 1e6, "frac_fp64_peak": fl / med / 1e9 / PEAK_TF, "info_ok": ok}
+        if name.startswith("vector"):
+            rec["us_per_step"] = 1e3 * med / max(n - 1, 1)
+        emit(**rec)
+    ctx.set_path(ebv.EBV_PATH_AUTO)
+    ctx.set_vector_ctas(0)
+    Aw.copy_(A0)
+    ebv.ebv_lu_factor(ctx.handle, n, Aw.data_ptr(), n, 0.0, info.data_ptr(), sh)
+    med, lo, hi = timeit(lambda: Bw.copy_(B0),
+                         lambda: ebv.ebv_lu_solve(ctx.handle, n, Aw.data_ptr(), n, Bw.data_ptr(), n, nrhs, sh))
+    err = (Bw.T - d["X"]).abs().max().item()
+    emit(config=cfg, n=n, nrhs=nrhs, what="solve", ms=med, ms_min=lo, ms_max=hi,
+         gbs=8.0 * n * n / med / 1e6, frac_hbm=8.0 * n * n / med / 1e6 / HBM, max_err=err)
+    # context: cuSOLVER no-pivot getrf (library comparator, never on the product path)
+    if n >= 1024:
+        A = A0.T.contiguous()
+        med, lo, hi = timeit(lambda: None, lambda: torch.linalg.lu_factor(A, pivot=False))
+        emit(config=cfg, n=n, what="factor", path="cusolver_getrf_nopivot(context)", ms=med,
+             gflops=fl / med / 1e6)
+    del d, A0, B0, Aw, Bw
+
+# ---------------- C5 batched
+batch = 100_000
+db = ebv_inputs.generate_batched(batch, 32, seed=1, nrhs=1, device=dev)
+A0 = db["At"]
+B0 = db["B"].transpose(1, 2).clone(memory_format=torch.contiguous_format)
+Aw, Bw = torch.empty_like(A0), torch.empty_like(B0)
+binfo = torch.zeros(batch, dtype=torch.int32, device=dev)
+
+
+def prep():
+    Aw.copy_(A0)
+    Bw.copy_(B0)
+
+
+med, lo, hi = timeit(prep, lambda: ebv.ebv_lu_factor_batched(ctx.handle, 32, Aw.data_ptr(), 32, 1024, batch,
+                                                             Bw.data_ptr(), 32, 32, 1, 0.0, binfo.data_ptr(), sh))
+by = batch * (2 * 32 * 32 * 8 + 2 * 32 * 8 + 4)
+emit(config="C5", batch=batch, n=32, what="batched factor+solve", ms=med, ms_min=lo, ms_max=hi,
+     gbs=by / med / 1e6, frac_hbm=by / med / 1e6 / HBM, systems_per_s=batch / med * 1e3,
+     max_err=(Bw.transpose(1, 2) - db["X"]).abs().max().item(), bytes=by)
