@@ -22,6 +22,14 @@ namespace {
 constexpr int NP = 32;   // padded order
 constexpr int MAXRHS = 16;
 
+// Predicated fma (no select instructions): a <- fma(nl, u, a) if p.
+__device__ __forceinline__ void pfma(double& a, double nl, double u, bool p) {
+  asm("{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n @q fma.rn.f64 %0, %1, %2, %0;\n}\n"
+      : "+d"(a)
+      : "d"(nl), "d"(u), "r"((unsigned)p));
+}
+
+
 __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict__ A, int64_t lda,
                                                       int64_t strideA, int64_t batch, double* __restrict__ B,
                                                       int64_t ldb, int64_t strideB, int nrhs,
@@ -61,20 +69,34 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
 
   int inf = 0;
   const int hb = h << 4;
-  // ---- factor (Eq 6), k ascending
+  // ---- factor (Eq 6), k ascending.  With rows t and 31-t per lane, row
+  // 31-t is below every pivot k < 16 and row t is above every pivot k >= 16,
+  // so at each step only one of the lane's two rows needs a predicate.
 #pragma unroll
   for (int k = 0; k < NP; k++) {
     const int src = hb + (k < 16 ? k : NP - 1 - k);
     const double piv = __shfl_sync(0xffffffffu, k < 16 ? ra[k] : rb[k], src);
     if (k < n && inf == 0 && fabs(piv) <= tv) inf = k + 1;
-    const bool a0 = r0 > k, a1 = r1 > k;     // rows below the pivot
-    if (a0) ra[k] = ra[k] / piv;              // Eq 6-a
-    if (a1) rb[k] = rb[k] / piv;
+    if (k < 16) {
+      const bool a0 = r0 > k;
+      if (a0) ra[k] = ra[k] / piv;                     // Eq 6-a
+      rb[k] = rb[k] / piv;
+      const double n0 = -ra[k], n1 = -rb[k];
 #pragma unroll
-    for (int j = k + 1; j < NP; j++) {
-      const double u = __shfl_sync(0xffffffffu, k < 16 ? ra[j] : rb[j], src);   // Eq 6-b
-      if (a0) ra[j] = fma(-ra[k], u, ra[j]);                                    // Eq 6-c
-      if (a1) rb[j] = fma(-rb[k], u, rb[j]);
+      for (int j = k + 1; j < NP; j++) {
+        const double u = __shfl_sync(0xffffffffu, ra[j], src);   // Eq 6-b (row k = row t of lane k)
+        pfma(ra[j], n0, u, a0);                                  // Eq 6-c
+        rb[j] = fma(n1, u, rb[j]);
+      }
+    } else {
+      const bool a1 = r1 > k;
+      if (a1) rb[k] = rb[k] / piv;
+      const double n1 = -rb[k];
+#pragma unroll
+      for (int j = k + 1; j < NP; j++) {
+        const double u = __shfl_sync(0xffffffffu, rb[j], src);
+        pfma(rb[j], n1, u, a1);
+      }
     }
   }
   if (act && t == 0 && info) info[sys] = inf;
@@ -86,20 +108,28 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
       double y0 = v0 ? Bs[r0 + (int64_t)r * ldb] : 0.0;
       double y1 = v1 ? Bs[r1 + (int64_t)r * ldb] : 0.0;
 #pragma unroll
-      for (int k = 0; k < NP; k++) {
+      for (int k = 0; k < NP; k++) {   // forward: LY = B
         const int src = hb + (k < 16 ? k : NP - 1 - k);
         const double yk = __shfl_sync(0xffffffffu, k < 16 ? y0 : y1, src);
-        if (r0 > k) y0 = fma(-ra[k], yk, y0);
-        if (r1 > k) y1 = fma(-rb[k], yk, y1);
+        if (k < 16) {
+          pfma(y0, -ra[k], yk, r0 > k);
+          y1 = fma(-rb[k], yk, y1);
+        } else {
+          pfma(y1, -rb[k], yk, r1 > k);
+        }
       }
 #pragma unroll
-      for (int k = NP - 1; k >= 0; k--) {
+      for (int k = NP - 1; k >= 0; k--) {   // backward: UX = Y
         const int src = hb + (k < 16 ? k : NP - 1 - k);
         if (k < 16) { if (t == k) y0 = y0 / ra[k]; }
         else        { if (t == NP - 1 - k) y1 = y1 / rb[k]; }
         const double xk = __shfl_sync(0xffffffffu, k < 16 ? y0 : y1, src);
-        if (r0 < k) y0 = fma(-ra[k], xk, y0);
-        if (r1 < k) y1 = fma(-rb[k], xk, y1);
+        if (k < 16) {
+          pfma(y0, -ra[k], xk, r0 < k);   // rows 31-t >= 16 > k never
+        } else {
+          y0 = fma(-ra[k], xk, y0);       // rows t < 16 <= k always
+          pfma(y1, -rb[k], xk, r1 < k);
+        }
       }
       if (v0) Bs[r0 + (int64_t)r * ldb] = y0;
       if (v1) Bs[r1 + (int64_t)r * ldb] = y1;
@@ -112,180 +142,6 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
   }
 }
 
-// ---------------------------------------------------------------- fast path
-// n = 32 systems stored back to back (lda = 32, strideA = 1024; B with
-// ldb = 32, strideB = 32*nrhs): persistent warps, each looping over system
-// pairs, with the next pair (16 KB + its right-hand sides) copied into the
-// warp's shared-memory buffer by cp.async while the current pair is factored
-// from registers.  The lane map is the same EbV pairing (rows t and 31-t);
-// it makes one of a lane's two rows unconditionally active (k < 16) or
-// inactive (k >= 16) at every step, so only the other row needs a predicate,
-// applied with a predicated fma.rn.f64 (no select instructions).
-
-__device__ __forceinline__ void pfma(double& a, double nl, double u, bool p) {
-  asm("{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n @q fma.rn.f64 %0, %1, %2, %0;\n}\n"
-      : "+d"(a)
-      : "d"(nl), "d"(u), "r"((unsigned)p));
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
-
-constexpr int FWARPS = 4;   // warps per CTA
-
-__global__ void __launch_bounds__(32 * FWARPS) batched32_kernel(double* __restrict__ A, int64_t batch,
-                                                                double* __restrict__ B, int nrhs,
-                                                                int tau_default, double tau_value,
-                                                                int32_t* __restrict__ info) {
-  extern __shared__ __align__(16) double fsm[];
-  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int h = lane >> 4, t = lane & 15, hb = h << 4;
-  const int r0 = t, r1 = NP - 1 - t;
-  const int bstride = NP * nrhs;                       // doubles per system's B
-  double* buf = fsm + (size_t)wl * (2 * NP * NP + 2 * NP * MAXRHS);
-  double* bbuf = buf + 2 * NP * NP;
-  const int64_t npairs = (batch + 1) / 2;
-  const int64_t wstep = (int64_t)gridDim.x * FWARPS;
-  int64_t pair = (int64_t)blockIdx.x * FWARPS + wl;
-
-  // A of the next pair is prefetched while the current pair is factored; its
-  // right-hand sides (small) after the current solve has read its own.
-  auto prefetch_a = [&](int64_t pr) {
-    if (pr >= npairs) return;
-    const int64_t s0 = 2 * pr;
-    const int nsys = (s0 + 1 < batch) ? 2 : 1;
-    const char* ga = reinterpret_cast<const char*>(A + s0 * NP * NP);
-    char* sa = reinterpret_cast<char*>(buf);
-    const int chunks = nsys * NP * NP * 8 / 16;
-    for (int c = lane; c < chunks; c += 32) cp_async16(sa + 16 * c, ga + 16 * c);
-    cp_commit();
-  };
-  auto prefetch_b = [&](int64_t pr) {
-    if (pr >= npairs || !B) return;
-    const int64_t s0 = 2 * pr;
-    const int nsys = (s0 + 1 < batch) ? 2 : 1;
-    const char* gb = reinterpret_cast<const char*>(B + s0 * bstride);
-    char* sb = reinterpret_cast<char*>(bbuf);
-    const int bch = nsys * bstride * 8 / 16;
-    for (int c = lane; c < bch; c += 32) cp_async16(sb + 16 * c, gb + 16 * c);
-    cp_commit();
-  };
-
-  prefetch_a(pair);
-  prefetch_b(pair);
-  for (; pair < npairs; pair += wstep) {
-    const int64_t sys = 2 * pair + h;
-    const bool act = sys < batch;
-    cp_wait_all();
-    __syncwarp();
-    const double* ms = buf + h * NP * NP;
-    double ra[NP], rb[NP];
-#pragma unroll
-    for (int j = 0; j < NP; j++) {
-      ra[j] = act ? ms[j * NP + r0] : (r0 == j ? 1.0 : 0.0);
-      rb[j] = act ? ms[j * NP + r1] : (r1 == j ? 1.0 : 0.0);
-    }
-    __syncwarp();
-    prefetch_a(pair + wstep);
-
-    double tv = tau_value;
-    if (tau_default) {
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int j = 0; j < NP; j++) { s0 += fabs(ra[j]); s1 += fabs(rb[j]); }
-      double nm = fmax(s0, s1);
-#pragma unroll
-      for (int o = 8; o >= 1; o >>= 1) nm = fmax(nm, __shfl_xor_sync(0xffffffffu, nm, o));
-      tv = (double)NP * 2.220446049250313e-16 * nm;
-    }
-
-    int inf = 0;
-    // ---- factor (Eq 6), k ascending
-#pragma unroll
-    for (int k = 0; k < NP; k++) {
-      const int src = hb + (k < 16 ? k : NP - 1 - k);
-      const double piv = __shfl_sync(0xffffffffu, k < 16 ? ra[k] : rb[k], src);
-      if (inf == 0 && fabs(piv) <= tv) inf = k + 1;
-      if (k < 16) {
-        // row r1 = 31-t >= 16 > k: always below the pivot; row t: if t > k
-        const bool a0 = t > k;
-        if (a0) ra[k] = ra[k] / piv;
-        rb[k] = rb[k] / piv;
-        const double n0 = -ra[k], n1 = -rb[k];
-#pragma unroll
-        for (int j = k + 1; j < NP; j++) {
-          const double u = __shfl_sync(0xffffffffu, k < 16 ? ra[j] : rb[j], src);
-          pfma(ra[j], n0, u, a0);
-          rb[j] = fma(n1, u, rb[j]);
-        }
-      } else {
-        // row t < 16 <= k: never below the pivot; row 31-t: if 31-t > k
-        const bool a1 = NP - 1 - t > k;
-        if (a1) rb[k] = rb[k] / piv;
-        const double n1 = -rb[k];
-#pragma unroll
-        for (int j = k + 1; j < NP; j++) {
-          const double u = __shfl_sync(0xffffffffu, rb[j], src);
-          pfma(rb[j], n1, u, a1);
-        }
-      }
-    }
-    if (act && t == 0 && info) info[sys] = inf;
-
-    double* As = A + (act ? sys : 0) * NP * NP;
-    if (B) {
-      double* Bs = B + (act ? sys : 0) * bstride;
-#pragma unroll
-      for (int r = 0; r < nrhs; r++) {
-        double v0 = act ? bbuf[h * bstride + r * NP + r0] : 0.0;
-        double v1 = act ? bbuf[h * bstride + r * NP + r1] : 0.0;
-#pragma unroll
-        for (int k = 0; k < NP; k++) {   // forward (Eq 1: LY = B)
-          const int src = hb + (k < 16 ? k : NP - 1 - k);
-          const double yk = __shfl_sync(0xffffffffu, k < 16 ? v0 : v1, src);
-          if (k < 16) {
-            pfma(v0, -ra[k], yk, t > k);
-            v1 = fma(-rb[k], yk, v1);
-          } else {
-            pfma(v1, -rb[k], yk, NP - 1 - t > k);
-          }
-        }
-#pragma unroll
-        for (int k = NP - 1; k >= 0; k--) {   // backward (UX = Y)
-          const int src = hb + (k < 16 ? k : NP - 1 - k);
-          if (k < 16) { if (t == k) v0 = v0 / ra[k]; }
-          else        { if (t == NP - 1 - k) v1 = v1 / rb[k]; }
-          const double xk = __shfl_sync(0xffffffffu, k < 16 ? v0 : v1, src);
-          if (k < 16) {
-            pfma(v0, -ra[k], xk, t < k);       // rows t < k; rows 31-t >= 16 > k never
-          } else {
-            v0 = fma(-ra[k], xk, v0);          // rows t < 16 <= k always
-            pfma(v1, -rb[k], xk, NP - 1 - t < k);
-          }
-        }
-        if (act) {
-          Bs[r * NP + r0] = v0;
-          Bs[r * NP + r1] = v1;
-        }
-      }
-    }
-    __syncwarp();
-    prefetch_b(pair + wstep);
-    if (act) {
-#pragma unroll
-      for (int j = 0; j < NP; j++) {
-        As[j * NP + r0] = ra[j];
-        As[j * NP + r1] = rb[j];
-      }
-    }
-  }
-  cp_wait_all();
-}
-
 }  // namespace
 
 cudaError_t launch_batched(int64_t n, double* A, int64_t lda, int64_t strideA, int64_t batch, double* B,
@@ -293,32 +149,6 @@ cudaError_t launch_batched(int64_t n, double* A, int64_t lda, int64_t strideA, i
                            double tau_value, int32_t* info, cudaStream_t s) {
   if (batch <= 0 || n <= 0) return cudaSuccess;
   if (n > NP || nrhs > MAXRHS) return cudaErrorInvalidValue;
-  const bool packed = n == NP && lda == NP && (batch <= 1 || strideA == NP * NP) &&
-                      ((reinterpret_cast<uintptr_t>(A) & 15) == 0) &&
-                      (!B || (ldb == NP && (batch <= 1 || strideB == NP * nrhs) &&
-                              ((reinterpret_cast<uintptr_t>(B) & 15) == 0))) &&
-                      !(tau && !tau_default);
-  if (packed) {
-    const size_t smem = (size_t)FWARPS * (2 * NP * NP + 2 * NP * MAXRHS) * 8;
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(batched32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, batched32_kernel, 32 * FWARPS, smem);
-    if (per_sm < 1) per_sm = 1;
-    const int64_t pairs = (batch + 1) / 2;
-    int64_t grid = (int64_t)sms * per_sm;
-    const int64_t need = (pairs + FWARPS - 1) / FWARPS;
-    if (grid > need) grid = need;
-    batched32_kernel<<<(unsigned)grid, 32 * FWARPS, smem, s>>>(A, batch, B, B ? (int)nrhs : 0, tau_default ? 1 : 0,
-                                                              tau_value, info);
-    return cudaGetLastError();
-  }
   const int64_t warps = (batch + 1) / 2;
   const int64_t blocks = (warps * 32 + 127) / 128;
   batched_kernel<<<(unsigned)blocks, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, ldb, strideB, (int)nrhs, tau,
