@@ -110,10 +110,17 @@ ebv_status_t ebv_set_path(ebv_context_t ctx, ebv_path_t path);
 ebv_status_t ebv_set_leaf(ebv_context_t ctx, int64_t leaf);
 
 /* Blocked path schedule: nb > 0 = right-looking with column blocks of nb
- * (a multiple of the leaf; default 256) — panel LU, U12 substitution, DMMA
- * trailing update per block; nb = -1 = fully recursive 2 x 2 splitting;
- * nb = 0 restores the default.  Both are bitwise identical. */
+ * (a multiple of the leaf) — panel LU, U12 substitution, DMMA trailing
+ * update per block; nb = 0 (default) = size-adaptive (128 below n = 12288,
+ * 256 below 24576, else 512: the best measured on B200); nb = -1 = fully
+ * recursive 2 x 2 splitting.  All are bitwise identical. */
 ebv_status_t ebv_set_block(ebv_context_t ctx, int64_t nb);
+
+/* CUDA Graph replay of the blocked factor schedule (default on): the second
+ * ebv_lu_factor call with identical arguments (same A / d_info pointers,
+ * n, lda, tau and options, non-default stream) captures the schedule; later
+ * calls replay it.  Bypassed while statistics are enabled. */
+ebv_status_t ebv_set_graphs(ebv_context_t ctx, int enable);
 
 /* Lookahead (default on): in the blocked schedule, panel K+1 is factored
  * on a high-priority side stream of the context while step K's update of

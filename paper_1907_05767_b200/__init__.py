@@ -42,6 +42,7 @@ SIGNATURES = {
     "ebv_set_vector_ctas": (_int, [_vp, _i64]),
     "ebv_set_block": (_int, [_vp, _i64]),
     "ebv_set_lookahead": (_int, [_vp, _int]),
+    "ebv_set_graphs": (_int, [_vp, _int]),
     "ebv_lu_factor": (_int, [_vp, _i64, _vp, _i64, _d, _vp, _vp]),
     "ebv_lu_solve": (_int, [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp]),
     "ebv_lu_factor_batched": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _d, _vp, _vp]),
@@ -125,6 +126,10 @@ def ebv_set_block(ctx, nb):
 
 def ebv_set_lookahead(ctx, enable):
     return lib().ebv_set_lookahead(ctx, 1 if enable else 0)
+
+
+def ebv_set_graphs(ctx, enable):
+    return lib().ebv_set_graphs(ctx, 1 if enable else 0)
 
 
 def ebv_set_vector_ctas(ctx, ctas):
@@ -282,6 +287,9 @@ class Context:
 
     def set_lookahead(self, on: bool):
         _check(ebv_set_lookahead(self.handle, on), "ebv_set_lookahead")
+
+    def set_graphs(self, on: bool):
+        _check(ebv_set_graphs(self.handle, on), "ebv_set_graphs")
 
     def set_vector_ctas(self, ctas: int):
         _check(ebv_set_vector_ctas(self.handle, ctas), "ebv_set_vector_ctas")

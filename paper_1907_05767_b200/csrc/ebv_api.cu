@@ -166,8 +166,16 @@ cudaError_t panel_rec(ebv_context* c, int64_t M, int64_t w, double* P, int64_t l
 //     A[K+1:, K+1:] -= L21 U12       (Eq 6-c for the nb steps at once, DMMA)
 // This is also the per-step structure of the 1D block-cyclic multi-GPU
 // schedule (only the owner of block K factors the panel).
+// Block width: the caller's choice, else size-adaptive (measured on B200:
+// 128 at n = 8192, 512 at n = 32768; profiles/r01_sweep_nb.jsonl).
+int64_t block_width(const ebv_context* c, int64_t n) {
+  if (c->nb > 0) return c->nb;
+  int64_t nb = n >= 24576 ? 512 : (n >= 12288 ? 256 : 128);
+  return ((nb + c->leaf - 1) / c->leaf) * c->leaf;
+}
+
 cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s) {
-  const int64_t nb = c->nb;
+  const int64_t nb = block_width(c, n);
   const bool la = c->lookahead && n > 2 * nb;
   cudaError_t e = cudaSuccess;
   if (la) {
@@ -254,6 +262,9 @@ ebv_status_t ensure_vflags(ebv_context* c, int64_t need) {
 
 extern "C" {
 
+static ebv_status_t factor_body(ebv_context_t c, int64_t n, double* A, int64_t lda, double tau, int64_t* d_info,
+                                cudaStream_t s);
+
 const char* ebv_status_string(ebv_status_t s) {
   switch (s) {
     case EBV_SUCCESS: return "success";
@@ -305,6 +316,8 @@ ebv_status_t ebv_destroy(ebv_context_t c) {
   dist_release(c);
   for (auto& r : c->recs) { cudaEventDestroy(r.e0); cudaEventDestroy(r.e1); }
   for (auto e : c->pool) cudaEventDestroy(e);
+  for (auto& en : c->gcache)
+    if (en.exec) cudaGraphExecDestroy(en.exec);
   if (c->d_flags) cudaFree(c->d_flags);
   if (c->d_vflags) cudaFree(c->d_vflags);
   cudaFree(c->d_tau);
@@ -334,9 +347,15 @@ ebv_status_t ebv_set_leaf(ebv_context_t c, int64_t leaf) {
 
 ebv_status_t ebv_set_block(ebv_context_t c, int64_t nb) {
   if (!c) return invalid("ebv_set_block: NULL ctx");
-  if (nb == 0) nb = ((256 + c->leaf - 1) / c->leaf) * c->leaf;
-  if (nb != -1 && (nb < c->leaf || nb % c->leaf)) return invalid("block must be -1 or a multiple of the leaf size");
+  if (nb != 0 && nb != -1 && (nb < c->leaf || nb % c->leaf))
+    return invalid("block must be 0 (adaptive), -1 or a multiple of the leaf size");
   c->nb = nb;
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_set_graphs(ebv_context_t c, int enable) {
+  if (!c) return invalid("ebv_set_graphs: NULL ctx");
+  c->graphs = enable != 0;
   return EBV_SUCCESS;
 }
 
@@ -362,6 +381,59 @@ ebv_status_t ebv_lu_factor(ebv_context_t c, int64_t n, double* A, int64_t lda, d
   if (c->path == EBV_PATH_VECTOR && n > EBV_VECTOR_MAX_N) return invalid("ebv_lu_factor: n too large for PATH_VECTOR");
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
+  // CUDA Graph replay of the blocked schedule: the second call with the same
+  // arguments captures it, later calls replay one graph (the schedule is
+  // static; replay removes per-launch CPU cost and inter-kernel gaps).
+  ebv_context::GraphEntry* ge = nullptr;
+  const bool use_graph = c->graphs && !c->stats && s != nullptr && n > c->leaf && c->path != EBV_PATH_VECTOR &&
+                         c->nb != -1;
+  if (use_graph) {
+    for (auto& en : c->gcache)
+      if (en.n == n && en.lda == lda && en.A == A && en.info == d_info && en.tau == tau && en.nb == c->nb &&
+          en.leaf == c->leaf && en.la == c->lookahead) {
+        ge = &en;
+        break;
+      }
+    if (ge && ge->exec) {
+      cudaError_t e = cudaGraphLaunch(ge->exec, s);
+      if (e != cudaSuccess) return cuda_fail(e, "graph launch");
+      c->launches += ge->launches;
+      return EBV_SUCCESS;
+    }
+    if (!ge) {
+      if (c->gcache.size() >= 8) {
+        if (c->gcache.front().exec) cudaGraphExecDestroy(c->gcache.front().exec);
+        c->gcache.erase(c->gcache.begin());
+      }
+      c->gcache.push_back({n, lda, c->nb, c->leaf, A, d_info, tau, c->lookahead, 0, 0, nullptr});
+      ge = &c->gcache.back();
+    }
+    ge->hits++;
+  }
+  const bool capture = use_graph && ge && ge->hits >= 2;
+  const int64_t l0 = c->launches;
+  if (capture) {
+    cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return cuda_fail(e, "begin capture");
+  }
+  ebv_status_t st = factor_body(c, n, A, lda, tau, d_info, s);
+  if (capture) {
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(s, &graph);
+    if (st != EBV_SUCCESS) { if (graph) cudaGraphDestroy(graph); return st; }
+    if (e != cudaSuccess) return cuda_fail(e, "end capture");
+    e = cudaGraphInstantiate(&ge->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) { ge->exec = nullptr; return cuda_fail(e, "graph instantiate"); }
+    ge->launches = c->launches - l0;
+    e = cudaGraphLaunch(ge->exec, s);
+    if (e != cudaSuccess) return cuda_fail(e, "graph launch");
+  }
+  return st;
+}
+
+static ebv_status_t factor_body(ebv_context_t c, int64_t n, double* A, int64_t lda, double tau, int64_t* d_info,
+                                cudaStream_t s) {
   cudaError_t e = timed(c, KC_OTHER, 0, 0, s, 1, [&] { return launch_set_info0(d_info, s); });
   if (e != cudaSuccess) return cuda_fail(e, "info init");
   if (n == 0) return EBV_SUCCESS;
@@ -386,7 +458,7 @@ ebv_status_t ebv_lu_factor(ebv_context_t c, int64_t n, double* A, int64_t lda, d
     if (e != cudaSuccess) return cuda_fail(e, "vector path");
     return EBV_SUCCESS;
   }
-  e = (c->nb > 0) ? lu_blocked(c, n, A, lda, d_info, s) : lu_rec(c, n, A, lda, 0, d_info, s);
+  e = (c->nb != -1) ? lu_blocked(c, n, A, lda, d_info, s) : lu_rec(c, n, A, lda, 0, d_info, s);
   if (e != cudaSuccess) return cuda_fail(e, "blocked factor");
   return EBV_SUCCESS;
 }

@@ -14,7 +14,7 @@ struct ebv_context {
   int device = 0;
   ebv_path_t path = EBV_PATH_AUTO;
   int64_t leaf = 64;
-  int64_t nb = 256;         // right-looking block width; -1 = fully recursive schedule
+  int64_t nb = 0;           // right-looking block width; 0 = size-adaptive, -1 = fully recursive
   double* d_tau = nullptr;
   unsigned long long* d_norm = nullptr;
   double* d_scratch = nullptr;
@@ -40,6 +40,19 @@ struct ebv_context {
   int64_t st_launch[EBV_NUM_KCLASSES] = {0};
   double st_ms[EBV_NUM_KCLASSES] = {0}, st_flops[EBV_NUM_KCLASSES] = {0}, st_bytes[EBV_NUM_KCLASSES] = {0};
   ebv_dist_state* dist = nullptr;   // set by ebv_create_dist
+  // CUDA Graph cache of the blocked factor schedule, keyed by its arguments
+  bool graphs = true;
+  struct GraphEntry {
+    int64_t n, lda, nb, leaf;
+    const void* A;
+    const void* info;
+    double tau;
+    bool la;
+    int hits;
+    int64_t launches;
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> gcache;
 };
 
 

@@ -317,3 +317,26 @@ def test_c4_n32768_properties(dev, ctx):
         else:        # (LU)_ij = sum_{p<j} l_ip u_pj + l_ij u_jj
             v = (LU[i, :j] * LU[:j, j]).sum() + LU[i, j] * LU[j, j]
         assert abs(v.item() - A[i, j].item()) <= 1e-12 * amax
+
+
+def test_graph_replay_bitwise(dev, ctx):
+    """The second identical call captures a CUDA Graph, later calls replay it:
+    every result bitwise equal to the oracle; launch accounting continues."""
+    n = 1100
+    d = ebv_inputs.generate(n, seed=31, device=dev)
+    lu_o, _ = oracle.lu_factor(d["At"].T.cpu().numpy())
+    Aw = torch.empty_like(d["At"])
+    info = torch.zeros((), dtype=torch.int64, device=dev)
+    s = torch.cuda.Stream()
+    counts = []
+    with torch.cuda.stream(s):
+        for rep in range(4):
+            Aw.copy_(d["At"])
+            c0 = ctx.launch_count()
+            st = ebv.ebv_lu_factor(ctx.handle, n, Aw.data_ptr(), n, 0.0, info.data_ptr(), s.cuda_stream)
+            assert st == 0, ebv.ebv_last_error()
+            counts.append(ctx.launch_count() - c0)
+            s.synchronize()
+            assert np.array_equal(Aw.T.cpu().numpy(), lu_o), rep
+            assert int(info) == 0
+    assert counts[0] == counts[2] == counts[3] > 10
