@@ -305,7 +305,9 @@ def run_ebv(args, rank, world, local):
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None,
                 "traffic": (traffic or {}).get("bytes_per_launch"),
-                "kernel": "gemm_sub_kernel (DMMA.8x8x4 trailing update, Eq 6-c)",
+                "traffic_launch": (traffic or {}).get("launch"),
+                "traffic_algorithmic_bytes": (traffic or {}).get("algorithmic_bytes"),
+                "kernel": "gemm_tma_kernel (TMA-fed DMMA.8x8x4 trailing update, Eq 6-c)",
                 "launches": g["launches"], "kernel_ms_per_step": g["ms"] / args.steps,
                 "share_of_step": g["ms"] / max(total_kernel_ms, 1e-9),
                 "algorithmic_flops_per_launch": g["flops"] / max(g["launches"], 1),
