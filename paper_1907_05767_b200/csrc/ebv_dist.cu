@@ -142,61 +142,151 @@ struct ebv_dist_state {
   int64_t nb = 256;
   ebv_layout_t layout = EBV_LAYOUT_CYCLIC;
   ncclComm_t comm = nullptr;
-  double* pbuf = nullptr;
+  double* pbuf = nullptr;       // two panel buffers (double-buffered), each pcap/2
   size_t pcap = 0;
+  cudaEvent_t ev_ready[2] = {nullptr, nullptr};   // panel K broadcast complete (side)
+  cudaEvent_t ev_free[2] = {nullptr, nullptr};    // step K done reading pbuf[K%2] (main)
+  cudaEvent_t ev_next = nullptr;                  // block K+1 columns updated (main)
+  cudaEvent_t ev_side = nullptr;                  // join point of the side stream
 };
 
 namespace {
 
 ebv_status_t ensure_pbuf(ebv_context* c, ebv_dist_state* d, size_t elems) {
-  if (elems <= d->pcap) return EBV_SUCCESS;
+  if (!d->ev_next) {
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < 2 && e == cudaSuccess; i++) {
+      e = cudaEventCreateWithFlags(&d->ev_ready[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_free[i], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_next, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_side, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e, "dist events");
+  }
+  if (2 * elems <= d->pcap) return EBV_SUCCESS;
   if (d->pbuf) cudaFree(d->pbuf);
   d->pbuf = nullptr;
   d->pcap = 0;
-  cudaError_t e = cudaMalloc(&d->pbuf, elems * sizeof(double));
+  cudaError_t e = cudaMalloc(&d->pbuf, 2 * elems * sizeof(double));
   if (e != cudaSuccess) { set_error("panel buffer alloc failed"); return EBV_ERR_ALLOC; }
-  d->pcap = elems;
+  d->pcap = 2 * elems;
   (void)c;
   return EBV_SUCCESS;
 }
 
+void release_events(ebv_dist_state* d) {
+  for (int i = 0; i < 2; i++) {
+    if (d->ev_ready[i]) cudaEventDestroy(d->ev_ready[i]);
+    if (d->ev_free[i]) cudaEventDestroy(d->ev_free[i]);
+  }
+  if (d->ev_next) cudaEventDestroy(d->ev_next);
+  if (d->ev_side) cudaEventDestroy(d->ev_side);
+}
+
 // The schedule over the views this process drives (one real rank, or all P
 // virtual ranks in emulation).  comm == nullptr means emulation.
+//
+// Streams: every panel factorization, pack and broadcast runs on the side
+// stream (one NCCL stream, collectives in step order on every rank); the
+// updates run on the caller's stream.  Lookahead: at step K the owner of
+// block K+1 updates those columns first, then factors panel K+1 on the side
+// stream while its caller stream updates the rest of its slab, so panel
+// K+1 (and its broadcast) overlaps step K's updates.  Panel buffers are
+// double-buffered by step parity; events order the reuse.
 ebv_status_t dist_factor(ebv_context* c, ebv_dist_state* d, std::vector<View>& views, int64_t n, int64_t* info,
                          cudaStream_t s) {
   const Plan& p0 = views[0].plan;
-  const int64_t nb = p0.nb;
-  ebv_status_t st = ensure_pbuf(c, d, (size_t)n * nb);
+  const int64_t nb = p0.nb, N = p0.N;
+  const size_t half = (size_t)n * nb;
+  ebv_status_t st = ensure_pbuf(c, d, half);
   if (st != EBV_SUCCESS) return st;
-  cudaError_t e = cudaSuccess;
-  for (int64_t K = 0; K < p0.N; K++) {
+  const bool real = d->comm && d->nranks > 1;
+  cudaStream_t side = c->side;
+  cudaError_t e = cudaEventRecord(d->ev_side, s);                  // side starts after the caller's work
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(side, d->ev_side, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "dist fork");
+  auto pbuf = [&](int64_t K) { return d->pbuf + (size_t)(K & 1) * half; };
+
+  // factor + pack panel K (owner's view) on the side stream
+  auto prepare_panel = [&](int64_t K) -> cudaError_t {
+    const int64_t c0 = K * nb, w = p0.width(K), M = n - c0;
+    for (auto& v : views) {
+      if (v.plan.rank != p0.owner(K)) continue;
+      double* P = v.A + c0 + v.plan.loc[K] * v.lda;
+      cudaError_t e2 = panel_rec(c, M, w, P, v.lda, c0, info, side);
+      if (e2 != cudaSuccess) return e2;
+      if (K >= 2) {   // pbuf[K%2] was read by step K-2 on the caller stream
+        e2 = cudaStreamWaitEvent(side, d->ev_free[K & 1], 0);
+        if (e2 != cudaSuccess) return e2;
+      }
+      e2 = cudaMemcpy2DAsync(pbuf(K), M * sizeof(double), P, v.lda * sizeof(double), M * sizeof(double), w,
+                             cudaMemcpyDeviceToDevice, side);
+      if (e2 != cudaSuccess) return e2;
+    }
+    return cudaSuccess;
+  };
+
+  e = prepare_panel(0);
+  if (e != cudaSuccess) return cuda_fail(e, "dist panel");
+  for (int64_t K = 0; K < N; K++) {
     const int64_t c0 = K * nb, w = p0.width(K), M = n - c0;
     const int64_t owner = p0.owner(K);
-    for (auto& v : views) {
-      if (v.plan.rank != owner) continue;
-      double* P = v.A + c0 + v.plan.loc[K] * v.lda;
-      e = panel_rec(c, M, w, P, v.lda, c0, info, s);
-      if (e != cudaSuccess) return cuda_fail(e, "dist panel");
-      e = cudaMemcpy2DAsync(d->pbuf, M * sizeof(double), P, v.lda * sizeof(double), M * sizeof(double), w,
-                            cudaMemcpyDeviceToDevice, s);
-      if (e != cudaSuccess) return cuda_fail(e, "dist pack");
-    }
-    if (d->comm && d->nranks > 1) {
-      ncclResult_t r = nccl().Broadcast(d->pbuf, d->pbuf, (size_t)(M * w), ncclFloat64, (int)owner, d->comm, s);
+    // ---- broadcast panel K (side stream, step order on every rank)
+    if (real) {
+      if (K >= 2) {
+        e = cudaStreamWaitEvent(side, d->ev_free[K & 1], 0);
+        if (e != cudaSuccess) return cuda_fail(e, "dist wait");
+      }
+      ncclResult_t r = nccl().Broadcast(pbuf(K), pbuf(K), (size_t)(M * w), ncclFloat64, (int)owner, d->comm, side);
       if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(panel)");
       c->launches += 1;
     }
+    e = cudaEventRecord(d->ev_ready[K & 1], side);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, d->ev_ready[K & 1], 0);
+    if (e != cudaSuccess) return cuda_fail(e, "dist order");
+    // ---- updates of step K on the caller stream; block K+1 first
+    const bool has_next = K + 1 < N;
+    const int64_t owner1 = has_next ? p0.owner(K + 1) : -1;
     for (auto& v : views) {
       const int64_t lc0 = suffix_after(v.plan, K);
-      const int64_t ncols = v.plan.cols - lc0;
-      if (ncols <= 0 || M - w < 0) continue;
+      int64_t ncols = v.plan.cols - lc0;
+      if (ncols <= 0) continue;
       double* X = v.A + c0 + lc0 * v.lda;
-      e = trsm_l(c, w, ncols, d->pbuf, M, X, v.lda, s);                                 // U12 = L11^-1 A12
-      if (e == cudaSuccess) e = gemm(c, M - w, ncols, w, d->pbuf + w, M, X, v.lda, X + w, v.lda, false, s);
-      if (e != cudaSuccess) return cuda_fail(e, "dist update");
+      int64_t first = 0;
+      if (has_next && v.plan.rank == owner1) {
+        const int64_t w1 = p0.width(K + 1);    // block K+1 is the first local block after K
+        e = trsm_l(c, w, w1, pbuf(K), M, X, v.lda, s);
+        if (e == cudaSuccess) e = gemm(c, M - w, w1, w, pbuf(K) + w, M, X, v.lda, X + w, v.lda, false, s);
+        if (e == cudaSuccess) e = cudaEventRecord(d->ev_next, s);
+        if (e != cudaSuccess) return cuda_fail(e, "dist update(next)");
+        first = w1;
+      }
+      if (ncols - first > 0) {
+        double* X2 = X + first * v.lda;
+        e = trsm_l(c, w, ncols - first, pbuf(K), M, X2, v.lda, s);
+        if (e == cudaSuccess)
+          e = gemm(c, M - w, ncols - first, w, pbuf(K) + w, M, X2, v.lda, X2 + w, v.lda, false, s);
+        if (e != cudaSuccess) return cuda_fail(e, "dist update");
+      }
+    }
+    e = cudaEventRecord(d->ev_free[K & 1], s);
+    if (e != cudaSuccess) return cuda_fail(e, "dist order");
+    // ---- lookahead: panel K+1 on the side stream once its columns are updated
+    if (has_next) {
+      bool mine = false;
+      for (auto& v : views) mine = mine || v.plan.rank == owner1;
+      if (mine) {
+        e = cudaStreamWaitEvent(side, d->ev_next, 0);
+        if (e == cudaSuccess) e = prepare_panel(K + 1);
+        if (e != cudaSuccess) return cuda_fail(e, "dist panel");
+      }
     }
   }
-  if (d->comm && d->nranks > 1) {
+  // join the side stream back into the caller's
+  e = cudaEventRecord(d->ev_side, side);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, d->ev_side, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "dist join");
+  if (real) {
     // first failing step over all owners: min over nonzero info words
     info_to_min_kernel<<<1, 1, 0, s>>>(info);
     ncclResult_t r = nccl().AllReduce(info, info, 1, ncclInt64, ncclMin, d->comm, s);
@@ -282,6 +372,7 @@ void dist_release(ebv_context* c) {   // called by ebv_destroy
   if (!c || !c->dist) return;
   if (c->dist->comm && nccl().ok) nccl().CommDestroy(c->dist->comm);
   if (c->dist->pbuf) cudaFree(c->dist->pbuf);
+  release_events(c->dist);
   delete c->dist;
   c->dist = nullptr;
 }
@@ -390,8 +481,9 @@ ebv_status_t ebv_lu_factor_dist_emulated(ebv_context_t c, int64_t n, int nranks,
   std::vector<View> views;
   for (int r = 0; r < nranks; r++) views.push_back(View{make_plan(n, nb, r, nranks, layout), slabs[r], lda});
   st = dist_factor(c, &tmp, views, n, d_info, s);
-  cudaStreamSynchronize(s);   // the temporary panel buffer dies with tmp
+  cudaStreamSynchronize(s);   // the temporary panel buffers / events die with tmp
   if (tmp.pbuf) cudaFree(tmp.pbuf);
+  release_events(&tmp);
   return st;
 }
 
