@@ -12,6 +12,18 @@ import torch
 import ebv_inputs
 import oracle
 
+def bits_eq(a, b):
+    """Bitwise equality (IEEE bit patterns, so -0.0 != +0.0 and NaN payloads
+    count), not just numeric equality."""
+    a = np.ascontiguousarray(np.asarray(a))
+    b = np.ascontiguousarray(np.asarray(b))
+    if a.shape != b.shape or a.dtype != b.dtype:
+        return False
+    if a.dtype == np.float64:
+        return np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    return np.array_equal(a, b)
+
+
 pytestmark = pytest.mark.gpu
 ebv = pytest.importorskip("paper_1907_05767_b200")
 
@@ -66,15 +78,15 @@ def test_emulated_dist_factor_and_solve_bitwise(dev, ctx, P, nb, layout, n):
     lu_g = assemble(slabs, colmaps, n)
     lu_o, info_o = oracle.lu_factor(d["At"].T.cpu().numpy())
     assert int(info) == info_o == 0
-    assert np.array_equal(lu_g, lu_o)
+    assert bits_eq(lu_g, lu_o)
     x_o = oracle.lu_solve(lu_o, d["B"].cpu().numpy())
-    assert np.array_equal(B.T.cpu().numpy(), x_o)
+    assert bits_eq(B.T.cpu().numpy(), x_o)
     # the one-GPU blocked schedule with the same block width is the same computation
     ctx.set_block(nb)
     LU1, _ = ebv.lu_factor(d["At"].T, ctx=ctx)
     ctx.set_block(0)
     torch.cuda.synchronize()
-    assert np.array_equal(LU1.cpu().numpy(), lu_g)
+    assert bits_eq(LU1.cpu().numpy(), lu_g)
 
 
 def test_emulated_dist_info(dev, ctx):
@@ -108,8 +120,8 @@ def test_real_nccl_single_rank(dev):
         assert ebv.ebv_lu_solve_dist(h, n, slab.data_ptr(), n, B.data_ptr(), n, 1, sh) == 0, ebv.ebv_last_error()
         torch.cuda.synchronize()
         lu_o, _ = oracle.lu_factor(d["At"].T.cpu().numpy())
-        assert np.array_equal(slab.T.cpu().numpy(), lu_o)
-        assert np.array_equal(B.T.cpu().numpy(), oracle.lu_solve(lu_o, d["B"].cpu().numpy()))
+        assert bits_eq(slab.T.cpu().numpy(), lu_o)
+        assert bits_eq(B.T.cpu().numpy(), oracle.lu_solve(lu_o, d["B"].cpu().numpy()))
         assert int(info) == 0
     finally:
         ebv.ebv_destroy(h)

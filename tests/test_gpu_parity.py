@@ -16,6 +16,18 @@ import ebv_inputs
 import oracle
 from oracle import closed_form
 
+def bits_eq(a, b):
+    """Bitwise equality (IEEE bit patterns, so -0.0 != +0.0 and NaN payloads
+    count), not just numeric equality."""
+    a = np.ascontiguousarray(np.asarray(a))
+    b = np.ascontiguousarray(np.asarray(b))
+    if a.shape != b.shape or a.dtype != b.dtype:
+        return False
+    if a.dtype == np.float64:
+        return np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    return np.array_equal(a, b)
+
+
 pytestmark = pytest.mark.gpu
 
 ebv = pytest.importorskip("paper_1907_05767_b200")
@@ -72,7 +84,7 @@ def test_blocked_factor_bitwise(dev, ctx, n):
     lu_g, info = run_factor(ctx, A)
     lu_o, info_o = oracle.lu_factor(A.cpu().numpy())
     assert info == info_o == 0
-    assert np.array_equal(lu_g, lu_o)
+    assert bits_eq(lu_g, lu_o)
 
 
 @pytest.mark.parametrize("nb", [64, 128, 192, 512, -1])
@@ -82,7 +94,7 @@ def test_blocked_schedules_bitwise(dev, ctx, nb):
     A = d["At"].T
     lu_g, _ = run_factor(ctx, A, nb=nb)
     lu_o, _ = oracle.lu_factor(A.cpu().numpy())
-    assert np.array_equal(lu_g, lu_o)
+    assert bits_eq(lu_g, lu_o)
 
 
 @pytest.mark.parametrize("leaf", [8, 16, 24, 32, 48])
@@ -92,7 +104,7 @@ def test_blocked_factor_leaf_sizes_bitwise(dev, ctx, leaf):
     A = d["At"].T
     lu_g, _ = run_factor(ctx, A, leaf=leaf)
     lu_o, _ = oracle.lu_factor(A.cpu().numpy())
-    assert np.array_equal(lu_g, lu_o)
+    assert bits_eq(lu_g, lu_o)
 
 
 def test_blocked_factor_2048_bitwise_and_tolerance(dev, ctx):
@@ -102,7 +114,7 @@ def test_blocked_factor_2048_bitwise_and_tolerance(dev, ctx):
     lu_g, _ = run_factor(ctx, A)
     lu_o, _ = oracle.lu_factor(A.cpu().numpy())
     assert tol_ok(lu_g, lu_o)
-    assert np.array_equal(lu_g, lu_o)
+    assert bits_eq(lu_g, lu_o)
 
 
 def test_leading_dimension_and_odd_strides(dev, ctx):
@@ -115,7 +127,7 @@ def test_leading_dimension_and_odd_strides(dev, ctx):
     LU, info = ebv.lu_factor(A, ctx=ctx, inplace=True)
     torch.cuda.synchronize()
     lu_o, _ = oracle.lu_factor(d["At"].T.cpu().numpy())
-    assert np.array_equal(store.T[:n, :].cpu().numpy(), lu_o)
+    assert bits_eq(store.T[:n, :].cpu().numpy(), lu_o)
     assert not store[:, n:].any()      # padding untouched
 
 
@@ -123,7 +135,7 @@ def test_determinism(dev, ctx):
     d = ebv_inputs.generate(777, seed=5, device=dev)
     a, _ = run_factor(ctx, d["At"].T)
     b, _ = run_factor(ctx, d["At"].T)
-    assert np.array_equal(a, b)
+    assert bits_eq(a, b)
 
 
 # ------------------------------------------------------------------ pivots / info
@@ -172,7 +184,7 @@ def test_solve_bitwise(dev, ctx, n, nrhs):
     torch.cuda.synchronize()
     lu_o, _ = oracle.lu_factor(A.cpu().numpy())
     x_o = oracle.lu_solve(lu_o, d["B"].cpu().numpy())
-    assert np.array_equal(X.cpu().numpy(), x_o)
+    assert bits_eq(X.cpu().numpy(), x_o)
     assert np.max(np.abs(X.cpu().numpy() - d["X"].cpu().numpy())) <= 1e-10
 
 
@@ -196,7 +208,7 @@ def test_vector_path_bitwise(dev, ctx, n, ctas):
     lu_g, info = run_factor(ctx, A, path=ebv.EBV_PATH_VECTOR, vector_ctas=ctas)
     lu_o, info_o = oracle.lu_factor(A.cpu().numpy())
     assert info == info_o
-    assert np.array_equal(lu_g, lu_o)
+    assert bits_eq(lu_g, lu_o)
 
 
 # ------------------------------------------------------------------ batched
@@ -213,10 +225,10 @@ def test_batched_bitwise(dev, ctx, n, batch, nrhs):
     a = db["At"].transpose(1, 2).cpu().numpy()
     b = db["B"][:, :, :nrhs].cpu().numpy() if nrhs else None
     lu_o, x_o, info_o = oracle.lu_factor_batched(a, b)
-    assert np.array_equal(info.cpu().numpy(), info_o)
-    assert np.array_equal(At.transpose(1, 2).cpu().numpy(), lu_o)
+    assert bits_eq(info.cpu().numpy(), info_o)
+    assert bits_eq(At.transpose(1, 2).cpu().numpy(), lu_o)
     if nrhs:
-        assert np.array_equal(Bt.transpose(1, 2).cpu().numpy(), x_o)
+        assert bits_eq(Bt.transpose(1, 2).cpu().numpy(), x_o)
 
 
 def test_batched_full_size_c5(dev, ctx):
@@ -229,8 +241,8 @@ def test_batched_full_size_c5(dev, ctx):
     torch.cuda.synchronize()
     lu_o, x_o, info_o = oracle.lu_factor_batched(db["At"].transpose(1, 2).cpu().numpy(), db["B"].cpu().numpy())
     assert not info.any().item()
-    assert np.array_equal(At.transpose(1, 2).cpu().numpy(), lu_o)
-    assert np.array_equal(Bt.transpose(1, 2).cpu().numpy(), x_o)
+    assert bits_eq(At.transpose(1, 2).cpu().numpy(), lu_o)
+    assert bits_eq(Bt.transpose(1, 2).cpu().numpy(), x_o)
 
 
 def test_batched_singular_systems(dev, ctx):
@@ -287,7 +299,7 @@ def test_c3_n8192_leading_submatrix_and_backward_error(dev, ctx):
     X = ebv.lu_solve(LU, d["B"], ctx=ctx)
     torch.cuda.synchronize()
     lu_o, _ = oracle.lu_factor(A[:m, :m].cpu().numpy())
-    assert np.array_equal(LU[:m, :m].cpu().numpy(), lu_o)
+    assert bits_eq(LU[:m, :m].cpu().numpy(), lu_o)
     assert (X - d["X"]).abs().max().item() <= 1e-10
     r = ((A @ X - d["B"]).abs().max() / (A.abs().sum(1).max() * X.abs().max())).item()
     assert r <= 1e-12
@@ -305,7 +317,7 @@ def test_c4_n32768_properties(dev, ctx):
     torch.cuda.synchronize()
     assert int(info) == 0
     lu_o, _ = oracle.lu_factor(A[:m, :m].cpu().numpy())
-    assert np.array_equal(LU[:m, :m].cpu().numpy(), lu_o)
+    assert bits_eq(LU[:m, :m].cpu().numpy(), lu_o)
     assert (x - d["X"][:, 0]).abs().max().item() <= 1e-10
     g = torch.Generator(device="cpu").manual_seed(0)
     ii = torch.randint(0, n, (2000,), generator=g).tolist()
@@ -337,6 +349,6 @@ def test_graph_replay_bitwise(dev, ctx):
             assert st == 0, ebv.ebv_last_error()
             counts.append(ctx.launch_count() - c0)
             s.synchronize()
-            assert np.array_equal(Aw.T.cpu().numpy(), lu_o), rep
+            assert bits_eq(Aw.T.cpu().numpy(), lu_o), rep
             assert int(info) == 0
     assert counts[0] == counts[2] == counts[3] > 10
