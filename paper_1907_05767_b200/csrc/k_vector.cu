@@ -2,136 +2,322 @@
 // Eq 6-a..c executed step by step, with the EbV equal-length
 // pairing (Eq 7) as the column -> CTA owner map.
 //
-// One persistent cooperative kernel.  CTA b owns the columns of the pairs
-// p = b, b+C, b+2C, ... where pair p = {p, n-1-p} (first with last: the two
-// columns' on-or-below-diagonal lengths sum to n+1, so every CTA holds the
-// same number of matrix entries — reading R12), and keeps them resident in
-// shared memory for the whole factorization.  Step k:
-//   * the owner of column k has applied updates 0..k-1 to it; it divides the
-//     sub-diagonal part by the pivot (Eq 6-a: the L_(k) vector), writes the
-//     column to A (its final value) and publishes flag[k] (release);
-//   * every CTA acquires flag[k], reads L_(k) from L2 and applies the rank-1
-//     update a_ij = fma(-l_ik, u_kj, a_ij) (Eq 6-c, u_kj = its own row-k
-//     entry, the U_(k) vector of Eq 6-b) to its owned columns j > k.
-// Lookahead: the owner of column k+1 updates that column first and publishes
-// L_(k+1) before touching its other columns, so the dependent chain per step
-// is one column update + one division + one flag hop.
-// Per entry the arithmetic is the oracle's (bitwise); `cyclic` selects the
-// plain j mod C owner map for comparison.
-#include <cooperative_groups.h>
-
+// One persistent cooperative kernel.  Columns are grouped in blocks of bw
+// consecutive columns; block pairs {J, Nb-1-J} (first with last: the paired
+// blocks' on-or-below-diagonal lengths sum to a constant, reading R12) are
+// dealt round-robin to the CTAs, which keep their columns resident in shared
+// memory for the whole factorization.  Block J's steps k:
+//   * the owner of block J runs them locally: Eq 6-a on column k (the L_(k)
+//     vector), Eq 6-c on the block's later columns with the U_(k) row
+//     entries it holds, writes the block's columns to A and publishes one
+//     release flag per block;
+//   * every other CTA acquires the flag, reads the block's L_(k) vectors from
+//     L2 and applies the bw rank-1 updates, in ascending k, to its columns
+//     of later blocks.
+// Lookahead: the owner of block J+1 applies block J to that block first,
+// then factors and publishes it, and only then updates its remaining
+// columns — so the dependent chain per block is one flag hop plus bw local
+// steps.  Inside a block the owner factors the bw x bw diagonal block in one
+// warp (shuffles carry the pivot row), then every row below runs the bw
+// steps in its own thread, dividing by a hoisted reciprocal with a verified
+// Markstein correction (true division when unverified).  Per entry the
+// arithmetic is the oracle's (bitwise); `cyclic` selects the plain J mod C
+// block map for comparison.  Measured per-block chain (probes/vector_trace,
+// n = 1024): flag hop ~0.5 us, apply ~3.5 us, diagonal block ~3 us (eight
+// dependent divisions), rows below ~3.5 us.
 #include "ebv_internal.cuh"
+
+#include <type_traits>
 
 namespace ebv {
 namespace {
 
-constexpr int VT = 256;   // threads per CTA
+constexpr int VT = 512;   // threads per CTA
 
-__device__ __forceinline__ int ld_relaxed(const int* p) {
-  int v;
-  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-// relaxed polls (an acquire load costs an L1 invalidation per poll on
-// sm_100a), then one acquire fence
-__device__ __forceinline__ void wait_flag(const int* p, int v) {
-  while (ld_relaxed(p) != v) __nanosleep(32);
-  asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-}
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
+// acquire polls: the invalidation of L1 an acquire load implies costs
+// nothing here (the CTA reads other CTAs' data only through L2), and it
+// saves the extra round trip of a relaxed poll followed by a fence
+__device__ __forceinline__ void wait_flag(const int* p, int v) {
+  int t;
+  do {
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(t) : "l"(p) : "memory");
+  } while (t != v);
+}
 
-__device__ __forceinline__ int owner_of(int j, int n, int C, int cyclic) {
-  if (cyclic) return j % C;
-  int p = j < n - 1 - j ? j : n - 1 - j;
+// q = RN(y/u) from r = RN(1/u) by one Markstein correction; `ok` is cleared
+// unless the exact remainder proves q correctly rounded (then the caller
+// redoes the row with true division) — same test as k_solve.cu's quot().
+__device__ __forceinline__ double quot(double y, double u, double r, bool& ok) {
+  const double q0 = y * r;
+  const double q = fma(r, fma(-u, q0, y), q0);
+  const double rr = fma(-u, q, y);
+  const long long qb = __double_as_longlong(q);
+  const long long e = qb & 0x7ff0000000000000LL;
+  const bool normal = e > (54LL << 52) && e < (0x7feLL << 52);
+  double lim = fabs(u) * __longlong_as_double(e - (53LL << 52));
+  const bool below = (rr < 0.0) != (u < 0.0);
+  const bool pow2 = (qb & 0x000fffffffffffffLL) == 0;
+  if (pow2 && below == (q > 0.0)) lim *= 0.5;
+  ok = ok && normal && fabs(rr) < lim;
+  return q;
+}
+
+__device__ __forceinline__ int block_owner(int J, int Nb, int C, int cyclic) {
+  if (cyclic) return J % C;
+  int p = J < Nb - 1 - J ? J : Nb - 1 - J;
   return p % C;
 }
 
+#ifdef EBV_VECTOR_TRACE
+// probes/vector_trace.cu: per-block phase timestamps (%globaltimer, ns)
+__device__ unsigned long long g_vtrace[2048][6];
+#define EBV_VTR(J, slot)                                                            \
+  do {                                                                             \
+    __syncthreads();                                                               \
+    if (tid == 0 && (J) < 2048) {                                                  \
+      unsigned long long t;                                                        \
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));                        \
+      g_vtrace[J][slot] = t;                                                       \
+    }                                                                              \
+  } while (0)
+#else
+#define EBV_VTR(J, slot) \
+  do {                   \
+  } while (0)
+#endif
+
+constexpr int BWMAX = 8;   // block width limit
+
+// The kernel body runs once per block with little work per thread, so it is
+// instruction-fetch sensitive: loops over rows and columns stay rolled and
+// only the bw-long step loops are unrolled (a fully unrolled variant was 10k
+// SASS instructions and 8x slower per block).
 __global__ void __launch_bounds__(VT, 1)
     vector_lu_kernel(int n, double* __restrict__ A, int64_t lda, const double* __restrict__ tau,
-                     unsigned long long* info_min, int* flags, int epoch, int cyclic, int maxcols) {
-  extern __shared__ double sm[];
-  const int C = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
-  double* sl = sm;                         // L_(k) of the current step (n)
-  double* scol = sm + n;                   // owned columns [maxcols][n]
-  __shared__ int cols[512];
+                     unsigned long long* info_min, int* flags, int epoch, int cyclic, int bw, int maxcols) {
+  extern __shared__ double scol[];         // owned columns [maxcols][n]
+  __shared__ int cols[1024];               // owned global column indices (ascending)
+  __shared__ double srcp[BWMAX];           // RN(1/u_kk) of the block being factored
   __shared__ int ncols_s;
+  const int C = gridDim.x, me = blockIdx.x, tid = threadIdx.x;
+  const int Nb = (n + bw - 1) / bw;
   if (tid == 0) {
     int c = 0;
-    for (int j = 0; j < n; j++)
-      if (owner_of(j, n, C, cyclic) == b) cols[c++] = j;
+    for (int J = 0; J < Nb; J++)
+      if (block_owner(J, Nb, C, cyclic) == me)
+        for (int j = J * bw; j < n && j < (J + 1) * bw; j++) cols[c++] = j;
     ncols_s = c;
   }
   __syncthreads();
   const int ncols = ncols_s;
   for (int c = 0; c < ncols; c++)
-    for (int i = tid; i < n; i += VT) scol[c * n + i] = A[i + (int64_t)cols[c] * lda];
+    for (int i = tid; i < n; i += VT) scol[(size_t)c * n + i] = A[i + (int64_t)cols[c] * lda];
   __syncthreads();
   const double tv = *tau;
 
-  // local slot of global column j, or -1
-  auto slot_of = [&](int j) -> int {
-    if (owner_of(j, n, C, cyclic) != b) return -1;
-    int lo = 0, hi = ncols - 1;
-    while (lo <= hi) {
+  // slot of the first owned column >= j (columns are ascending)
+  auto first_slot = [&](int j) -> int {
+    int lo = 0, hi = ncols;
+    while (lo < hi) {
       int mid = (lo + hi) >> 1;
-      if (cols[mid] == j) return mid;
-      if (cols[mid] < j) lo = mid + 1; else hi = mid - 1;
+      if (cols[mid] < j) lo = mid + 1; else hi = mid;
     }
-    return -1;
-  };
-  // Eq 6-a on an owned column + publish: the L_(k) vector becomes final
-  auto publish = [&](int k, int c) {
-    double* col = scol + c * n;
-    const double piv = col[k];
-    if (tid == 0 && fabs(piv) <= tv) atomicMin(info_min, (unsigned long long)(k + 1));
-    for (int i = k + 1 + tid; i < n; i += VT) col[i] = col[i] / piv;
-    __syncthreads();
-    for (int i = tid; i < n; i += VT) A[i + (int64_t)k * lda] = col[i];
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) st_release(flags + k, epoch);
+    return lo;
   };
 
-  {
-    int c0 = slot_of(0);
-    if (c0 >= 0) publish(0, c0);
-  }
-  int first = 0;   // owned columns < first are finished (j <= k)
-  for (int k = 0; k < n - 1; k++) {
-    const int ck = slot_of(k);
-    const double* l;
-    if (ck >= 0) {
-      l = scol + ck * n;            // the owner already holds L_(k)
-    } else {
-      if (tid == 0) wait_flag(flags + k, epoch);
-      __syncthreads();
-      for (int i = k + 1 + tid; i < n; i += VT) sl[i] = __ldcg(A + i + (int64_t)k * lda);
-      __syncthreads();
-      l = sl;
-    }
-    while (first < ncols && cols[first] <= k) first++;
-    // lookahead: column k+1 first
-    const int cn = slot_of(k + 1);
-    if (cn >= 0) {
-      double* col = scol + cn * n;
-      const double u = col[k];
-      for (int i = k + 1 + tid; i < n; i += VT) col[i] = fma(-l[i], u, col[i]);
-      __syncthreads();
-      publish(k + 1, cn);
-    }
-    // Eq 6-c on the remaining owned columns j > k+1
-    for (int c = first; c < ncols; c++) {
-      if (c == cn) continue;
-      double* col = scol + c * n;
-      const double u = col[k];
-      for (int i = k + 1 + tid; i < n; i += VT) col[i] = fma(-l[i], u, col[i]);
+  // Apply the steps k0..k1-1 (block J's L_(k) vectors at lsrc + (k-k0)*n) to
+  // owned columns in slots [c0, c1) (Eq 6-c).  Every entry still receives
+  // its fma's in ascending k: phase A finishes rows k0+1..k1-1 of each
+  // column (the U_(k) row entries the later steps multiply by), phase B then
+  // runs each row i >= k1 through all of the block's steps.
+  auto apply = [&](int k0, int k1, const double* lsrc, int64_t lstr, int c0, int c1) {
+    if (c0 >= c1) return;
+    const int nbk = k1 - k0;
+#pragma unroll 1
+    for (int c = c0 + tid; c < c1; c += VT) {      // phase A: one thread per column
+      double* col = scol + (size_t)c * n + k0;
+      double a[BWMAX];
+#pragma unroll
+      for (int ii = 0; ii < BWMAX; ii++) a[ii] = ii < nbk ? col[ii] : 0.0;
+#pragma unroll
+      for (int kk = 0; kk < BWMAX - 1; kk++)
+#pragma unroll
+        for (int ii = kk + 1; ii < BWMAX; ii++)
+          if (ii < nbk) a[ii] = fma(-lsrc[kk * lstr + k0 + ii], a[kk], a[ii]);
+#pragma unroll
+      for (int ii = 1; ii < BWMAX; ii++)
+        if (ii < nbk) col[ii] = a[ii];
     }
     __syncthreads();
+#pragma unroll 1
+    for (int i = k1 + tid; i < n; i += VT) {       // phase B: rows >= k1
+      double l[BWMAX];
+#pragma unroll
+      for (int kk = 0; kk < BWMAX; kk++) l[kk] = kk < nbk ? lsrc[kk * lstr + i] : 0.0;
+      int c = c0;
+#pragma unroll 1
+      for (; c + 3 < c1; c += 4) {                 // four independent chains per thread
+        double* p0 = scol + (size_t)c * n;
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) v[q] = p0[(size_t)q * n + i];
+#pragma unroll
+        for (int kk = 0; kk < BWMAX; kk++)
+          if (kk < nbk)
+#pragma unroll
+            for (int q = 0; q < 4; q++) v[q] = fma(-l[kk], p0[(size_t)q * n + k0 + kk], v[q]);
+#pragma unroll
+        for (int q = 0; q < 4; q++) p0[(size_t)q * n + i] = v[q];
+      }
+#pragma unroll 1
+      for (; c < c1; c++) {
+        double* p0 = scol + (size_t)c * n;
+        double v0 = p0[i];
+#pragma unroll
+        for (int kk = 0; kk < BWMAX; kk++)
+          if (kk < nbk) v0 = fma(-l[kk], p0[k0 + kk], v0);
+        p0[i] = v0;
+      }
+    }
+    __syncthreads();
+  };
+
+  // Factor owned block J (its columns are up to date through step J*bw-1),
+  // write its rows >= J*bw to A and publish flag[J].  Phase A: the bw x bw
+  // diagonal block by the first bw lanes of warp 0 (row k0+r per lane, Eq
+  // 6-a/6-c with the pivot row broadcast by shuffles, Eq 6-b); phase B:
+  // every row i >= k1 through the block's steps in its own thread — per
+  // entry the same fma chain then division as the step-by-step order.
+  auto factor_block = [&](int J) {
+    const int k0 = J * bw, k1 = min(n, (J + 1) * bw), nbk = k1 - k0;
+    const int s0 = first_slot(k0);
+    EBV_VTR(J, 1);
+    double* blk = scol + (size_t)s0 * n;           // column c of the block at blk + c*n
+    if (tid < 32) {
+      const int r = tid;
+      double a[BWMAX];
+#pragma unroll
+      for (int c = 0; c < BWMAX; c++) a[c] = (r < nbk && c < nbk) ? blk[(size_t)c * n + k0 + r] : 0.0;
+#pragma unroll
+      for (int kk = 0; kk < BWMAX; kk++) {
+        if (kk < nbk) {
+          const double piv = __shfl_sync(0xffffffffu, a[kk], kk);
+          if (r == 0 && fabs(piv) <= tv) atomicMin(info_min, (unsigned long long)(k0 + kk + 1));
+          const bool below = r > kk && r < nbk;
+          if (below) a[kk] = a[kk] / piv;                               // Eq 6-a
+#pragma unroll
+          for (int c = kk + 1; c < BWMAX; c++) {
+            const double u = __shfl_sync(0xffffffffu, a[c], kk);        // Eq 6-b
+            if (below && c < nbk) a[c] = fma(-a[kk], u, a[c]);          // Eq 6-c
+          }
+        }
+      }
+      if (r < nbk) {
+#pragma unroll
+        for (int c = 0; c < BWMAX; c++)
+          if (c < nbk) {
+            blk[(size_t)c * n + k0 + r] = a[c];
+            A[k0 + r + (int64_t)(k0 + c) * lda] = a[c];
+          }
+        double d = a[0];
+#pragma unroll
+        for (int c = 1; c < BWMAX; c++)
+          if (c == r) d = a[c];
+        srcp[r] = 1.0 / d;
+      }
+    }
+    __syncthreads();
+    EBV_VTR(J, 2);
+    // rows below: the quotient from the hoisted reciprocal, verified; rows
+    // with an unverified step are redone with true division
+    // (two rows per thread at a time, for overlap of their dependent chains)
+    auto below_rows = [&](int i0, auto exact_tag) {
+      constexpr bool exact = decltype(exact_tag)::value;
+      double a[2][BWMAX];
+      bool ok[2] = {true, true};
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int i = i0 + h * VT;
+#pragma unroll
+        for (int c = 0; c < BWMAX; c++) a[h][c] = (c < nbk && i < n) ? blk[(size_t)c * n + i] : 0.0;
+      }
+#pragma unroll
+      for (int kk = 0; kk < BWMAX; kk++) {
+        if (kk < nbk) {
+          const double u = blk[(size_t)kk * n + k0 + kk], rp = srcp[kk];
+#pragma unroll
+          for (int h = 0; h < 2; h++) a[h][kk] = exact ? a[h][kk] / u : quot(a[h][kk], u, rp, ok[h]);   // Eq 6-a
+#pragma unroll
+          for (int c = kk + 1; c < BWMAX; c++)
+            if (c < nbk) {
+              const double uc = blk[(size_t)c * n + k0 + kk];
+#pragma unroll
+              for (int h = 0; h < 2; h++) a[h][c] = fma(-a[h][kk], uc, a[h][c]);                    // Eq 6-c
+            }
+        }
+      }
+      const bool good = ok[0] && (ok[1] || i0 + VT >= n);
+      if (good) {
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int i = i0 + h * VT;
+          if (i < n)
+#pragma unroll
+            for (int c = 0; c < BWMAX; c++)
+              if (c < nbk) {
+                blk[(size_t)c * n + i] = a[h][c];
+                A[i + (int64_t)(k0 + c) * lda] = a[h][c];
+              }
+        }
+      }
+      return good;
+    };
+#pragma unroll 1
+    for (int i = k1 + tid; i < n; i += 2 * VT)
+      if (!below_rows(i, std::false_type{})) below_rows(i, std::true_type{});
+    __syncthreads();
+    EBV_VTR(J, 3);
+    if (tid == 0) st_release(flags + J, epoch);
+    EBV_VTR(J, 4);
+  };
+
+  if (block_owner(0, Nb, C, cyclic) == me) factor_block(0);
+  for (int J = 0; J < Nb - 1; J++) {
+    const int k0 = J * bw, k1 = min(n, (J + 1) * bw);
+    const int c1 = first_slot(k1);                  // first owned column after block J
+    if (c1 >= ncols) break;                         // nothing of mine is updated by block J or later
+    const double* lsrc;
+    int64_t lstr = n;
+    if (block_owner(J, Nb, C, cyclic) == me) {
+      lsrc = scol + (size_t)first_slot(k0) * n;    // block J's columns, final here
+    } else {
+      if (tid == 0) wait_flag(flags + J, epoch);
+      __syncthreads();
+      // read its L_(k) vectors in place from L2: the acquire above ordered
+      // them, and the acquire's L1 invalidation leaves no stale line (staging
+      // them in shared memory first cost a further ~4 us per block)
+      lsrc = A + (int64_t)k0 * lda;
+      lstr = lda;
+    }
+    if (block_owner(J + 1, Nb, C, cyclic) == me) {
+      EBV_VTR(J + 1, 0);
+      // lookahead: block J+1 first, factor + publish it, then the rest
+      const int c2 = first_slot(min(n, (J + 2) * bw));
+      apply(k0, k1, lsrc, lstr, c1, c2);
+      factor_block(J + 1);
+      apply(k0, k1, lsrc, lstr, c2, ncols);
+    } else {
+      apply(k0, k1, lsrc, lstr, c1, ncols);
+    }
   }
-  for (int c = 0; c < ncols; c++)
-    for (int i = tid; i < n; i += VT) A[i + (int64_t)cols[c] * lda] = scol[c * n + i];
+  // the U part (rows above each owned block) was completed in shared memory
+  for (int c = 0; c < ncols; c++) {
+    const int j = cols[c], top = (j / bw) * bw;
+    for (int i = tid; i < top; i += VT) A[i + (int64_t)j * lda] = scol[(size_t)c * n + i];
+  }
 }
 
 __global__ void info_finalize_kernel(const unsigned long long* info_min, int64_t* info) {
@@ -139,33 +325,53 @@ __global__ void info_finalize_kernel(const unsigned long long* info_min, int64_t
   *info = (v == ~0ull) ? 0 : (int64_t)v;
 }
 
-int max_cols(int64_t n, int C, int cyclic) {
-  if (cyclic) return (int)((n + C - 1) / C);
-  int64_t pairs = (n + 1) / 2;
-  return (int)(2 * ((pairs + C - 1) / C));
+int max_cols(int64_t n, int C, int cyclic, int bw) {
+  const int64_t Nb = (n + bw - 1) / bw;
+  if (cyclic) return (int)(((Nb + C - 1) / C) * bw);
+  const int64_t pairs = (Nb + 1) / 2;
+  return (int)(2 * ((pairs + C - 1) / C) * bw);
+}
+
+int clamp_ctas(int64_t n, int num_ctas, int bw) {
+  const int cyclic = num_ctas < 0 ? 1 : 0;
+  int C = num_ctas < 0 ? -num_ctas : num_ctas;
+  const int64_t Nb = (n + bw - 1) / bw;
+  const int64_t units = cyclic ? Nb : (Nb + 1) / 2;
+  if (C > units) C = (int)units;
+  if (C < 1) C = 1;
+  return C;
+}
+
+size_t smem_for(int64_t n, int num_ctas, int bw) {
+  const int cyclic = num_ctas < 0 ? 1 : 0;
+  const int C = clamp_ctas(n, num_ctas, bw);
+  return (size_t)max_cols(n, C, cyclic, bw) * n * 8;
+}
+
+// largest block width in {8, 4, 2, 1} whose shared-memory image fits
+int pick_bw(int64_t n, int num_ctas) {
+  int smem_max = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  for (int bw = 8; bw >= 1; bw >>= 1)
+    if (max_cols(n, clamp_ctas(n, num_ctas, bw), num_ctas < 0, bw) <= 1024 &&
+        smem_for(n, num_ctas, bw) + 9000 <= (size_t)smem_max)
+      return bw;
+  return 0;
 }
 
 }  // namespace
 
 size_t vector_smem_bytes(int64_t n, int num_ctas) {
-  const int cyclic = num_ctas < 0 ? 1 : 0;
-  int C = num_ctas < 0 ? -num_ctas : num_ctas;
-  if (C > (n + 1) / 2 && !cyclic) C = (int)((n + 1) / 2);
-  if (C > n) C = (int)n;
-  if (C < 1) C = 1;
-  return ((size_t)max_cols(n, C, cyclic) * n + n) * 8;
+  const int bw = pick_bw(n, num_ctas);
+  return bw ? smem_for(n, num_ctas, bw) : (size_t)1 << 40;
 }
 
 int vector_max_ctas(int device, int64_t n) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  // prefer a CTA count dividing the number of pairs (even per-step balance),
-  // capped by one CTA per SM (cooperative residency)
-  int64_t pairs = (n + 1) / 2;
-  int best = sms < pairs ? sms : (int)pairs;
-  for (int c = best; c >= best * 3 / 4 && c >= 1; c--)
-    if (pairs % c == 0) return c;
-  return best < 1 ? 1 : best;
+  (void)n;
+  return sms;   // clamped to the number of block pairs at launch
 }
 
 cudaError_t launch_vector_lu(int64_t n, double* A, int64_t lda, const double* tau, int64_t* info, int* flags_ws,
@@ -179,19 +385,17 @@ cudaError_t launch_vector_lu(int64_t n, double* A, int64_t lda, const double* ta
     return cudaGetLastError();
   }
   const int cyclic = num_ctas < 0 ? 1 : 0;
-  int C = num_ctas < 0 ? -num_ctas : num_ctas;
-  if (C > (n + 1) / 2 && !cyclic) C = (int)((n + 1) / 2);
-  if (C > n) C = (int)n;
-  const int mc = max_cols(n, C, cyclic);
-  if (mc > 512) return cudaErrorInvalidValue;
-  const size_t smem = ((size_t)mc * n + n) * 8;
+  const int bw = pick_bw(n, num_ctas);
+  if (bw == 0) return cudaErrorInvalidValue;
+  const int C = clamp_ctas(n, num_ctas, bw);
+  const int mc = max_cols(n, C, cyclic, bw);
+  const size_t smem = smem_for(n, num_ctas, bw);
   e = cudaFuncSetAttribute(vector_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   static int epoch = 0;
   epoch = (epoch % 0x3FFFFFF0) + 1;
-  int nn = (int)n;
-  int ep = epoch;
-  void* args[] = {&nn, &A, &lda, (void*)&tau, &info_min, &flags_ws, &ep, (void*)&cyclic, (void*)&mc};
+  int nn = (int)n, ep = epoch, cy = cyclic, bwv = bw, mcv = mc;
+  void* args[] = {&nn, &A, &lda, (void*)&tau, &info_min, &flags_ws, &ep, &cy, &bwv, &mcv};
   e = cudaLaunchCooperativeKernel((void*)vector_lu_kernel, dim3(C), dim3(VT), args, smem, s);
   if (e != cudaSuccess) return e;
   info_finalize_kernel<<<1, 1, 0, s>>>(info_min, info);

@@ -201,7 +201,7 @@ def test_solve_vector_rhs_and_backward_error(dev, ctx):
 
 # ------------------------------------------------------------------ vector path (EbV owner map)
 @pytest.mark.parametrize("n,ctas", [(1, 0), (2, 0), (3, 0), (64, 0), (255, 0), (1024, 0), (1024, 128), (1024, -128),
-                                    (1000, 100), (1536, 0)])
+                                    (1000, 100), (1536, 0), (300, -7), (301, 5), (33, 1)])
 def test_vector_path_bitwise(dev, ctx, n, ctas):
     d = ebv_inputs.generate(n, seed=3 * n + 1, device=dev)
     A = d["At"].T
