@@ -369,7 +369,8 @@ def run_ebv(args, rank, world, local):
             "config": {"workload": f"dense diagonally dominant fp64 n={n}, {nrhs} rhs (BASELINE configs[3])",
                        "n": n, "nrhs": nrhs, "seed": args.seed,
                        "path": ("1D block-cyclic over %d GPUs, nb=%d, NCCL panel broadcast" % (world, nb)) if world > 1
-                       else "blocked right-looking nb=256, recursive panel, lookahead, TMA-fed DMMA update",
+                       else "blocked right-looking nb=%d (size-adaptive), recursive panel, lookahead, "
+                            "TMA-fed DMMA update" % ctx.block_width(n),
                        "parallelism": f"1d-block-cyclic x{world}" if world > 1 else "1 GPU",
                        "l2": "inputs (8.6 GB) larger than L2 (126 MB); no flush needed"},
             "factor_ms": statistics.median(f_ms), "solve_ms": statistics.median(s_ms),

@@ -116,6 +116,11 @@ ebv_status_t ebv_set_leaf(ebv_context_t ctx, int64_t leaf);
  * recursive 2 x 2 splitting.  All are bitwise identical. */
 ebv_status_t ebv_set_block(ebv_context_t ctx, int64_t nb);
 
+/* The column block width the blocked schedule will use for order n on this
+ * context (the ebv_set_block value, or the size-adaptive choice; -1 for the
+ * recursive schedule); 0 for a NULL ctx.  Host only, no device work. */
+int64_t ebv_block_width(ebv_context_t ctx, int64_t n);
+
 /* CUDA Graph replay of the blocked factor schedule (default on): the second
  * ebv_lu_factor call with identical arguments (same A / d_info pointers,
  * n, lda, tau and options, non-default stream) captures the schedule; later

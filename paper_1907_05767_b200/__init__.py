@@ -41,6 +41,7 @@ SIGNATURES = {
     "ebv_set_leaf": (_int, [_vp, _i64]),
     "ebv_set_vector_ctas": (_int, [_vp, _i64]),
     "ebv_set_block": (_int, [_vp, _i64]),
+    "ebv_block_width": (_i64, [_vp, _i64]),
     "ebv_set_lookahead": (_int, [_vp, _int]),
     "ebv_set_graphs": (_int, [_vp, _int]),
     "ebv_lu_factor": (_int, [_vp, _i64, _vp, _i64, _d, _vp, _vp]),
@@ -122,6 +123,10 @@ def ebv_set_leaf(ctx, leaf):
 
 def ebv_set_block(ctx, nb):
     return lib().ebv_set_block(ctx, nb)
+
+
+def ebv_block_width(ctx, n):
+    return lib().ebv_block_width(ctx, n)
 
 
 def ebv_set_lookahead(ctx, enable):
@@ -284,6 +289,10 @@ class Context:
 
     def set_block(self, nb: int):
         _check(ebv_set_block(self.handle, nb), "ebv_set_block")
+
+    def block_width(self, n: int) -> int:
+        """Column block width the blocked schedule uses at order n (-1: recursive)."""
+        return int(ebv_block_width(self.handle, n))
 
     def set_lookahead(self, on: bool):
         _check(ebv_set_lookahead(self.handle, on), "ebv_set_lookahead")

@@ -345,6 +345,11 @@ ebv_status_t ebv_set_leaf(ebv_context_t c, int64_t leaf) {
   return EBV_SUCCESS;
 }
 
+int64_t ebv_block_width(ebv_context_t c, int64_t n) {
+  if (!c) return 0;
+  return c->nb < 0 ? -1 : block_width(c, n);
+}
+
 ebv_status_t ebv_set_block(ebv_context_t c, int64_t nb) {
   if (!c) return invalid("ebv_set_block: NULL ctx");
   if (nb != 0 && nb != -1 && (nb < c->leaf || nb % c->leaf))

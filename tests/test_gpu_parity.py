@@ -199,6 +199,15 @@ def test_solve_vector_rhs_and_backward_error(dev, ctx):
     assert float(r) <= 1e-12
 
 
+def test_block_width_query(dev):
+    c = ebv.Context(0)
+    assert c.block_width(8192) == 128 and c.block_width(16384) == 256 and c.block_width(32768) == 512
+    c.set_block(192)
+    assert c.block_width(32768) == 192
+    c.set_block(-1)
+    assert c.block_width(1000) == -1
+
+
 # ------------------------------------------------------------------ vector path (EbV owner map)
 @pytest.mark.parametrize("n,ctas", [(1, 0), (2, 0), (3, 0), (64, 0), (255, 0), (1024, 0), (1024, 128), (1024, -128),
                                     (1000, 100), (1536, 0), (300, -7), (301, 5), (33, 1)])
