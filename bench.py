@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--nb", type=int, default=256, help="column block width of the multi-GPU layout")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the multi-GPU (1D block-cyclic + NCCL) schedule even on one rank")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE_M)
     return ap.parse_args()
@@ -218,10 +220,12 @@ def run_ebv(args, rank, world, local):
     stream = torch.cuda.current_stream(dev)
     sh = stream.cuda_stream
     info = torch.zeros((), dtype=torch.int64, device=dev)
-    if world > 1:
+    use_dist = world > 1 or args.force_dist
+    if use_dist:
         # one system over all ranks: 1D block-cyclic slabs, NCCL panel broadcast
         uid = [ebv.ebv_get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
+        if world > 1:
+            dist.broadcast_object_list(uid, src=0)
         handle = ebv.ebv_create_dist(local, uid[0], rank, world, nb, ebv.EBV_LAYOUT_CYCLIC)
         ctx = ebv.Context.__new__(ebv.Context)
         ctx.device, ctx.handle = local, handle
@@ -240,7 +244,7 @@ def run_ebv(args, rank, world, local):
     Bw = torch.empty_like(B0)
 
     def factor_solve():
-        if world > 1:
+        if use_dist:
             s = ebv.ebv_lu_factor_dist(ctx.handle, n, Aw.data_ptr(), n, 0.0, info.data_ptr(), sh)
             return s, lambda: ebv.ebv_lu_solve_dist(ctx.handle, n, Aw.data_ptr(), n, Bw.data_ptr(), n, nrhs, sh)
         s = ebv.ebv_lu_factor(ctx.handle, n, Aw.data_ptr(), n, 0.0, info.data_ptr(), sh)
@@ -368,10 +372,10 @@ def run_ebv(args, rank, world, local):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (ebv_inputs counter-hash DD generator, on device)",
             "config": {"workload": f"dense diagonally dominant fp64 n={n}, {nrhs} rhs (BASELINE configs[3])",
                        "n": n, "nrhs": nrhs, "seed": args.seed,
-                       "path": ("1D block-cyclic over %d GPUs, nb=%d, NCCL panel broadcast" % (world, nb)) if world > 1
+                       "path": ("1D block-cyclic over %d GPUs, nb=%d, NCCL panel broadcast" % (world, nb)) if use_dist
                        else "blocked right-looking nb=%d (size-adaptive), recursive panel, lookahead, "
                             "TMA-fed DMMA update" % ctx.block_width(n),
-                       "parallelism": f"1d-block-cyclic x{world}" if world > 1 else "1 GPU",
+                       "parallelism": f"1d-block-cyclic x{world}" if use_dist else "1 GPU",
                        "l2": "inputs (8.6 GB) larger than L2 (126 MB); no flush needed"},
             "factor_ms": statistics.median(f_ms), "solve_ms": statistics.median(s_ms),
             "factor_gflops": fl / (statistics.median(f_ms) / 1e3) / 1e9,

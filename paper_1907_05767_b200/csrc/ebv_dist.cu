@@ -148,6 +148,8 @@ struct ebv_dist_state {
   cudaEvent_t ev_free[2] = {nullptr, nullptr};    // step K done reading pbuf[K%2] (main)
   cudaEvent_t ev_next = nullptr;                  // block K+1 columns updated (main)
   cudaEvent_t ev_side = nullptr;                  // join point of the side stream
+  int* sws = nullptr;           // ring-solve workspace: per RHS group, the two sweeps' row-block
+  int64_t sws_cap = 0;          // flags, then one launch ticket per (window, sweep, group)
 };
 
 namespace {
@@ -297,53 +299,71 @@ ebv_status_t dist_factor(ebv_context* c, ebv_dist_state* d, std::vector<View>& v
   return EBV_SUCCESS;
 }
 
+// The ring solve.  Forward, K ascending: owner(K) receives the right-hand
+// side from owner(K-1), runs one window launch of the wavefront solve kernel
+// over its block column K (the diagonal block substituted, the rows below
+// updated by the block's columns, per entry in canonical order) and sends the
+// right-hand side on to owner(K+1).  Backward mirrors it with K descending.
+// Every entry sees the oracle's operation sequence (the ring visits the
+// column blocks in order), so X is bitwise the one-GPU result for every P.
 ebv_status_t dist_solve(ebv_context* c, ebv_dist_state* d, std::vector<View>& views, int64_t n, double* B,
                         int64_t ldb, int64_t nrhs, cudaStream_t s) {
   const Plan& p0 = views[0].plan;
   const int64_t nb = p0.nb, N = p0.N;
   const bool real = d->comm && d->nranks > 1;
   const size_t cnt = (size_t)(ldb * (nrhs - 1) + n);
+  if (n <= 0 || nrhs <= 0) return EBV_SUCCESS;
   auto find = [&](int64_t J) -> View* {
     for (auto& v : views)
       if (v.plan.rank == p0.owner(J)) return &v;
     return nullptr;
   };
-  cudaError_t e = cudaSuccess;
-  ncclResult_t r = ncclSuccess;
-  // forward: LY = B, blocks ascending
-  for (int64_t K = 0; K < N; K++) {
-    View* v = find(K);
-    if (!v) continue;
-    const int64_t c0 = K * nb, w = p0.width(K);
-    if (real && K > 0 && p0.owner(K - 1) != v->plan.rank) {
-      r = nccl().Recv(B, cnt, ncclFloat64, (int)p0.owner(K - 1), d->comm, s);
-      if (r != ncclSuccess) return nccl_fail(r, "ncclRecv(fwd)");
-    }
-    const double* Lk = v->A + v->plan.loc[K] * v->lda;
-    e = trsm_l(c, w, nrhs, Lk + c0, v->lda, B + c0, ldb, s);
-    if (e == cudaSuccess) e = gemm(c, n - c0 - w, nrhs, w, Lk + c0 + w, v->lda, B + c0, ldb, B + c0 + w, ldb, false, s);
-    if (e != cudaSuccess) return cuda_fail(e, "dist forward");
-    if (real && K + 1 < N && p0.owner(K + 1) != v->plan.rank) {
-      r = nccl().Send(B, cnt, ncclFloat64, (int)p0.owner(K + 1), d->comm, s);
-      if (r != ncclSuccess) return nccl_fail(r, "ncclSend(fwd)");
-    }
+  const int64_t G = solve_max_rhs();
+  const int64_t groups = (nrhs + G - 1) / G;
+  const int64_t NBr = (n + solve_block_rows() - 1) / solve_block_rows();
+  const int64_t nflags = 2 * NBr * groups, ntick = 2 * N * groups;
+  if (nflags + ntick > d->sws_cap) {
+    if (d->sws) cudaFree(d->sws);
+    d->sws = nullptr;
+    d->sws_cap = 0;
+    cudaError_t e = cudaMalloc(&d->sws, (nflags + ntick) * sizeof(int));
+    if (e != cudaSuccess) { set_error("ring-solve workspace alloc failed"); return EBV_ERR_ALLOC; }
+    e = cudaMemset(d->sws, 0, (nflags + ntick) * sizeof(int));
+    if (e != cudaSuccess) return cuda_fail(e, "ring-solve workspace");
+    d->sws_cap = nflags + ntick;
   }
-  // backward: UX = Y, blocks descending
-  for (int64_t K = N - 1; K >= 0; K--) {
-    View* v = find(K);
-    if (!v) continue;
-    const int64_t c0 = K * nb, w = p0.width(K);
-    if (real && K + 1 < N && p0.owner(K + 1) != v->plan.rank) {
-      r = nccl().Recv(B, cnt, ncclFloat64, (int)p0.owner(K + 1), d->comm, s);
-      if (r != ncclSuccess) return nccl_fail(r, "ncclRecv(bwd)");
-    }
-    const double* Uk = v->A + v->plan.loc[K] * v->lda;
-    e = trsm_lu(c, w, nrhs, Uk + c0, v->lda, B + c0, ldb, s);
-    if (e == cudaSuccess && c0 > 0) e = gemm(c, c0, nrhs, w, Uk, v->lda, B + c0, ldb, B, ldb, true, s);
-    if (e != cudaSuccess) return cuda_fail(e, "dist backward");
-    if (real && K > 0 && p0.owner(K - 1) != v->plan.rank) {
-      r = nccl().Send(B, cnt, ncclFloat64, (int)p0.owner(K - 1), d->comm, s);
-      if (r != ncclSuccess) return nccl_fail(r, "ncclSend(bwd)");
+  int* flags = d->sws;
+  int* tick = d->sws + nflags;
+  cudaError_t e = cudaMemsetAsync(tick, 0, ntick * sizeof(int), s);
+  if (e != cudaSuccess) return cuda_fail(e, "ring-solve tickets");
+  c->solve_epoch++;
+  const int ep = (int)(c->solve_epoch % 0x3FFFFFF0) + 1;
+  ncclResult_t r = ncclSuccess;
+  for (int pass = 0; pass < 2; pass++) {
+    const bool fwd = pass == 0;
+    for (int64_t t = 0; t < N; t++) {
+      const int64_t K = fwd ? t : N - 1 - t;
+      View* v = find(K);
+      if (!v) continue;
+      const int64_t c0 = K * nb, w = p0.width(K);
+      const int64_t prev = fwd ? K - 1 : K + 1, next = fwd ? K + 1 : K - 1;
+      if (real && prev >= 0 && prev < N && p0.owner(prev) != v->plan.rank) {
+        r = nccl().Recv(B, cnt, ncclFloat64, (int)p0.owner(prev), d->comm, s);
+        if (r != ncclSuccess) return nccl_fail(r, fwd ? "ncclRecv(fwd)" : "ncclRecv(bwd)");
+      }
+      const double* Lk = v->A + v->plan.loc[K] * v->lda;
+      for (int64_t g = 0; g < groups; g++) {
+        const int64_t r0 = g * G, nr = nrhs - r0 < G ? nrhs - r0 : G;
+        int* fl = flags + (g * 2 + pass) * NBr;
+        int* tk = tick + (g * 2 + pass) * N + K;
+        e = timed(c, KC_SOLVE, 2.0 * w * (fwd ? n - c0 : c0 + w) * nr, 8.0 * w * (fwd ? n - c0 : c0 + w), s, 1,
+                  [&] { return launch_solve_window(n, Lk, v->lda, c0, w, fwd, B + r0 * ldb, ldb, nr, tk, fl, ep, s); });
+        if (e != cudaSuccess) return cuda_fail(e, fwd ? "dist forward" : "dist backward");
+      }
+      if (real && next >= 0 && next < N && p0.owner(next) != v->plan.rank) {
+        r = nccl().Send(B, cnt, ncclFloat64, (int)p0.owner(next), d->comm, s);
+        if (r != ncclSuccess) return nccl_fail(r, fwd ? "ncclSend(fwd)" : "ncclSend(bwd)");
+      }
     }
   }
   if (real) {
@@ -372,6 +392,7 @@ void dist_release(ebv_context* c) {   // called by ebv_destroy
   if (!c || !c->dist) return;
   if (c->dist->comm && nccl().ok) nccl().CommDestroy(c->dist->comm);
   if (c->dist->pbuf) cudaFree(c->dist->pbuf);
+  if (c->dist->sws) cudaFree(c->dist->sws);
   release_events(c->dist);
   delete c->dist;
   c->dist = nullptr;

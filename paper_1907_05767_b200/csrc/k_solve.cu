@@ -95,10 +95,16 @@ __device__ __forceinline__ double quot(double y, double u, double r, bool own, b
   return q;
 }
 
+// Window form (the multi-GPU ring solve, ebv_dist.cu): only the column
+// blocks [jlo, jhi) (units of BR) take part, addressed as
+// LU[row + (col - cbase) * lda]; forward, row blocks I >= jlo are processed
+// (I < jhi: substituted and released; below: only updated by the window's
+// columns); backward, row blocks I < jhi (I >= jlo substituted; above: only
+// updated).  The full solve is the window [0, NB) with cbase = 0.
 template <bool FORWARD, int NR>
 __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __restrict__ LU, int64_t lda,
                                                    double* B, int64_t ldb, int nrhs, int* ticket, int* flags,
-                                                   int epoch) {
+                                                   int epoch, int64_t jlo, int64_t jhi, int64_t cbase) {
   __shared__ double sd[BR * TSTR];          // diagonal tile: sd[c*TSTR + r] = LU(I*BR + r, I*BR + c)
   __shared__ double sbuf[BR * MAXR];        // published values of block J (sy[k*MAXR + r]),
   double* sy = sbuf;                        // then the hand-off to the diagonal warps (sacc)
@@ -113,33 +119,35 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
     __syncthreads();
     const int64_t t = s_blk;
     __syncthreads();
-    if (t >= NB) return;
-    const int64_t I = FORWARD ? t : NB - 1 - t;
+    if (t >= (FORWARD ? NB - jlo : jhi)) return;
+    const int64_t I = FORWARD ? jlo + t : jhi - 1 - t;
+    const bool diag = I >= jlo && I < jhi;
     const int64_t row = I * BR + i;
     const bool rv = row < n;
     EBV_TR(0);
 
     // stage the diagonal tile (read-only: no dependence on other blocks)
-    for (int c = 0; c < BR; c++) {
-      const int64_t col = I * BR + c;
-      sd[c * TSTR + i] = (rv && col < n) ? LU[row + col * lda] : 0.0;
-    }
+    if (diag)
+      for (int c = 0; c < BR; c++) {
+        const int64_t col = I * BR + c;
+        sd[c * TSTR + i] = (rv && col < n) ? LU[row + (col - cbase) * lda] : 0.0;
+      }
     double acc[MAXR];
 #pragma unroll
     for (int r = 0; r < MAXR; r++) acc[r] = (rv && r < nr) ? B[row + (int64_t)r * ldb] : 0.0;
 
-    const int64_t nJ = FORWARD ? I : NB - 1 - I;
+    const int64_t nJ = FORWARD ? (I < jhi ? I : jhi) - jlo : jhi - (I + 1 > jlo ? I + 1 : jlo);
     for (int64_t jj = 0; jj < nJ; jj++) {
-      const int64_t J = FORWARD ? jj : NB - 1 - jj;
+      const int64_t J = FORWARD ? jlo + jj : jhi - 1 - jj;
       // this thread's row segment of tile (I, J): issued before the wait
       double l[BR];
-      const double* src = LU + (rv ? row : 0) + (J * BR) * lda;
+      const double* src = LU + (rv ? row : 0) + (J * BR - cbase) * lda;
 #pragma unroll
       for (int k = 0; k < BR; k++) l[k] = (rv && J * BR + k < n) ? __ldg(src + k * lda) : 0.0;
       if (jj + 1 == nJ) {
         EBV_TR(1);
       }
-      if (i == 0) wait_flag(flags + J, epoch, jj + 1 == nJ);
+      if (i == 0) wait_flag(flags + J, epoch, diag && jj + 1 == nJ);
       if (jj + 1 == nJ) {
         EBV_TR(2);
       }
@@ -163,6 +171,14 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
           for (int r = 0; r < MAXR; r++)
             if (r < nr) acc[r] = fma(-l[k], sy[k * MAXR + r], acc[r]);
       }
+    }
+
+    if (!diag) {   // outside the window's rows: only the window's updates
+#pragma unroll
+      for (int r = 0; r < MAXR; r++)
+        if (rv && r < nr) B[row + (int64_t)r * ldb] = acc[r];
+      __syncthreads();   // sy is re-staged by the next block
+      continue;
     }
 
     // ---- diagonal block: warp w takes right-hand sides r = w, w+2, ...
@@ -319,12 +335,22 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
 
 template <bool FWD>
 cudaError_t launch_one(int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb, int nr, int* ticket,
-                       int* flags, int ep, int64_t grid, cudaStream_t s) {
+                       int* flags, int ep, int64_t grid, cudaStream_t s, int64_t jlo, int64_t jhi, int64_t cbase) {
   if (nr == 1)
-    solve_kernel<FWD, 1><<<(unsigned)grid, BR, 0, s>>>(n, LU, lda, B, ldb, nr, ticket, flags, ep);
+    solve_kernel<FWD, 1><<<(unsigned)grid, BR, 0, s>>>(n, LU, lda, B, ldb, nr, ticket, flags, ep, jlo, jhi, cbase);
   else
-    solve_kernel<FWD, 0><<<(unsigned)grid, BR, 0, s>>>(n, LU, lda, B, ldb, nr, ticket, flags, ep);
+    solve_kernel<FWD, 0><<<(unsigned)grid, BR, 0, s>>>(n, LU, lda, B, ldb, nr, ticket, flags, ep, jlo, jhi, cbase);
   return cudaGetLastError();
+}
+
+int64_t resident_grid(int64_t units) {
+  int dev = 0, sms = 148, per_sm = 8;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<true, 0>, BR, 0);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t cap = (int64_t)sms * per_sm;
+  return units < cap ? units : cap;
 }
 
 }  // namespace
@@ -334,14 +360,8 @@ int64_t solve_block_rows() { return BR; }
 cudaError_t launch_solve(int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb, int64_t nrhs,
                          int* ticket_ws, int* flags_ws, int64_t epoch, cudaStream_t s) {
   if (n <= 0 || nrhs <= 0) return cudaSuccess;
-  int dev = 0, sms = 148, per_sm = 8;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<true, 0>, BR, 0);
-  if (per_sm < 1) per_sm = 1;
   const int64_t NB = (n + BR - 1) / BR;
-  const int64_t cap = (int64_t)sms * per_sm;
-  const int64_t grid = NB < cap ? NB : cap;
+  const int64_t grid = resident_grid(NB);
   for (int64_t r0 = 0; r0 < nrhs; r0 += MAXR) {
     const int nr = (int)((nrhs - r0) < MAXR ? (nrhs - r0) : MAXR);
     for (int pass = 0; pass < 2; pass++) {
@@ -349,12 +369,31 @@ cudaError_t launch_solve(int64_t n, const double* LU, int64_t lda, double* B, in
       const int ep = (int)(((epoch * 64 + (r0 / MAXR) * 2 + pass) % 0x3FFFFFFF) + 1);
       cudaError_t e = cudaMemsetAsync(ticket_ws + pass, 0, sizeof(int), s);
       if (e != cudaSuccess) return e;
-      e = fwd ? launch_one<true>(n, LU, lda, B + r0 * ldb, ldb, nr, ticket_ws, flags_ws, ep, grid, s)
-              : launch_one<false>(n, LU, lda, B + r0 * ldb, ldb, nr, ticket_ws + 1, flags_ws + NB, ep, grid, s);
+      e = fwd ? launch_one<true>(n, LU, lda, B + r0 * ldb, ldb, nr, ticket_ws, flags_ws, ep, grid, s, 0, NB, 0)
+              : launch_one<false>(n, LU, lda, B + r0 * ldb, ldb, nr, ticket_ws + 1, flags_ws + NB, ep, grid, s, 0, NB,
+                                  0);
       if (e != cudaSuccess) return e;
     }
   }
   return cudaSuccess;
 }
+
+// One column window of the ring solve: forward (fwd) or backward sweep of
+// the columns [c0, c0 + w) (c0 a multiple of BR) whose entries are at
+// LUw[row + (col - c0) * ldl]; nrhs <= MAXR.  ticket: one zeroed int for this
+// launch; flags: the sweep's NB flags (released once per sweep by the block
+// that substitutes them, so one epoch serves the whole sweep).
+cudaError_t launch_solve_window(int64_t n, const double* LUw, int64_t ldl, int64_t c0, int64_t w, bool fwd, double* B,
+                                int64_t ldb, int64_t nrhs, int* ticket, int* flags, int epoch, cudaStream_t s) {
+  if (n <= 0 || nrhs <= 0 || w <= 0) return cudaSuccess;
+  if (nrhs > MAXR || c0 % BR) return cudaErrorInvalidValue;
+  const int64_t NB = (n + BR - 1) / BR;
+  const int64_t jlo = c0 / BR, jhi = (c0 + w + BR - 1) / BR;
+  const int64_t grid = resident_grid(fwd ? NB - jlo : jhi);
+  return fwd ? launch_one<true>(n, LUw, ldl, B, ldb, (int)nrhs, ticket, flags, epoch, grid, s, jlo, jhi, c0)
+             : launch_one<false>(n, LUw, ldl, B, ldb, (int)nrhs, ticket, flags, epoch, grid, s, jlo, jhi, c0);
+}
+
+int64_t solve_max_rhs() { return MAXR; }
 
 }  // namespace ebv

@@ -89,6 +89,26 @@ def test_emulated_dist_factor_and_solve_bitwise(dev, ctx, P, nb, layout, n):
     assert bits_eq(LU1.cpu().numpy(), lu_g)
 
 
+@pytest.mark.parametrize("P,nb,n,nrhs", [(3, 64, 700, 20), (2, 128, 1000, 16), (5, 64, 333, 3)])
+def test_emulated_dist_solve_many_rhs_bitwise(dev, ctx, P, nb, n, nrhs):
+    """The ring solve in right-hand-side groups of 16 (and a ragged last
+    block): bitwise the oracle."""
+    d = ebv_inputs.generate(n, seed=n + nrhs, nrhs=nrhs, device=dev)
+    slabs, colmaps = slabs_for(d, n, nb, P, 0, dev)
+    info = torch.zeros((), dtype=torch.int64, device=dev)
+    sh = torch.cuda.current_stream().cuda_stream
+    assert ebv.ebv_lu_factor_dist_emulated(ctx.handle, n, P, nb, 0, [s.data_ptr() for s in slabs], n, 0.0,
+                                           info.data_ptr(), sh) == 0, ebv.ebv_last_error()
+    B = d["B"].T.clone(memory_format=torch.contiguous_format)
+    for _ in range(2):   # twice: the flags' epochs advance per call
+        Bw = B.clone()
+        assert ebv.ebv_lu_solve_dist_emulated(ctx.handle, n, P, nb, 0, [s.data_ptr() for s in slabs], n,
+                                              Bw.data_ptr(), n, nrhs, sh) == 0, ebv.ebv_last_error()
+        torch.cuda.synchronize()
+        lu_o, _ = oracle.lu_factor(d["At"].T.cpu().numpy())
+        assert bits_eq(Bw.T.cpu().numpy(), oracle.lu_solve(lu_o, d["B"].cpu().numpy()))
+
+
 def test_emulated_dist_info(dev, ctx):
     n, nb, P = 400, 64, 3
     A = torch.eye(n, dtype=torch.float64, device=dev) * 3.0
