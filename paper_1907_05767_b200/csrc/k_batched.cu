@@ -22,14 +22,13 @@ namespace {
 constexpr int NP = 32;   // padded order
 constexpr int MAXRHS = 16;
 
-// Predicated fma (no select instructions): a <- fma(nl, u, a) if p.
-__device__ __forceinline__ void pfma(double& a, double nl, double u, bool p) {
-  asm("{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n @q fma.rn.f64 %0, %1, %2, %0;\n}\n"
-      : "+d"(a)
-      : "d"(nl), "d"(u), "r"((unsigned)p));
-}
+constexpr int CH = 8;     // columns per shuffle chunk
 
-
+// Row updates of rows that may sit above the pivot are guarded by a branch
+// around a chunk of CH fma's (a predicated fma is if-converted by ptxas into
+// an fma plus two selects, which made selects 20% of the instruction stream).
+// FULL: n == 32 (no identity padding: no predicates on loads and stores).
+template <bool FULL>
 __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict__ A, int64_t lda,
                                                       int64_t strideA, int64_t batch, double* __restrict__ B,
                                                       int64_t ldb, int64_t strideB, int nrhs,
@@ -41,14 +40,19 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
   const int64_t sys = 2 * warp + h;
   const bool act = sys < batch;
   const int r0 = t, r1 = NP - 1 - t;              // the paired rows of this lane
-  const bool v0 = act && r0 < n, v1 = act && r1 < n;
+  const bool v0 = act && (FULL || r0 < n), v1 = act && (FULL || r1 < n);
   double* As = A + (act ? sys : 0) * strideA;
 
   double ra[NP], rb[NP];
 #pragma unroll
   for (int j = 0; j < NP; j++) {
-    ra[j] = (v0 && j < n) ? As[r0 + (int64_t)j * lda] : (r0 == j ? 1.0 : 0.0);
-    rb[j] = (v1 && j < n) ? As[r1 + (int64_t)j * lda] : (r1 == j ? 1.0 : 0.0);
+    if (FULL) {
+      ra[j] = act ? As[r0 + (int64_t)j * lda] : (r0 == j ? 1.0 : 0.0);
+      rb[j] = act ? As[r1 + (int64_t)j * lda] : (r1 == j ? 1.0 : 0.0);
+    } else {
+      ra[j] = (v0 && j < n) ? As[r0 + (int64_t)j * lda] : (r0 == j ? 1.0 : 0.0);
+      rb[j] = (v1 && j < n) ? As[r1 + (int64_t)j * lda] : (r1 == j ? 1.0 : 0.0);
+    }
   }
 
   double tv = tau_value;
@@ -57,7 +61,7 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll
     for (int j = 0; j < NP; j++) {
-      if (j < n) { s0 += fabs(ra[j]); s1 += fabs(rb[j]); }
+      if (FULL || j < n) { s0 += fabs(ra[j]); s1 += fabs(rb[j]); }
     }
     double nm = fmax(v0 ? s0 : 0.0, v1 ? s1 : 0.0);
 #pragma unroll
@@ -71,31 +75,47 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
   const int hb = h << 4;
   // ---- factor (Eq 6), k ascending.  With rows t and 31-t per lane, row
   // 31-t is below every pivot k < 16 and row t is above every pivot k >= 16,
-  // so at each step only one of the lane's two rows needs a predicate.
+  // so at each step only one of the lane's two rows needs a guard.
 #pragma unroll
   for (int k = 0; k < NP; k++) {
     const int src = hb + (k < 16 ? k : NP - 1 - k);
     const double piv = __shfl_sync(0xffffffffu, k < 16 ? ra[k] : rb[k], src);
-    if (k < n && inf == 0 && fabs(piv) <= tv) inf = k + 1;
+    if ((FULL || k < n) && inf == 0 && fabs(piv) <= tv) inf = k + 1;
     if (k < 16) {
       const bool a0 = r0 > k;
       if (a0) ra[k] = ra[k] / piv;                     // Eq 6-a
       rb[k] = rb[k] / piv;
       const double n0 = -ra[k], n1 = -rb[k];
 #pragma unroll
-      for (int j = k + 1; j < NP; j++) {
-        const double u = __shfl_sync(0xffffffffu, ra[j], src);   // Eq 6-b (row k = row t of lane k)
-        pfma(ra[j], n0, u, a0);                                  // Eq 6-c
-        rb[j] = fma(n1, u, rb[j]);
+      for (int j0 = k + 1; j0 < NP; j0 += CH) {
+        double u[CH];
+#pragma unroll
+        for (int q = 0; q < CH; q++)
+          if (j0 + q < NP) u[q] = __shfl_sync(0xffffffffu, ra[j0 + q], src);   // Eq 6-b (row k)
+#pragma unroll
+        for (int q = 0; q < CH; q++)
+          if (j0 + q < NP) rb[j0 + q] = fma(n1, u[q], rb[j0 + q]);            // Eq 6-c
+        if (a0) {
+#pragma unroll
+          for (int q = 0; q < CH; q++)
+            if (j0 + q < NP) ra[j0 + q] = fma(n0, u[q], ra[j0 + q]);
+        }
       }
     } else {
       const bool a1 = r1 > k;
       if (a1) rb[k] = rb[k] / piv;
       const double n1 = -rb[k];
 #pragma unroll
-      for (int j = k + 1; j < NP; j++) {
-        const double u = __shfl_sync(0xffffffffu, rb[j], src);
-        pfma(rb[j], n1, u, a1);
+      for (int j0 = k + 1; j0 < NP; j0 += CH) {
+        double u[CH];
+#pragma unroll
+        for (int q = 0; q < CH; q++)
+          if (j0 + q < NP) u[q] = __shfl_sync(0xffffffffu, rb[j0 + q], src);
+        if (a1) {
+#pragma unroll
+          for (int q = 0; q < CH; q++)
+            if (j0 + q < NP) rb[j0 + q] = fma(n1, u[q], rb[j0 + q]);
+        }
       }
     }
   }
@@ -112,10 +132,10 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
         const int src = hb + (k < 16 ? k : NP - 1 - k);
         const double yk = __shfl_sync(0xffffffffu, k < 16 ? y0 : y1, src);
         if (k < 16) {
-          pfma(y0, -ra[k], yk, r0 > k);
+          if (r0 > k) y0 = fma(-ra[k], yk, y0);
           y1 = fma(-rb[k], yk, y1);
         } else {
-          pfma(y1, -rb[k], yk, r1 > k);
+          if (r1 > k) y1 = fma(-rb[k], yk, y1);
         }
       }
 #pragma unroll
@@ -125,10 +145,10 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
         else        { if (t == NP - 1 - k) y1 = y1 / rb[k]; }
         const double xk = __shfl_sync(0xffffffffu, k < 16 ? y0 : y1, src);
         if (k < 16) {
-          pfma(y0, -ra[k], xk, r0 < k);   // rows 31-t >= 16 > k never
+          if (r0 < k) y0 = fma(-ra[k], xk, y0);   // rows 31-t >= 16 > k never
         } else {
-          y0 = fma(-ra[k], xk, y0);       // rows t < 16 <= k always
-          pfma(y1, -rb[k], xk, r1 < k);
+          y0 = fma(-ra[k], xk, y0);               // rows t < 16 <= k always
+          if (r1 < k) y1 = fma(-rb[k], xk, y1);
         }
       }
       if (v0) Bs[r0 + (int64_t)r * ldb] = y0;
@@ -137,8 +157,8 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
   }
 #pragma unroll
   for (int j = 0; j < NP; j++) {
-    if (v0 && j < n) As[r0 + (int64_t)j * lda] = ra[j];
-    if (v1 && j < n) As[r1 + (int64_t)j * lda] = rb[j];
+    if (v0 && (FULL || j < n)) As[r0 + (int64_t)j * lda] = ra[j];
+    if (v1 && (FULL || j < n)) As[r1 + (int64_t)j * lda] = rb[j];
   }
 }
 
@@ -151,8 +171,12 @@ cudaError_t launch_batched(int64_t n, double* A, int64_t lda, int64_t strideA, i
   if (n > NP || nrhs > MAXRHS) return cudaErrorInvalidValue;
   const int64_t warps = (batch + 1) / 2;
   const int64_t blocks = (warps * 32 + 127) / 128;
-  batched_kernel<<<(unsigned)blocks, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, ldb, strideB, (int)nrhs, tau,
-                                                  tau_default ? 1 : 0, tau_value, info);
+  if (n == NP)
+    batched_kernel<true><<<(unsigned)blocks, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, ldb, strideB, (int)nrhs,
+                                                          tau, tau_default ? 1 : 0, tau_value, info);
+  else
+    batched_kernel<false><<<(unsigned)blocks, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, ldb, strideB,
+                                                           (int)nrhs, tau, tau_default ? 1 : 0, tau_value, info);
   return cudaGetLastError();
 }
 
