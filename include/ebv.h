@@ -276,6 +276,14 @@ ebv_status_t ebv_stats_reset(ebv_context_t ctx);
 ebv_status_t ebv_stats_get(ebv_context_t ctx, int kclass, int64_t* launches, double* ms,
                            double* flops, double* bytes);
 
+/* The recorded launches since the last reset as a timeline: writes up to
+ * max_records triples (class, start ms, end ms) to out (class + 256 when
+ * the launch went to the lookahead side stream), times relative to
+ * the first recorded launch's start, in launch order; returns the number of
+ * records available (-1 on invalid arguments).  Synchronizes like
+ * ebv_stats_get.  A diagnostic: the bracketing events add a little time. */
+int64_t ebv_stats_timeline(ebv_context_t ctx, double* out, int64_t max_records);
+
 /* Number of kernels this context launched since creation (all classes). */
 int64_t ebv_launch_count(ebv_context_t ctx);
 

@@ -42,6 +42,7 @@ SIGNATURES = {
     "ebv_set_vector_ctas": (_int, [_vp, _i64]),
     "ebv_set_block": (_int, [_vp, _i64]),
     "ebv_block_width": (_i64, [_vp, _i64]),
+    "ebv_stats_timeline": (_i64, [_vp, _vp, _i64]),
     "ebv_set_lookahead": (_int, [_vp, _int]),
     "ebv_set_graphs": (_int, [_vp, _int]),
     "ebv_lu_factor": (_int, [_vp, _i64, _vp, _i64, _d, _vp, _vp]),
@@ -317,6 +318,18 @@ class Context:
                                        ctypes.byref(by)), "ebv_stats_get")
             out[name] = {"launches": n.value, "ms": ms.value, "flops": fl.value, "bytes": by.value}
         return out
+
+    def timeline(self) -> list:
+        """Recorded launches since the last stats reset:
+        [(class name, start ms, end ms, on the lookahead side stream)]."""
+        L = lib()
+        n = L.ebv_stats_timeline(self.handle, None, 0)
+        if n < 0:
+            raise EbvError("ebv_stats_timeline failed")
+        buf = (ctypes.c_double * (3 * max(n, 1)))()
+        n = L.ebv_stats_timeline(self.handle, buf, n)
+        return [(KCLASSES[int(buf[3 * i]) & 0xFF], buf[3 * i + 1], buf[3 * i + 2], bool(int(buf[3 * i]) >> 8))
+                for i in range(n)]
 
     def launch_count(self) -> int:
         return ebv_launch_count(self.handle)

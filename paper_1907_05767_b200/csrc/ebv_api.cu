@@ -144,10 +144,10 @@ cudaError_t panel_rec(ebv_context* c, int64_t M, int64_t w, double* P, int64_t l
                       cudaStream_t s) {
   if (w <= 0) return cudaSuccess;
   if (w <= c->leaf) {
-    double fl = 2.0 / 3.0 * w * w * w, by = 16.0 * w * w;
-    cudaError_t e = timed(c, KC_LEAF, fl, by, s, 1, [&] { return launch_leaf_lu(w, P, lda, c->d_tau, info, koff, s); });
-    if (e != cudaSuccess) return e;
-    return trsm_r(c, M - w, w, P + w, lda, P, lda, s);
+    // diagonal block LU and the rows below (L21 = A21 U11^-1) in one launch
+    double fl = 2.0 / 3.0 * w * w * w + (double)(M - w) * w * w, by = 16.0 * M * w;
+    return timed(c, KC_LEAF, fl, by, s, 1,
+                 [&] { return launch_panel_leaf(M, w, P, lda, c->d_tau, info, koff, c->d_pcount, s); });
   }
   int64_t h = split_point(w, c->leaf);
   cudaError_t e = panel_rec(c, M, h, P, lda, koff, info, s);
@@ -299,6 +299,7 @@ ebv_status_t ebv_create(ebv_context_t* ctx, int device) {
   c->d_norm = reinterpret_cast<unsigned long long*>(base + 8);
   c->d_scratch = reinterpret_cast<double*>(base + 16);
   c->d_ticket = reinterpret_cast<int*>(base + 64);
+  c->d_pcount = reinterpret_cast<int*>(base + 128);
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   e = cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi);
@@ -590,11 +591,25 @@ static void drain(ebv_context* c) {
     cudaEventSynchronize(r.e1);
     float ms = 0;
     cudaEventElapsedTime(&ms, r.e0, r.e1);
-    c->st_launch[r.cls]++;
-    c->st_ms[r.cls] += ms;
-    c->st_flops[r.cls] += r.flops;
-    c->st_bytes[r.cls] += r.bytes;
-    c->pool.push_back(r.e0);
+    const int cls = r.cls & 0xFF;
+    c->st_launch[cls]++;
+    c->st_ms[cls] += ms;
+    c->st_flops[cls] += r.flops;
+    c->st_bytes[cls] += r.bytes;
+    bool keep = false;
+    if (!c->tl_ref) {   // the first launch since reset is the timeline's origin
+      c->tl_ref = r.e0;
+      keep = true;
+    }
+    float t0 = 0, t1 = 0;
+    cudaEventElapsedTime(&t0, c->tl_ref, r.e0);
+    cudaEventElapsedTime(&t1, c->tl_ref, r.e1);
+    if (c->tl.size() < ((size_t)3 << 20)) {
+      c->tl.push_back(r.cls);
+      c->tl.push_back(t0);
+      c->tl.push_back(t1);
+    }
+    if (!keep) c->pool.push_back(r.e0);
     c->pool.push_back(r.e1);
   }
   c->recs.clear();
@@ -605,7 +620,20 @@ ebv_status_t ebv_stats_reset(ebv_context_t c) {
   DeviceGuard g(c->device);
   drain(c);
   for (int i = 0; i < EBV_NUM_KCLASSES; i++) c->st_launch[i] = 0, c->st_ms[i] = c->st_flops[i] = c->st_bytes[i] = 0;
+  c->tl.clear();
+  if (c->tl_ref) c->pool.push_back(c->tl_ref);
+  c->tl_ref = nullptr;
   return EBV_SUCCESS;
+}
+
+int64_t ebv_stats_timeline(ebv_context_t c, double* out, int64_t max_records) {
+  if (!c || max_records < 0 || (max_records > 0 && !out)) return -1;
+  DeviceGuard g(c->device);
+  drain(c);
+  const int64_t nrec = (int64_t)(c->tl.size() / 3);
+  const int64_t m = nrec < max_records ? nrec : max_records;
+  for (int64_t i = 0; i < 3 * m; i++) out[i] = c->tl[i];
+  return nrec;
 }
 
 ebv_status_t ebv_stats_get(ebv_context_t c, int kclass, int64_t* launches, double* ms, double* flops, double* bytes) {

@@ -39,6 +39,8 @@ cudaError_t launch_leaf_lu(int64_t n, double* A, int64_t lda, const double* tau,
 
 // X <- X U^-1, U upper triangular k x k (k <= 64, non-unit), X m x k:
 // row-parallel substitution (the L21 panel of the blocked form).
+cudaError_t launch_panel_leaf(int64_t M, int64_t w, double* P, int64_t lda, const double* tau, int64_t* info,
+                              int64_t koff, int* count, cudaStream_t s);
 cudaError_t launch_trsm_right_upper(int64_t m, int64_t k, double* X, int64_t ldx, const double* U,
                                     int64_t ldu, cudaStream_t s);
 

@@ -19,6 +19,7 @@ struct ebv_context {
   unsigned long long* d_norm = nullptr;
   double* d_scratch = nullptr;
   int* d_ticket = nullptr;
+  int* d_pcount = nullptr;  // panel-leaf arrival counter (zero between launches; self-resetting)
   int* d_flags = nullptr;
   int64_t flags_cap = 0;
   int* d_vflags = nullptr;
@@ -39,6 +40,8 @@ struct ebv_context {
   std::vector<cudaEvent_t> pool;
   int64_t st_launch[EBV_NUM_KCLASSES] = {0};
   double st_ms[EBV_NUM_KCLASSES] = {0}, st_flops[EBV_NUM_KCLASSES] = {0}, st_bytes[EBV_NUM_KCLASSES] = {0};
+  std::vector<double> tl;           // stats timeline: (class, start ms, end ms) per launch
+  cudaEvent_t tl_ref = nullptr;     // the timeline's time origin (first launch since reset)
   ebv_dist_state* dist = nullptr;   // set by ebv_create_dist
   // CUDA Graph cache of the blocked factor schedule, keyed by its arguments
   bool graphs = true;
@@ -82,7 +85,7 @@ template <class F>
 cudaError_t timed(ebv_context* c, int cls, double flops, double bytes, cudaStream_t s, int nlaunch, F&& f) {
   c->launches += nlaunch;
   if (!c->stats) return f();
-  ebv_context::Rec r{cls, get_event(c), get_event(c), flops, bytes};
+  ebv_context::Rec r{cls | (s != nullptr && s == c->side ? 256 : 0), get_event(c), get_event(c), flops, bytes};
   cudaEventRecord(r.e0, s);
   cudaError_t e = f();
   cudaEventRecord(r.e1, s);

@@ -30,6 +30,15 @@ constexpr int S = W + 2;     // smem row stride (doubles): 16-byte aligned rows
 constexpr int G = 8;          // lanes per row / column
 constexpr int Q = W / G;      // entries per lane
 
+// Code size: these kernels are latency-bound chains executed a few times per
+// launch, so a fully unrolled 64-step body (3-5k SASS instructions) ran
+// instruction-fetch bound.  The step loop is rolled over blocks of G steps:
+// inside a block the G steps are unrolled, and at the end of the block each
+// lane's first register (column j + G*qk, now final) is stored and the
+// register file is rotated down by one, so the live entries of block qk are
+// always a[0..Q-1-qk].  Rotated-in slots are dead (never stored); the shared
+// rows are padded to 2W so their reads stay in bounds.
+
 // ---------------------------------------------------------------- leaf LU
 // 512 threads: row i of the block is owned by group i.  Step k: group k
 // publishes its final row (the U_(k) vector, Eq 6-b) to shared memory; every
@@ -38,7 +47,7 @@ constexpr int Q = W / G;      // entries per lane
 // padded (exactly neutral).
 __global__ void __launch_bounds__(W * G) leaf_lu_kernel(int w, double* __restrict__ A, int64_t lda,
                                                         const double* __restrict__ tau, int64_t* info, int64_t koff) {
-  __shared__ __align__(16) double urow[2][W];
+  __shared__ __align__(16) double urow[2][2 * W];
   __shared__ int smin;
   const int tid = threadIdx.x, i = tid / G, j = tid % G, lane = tid & 31, base = lane & ~(G - 1);
   double a[Q];
@@ -49,75 +58,227 @@ __global__ void __launch_bounds__(W * G) leaf_lu_kernel(int w, double* __restric
   }
   if (tid == 0) smin = 0x7fffffff;
   const double tv = *tau;
+#pragma unroll 1
+  for (int qk = 0; qk < Q; qk++) {
 #pragma unroll
-  for (int k = 0; k < W; k++) {
-    const int o = k % G, qk = k / G;
-    double* ur = urow[k & 1];
-    if (i == k) {
+    for (int o = 0; o < G; o++) {
+      const int k = qk * G + o;
+      double* ur = urow[o & 1] + G * qk;           // ur[j + G*q] = u(k, j + G*(q + qk))
+      if (i == k) {
 #pragma unroll
-      for (int q = qk; q < Q; q++) ur[j + G * q] = a[q];
+        for (int q = 0; q < Q; q++) ur[j + G * q] = a[q];
+      }
+      __syncthreads();
+      const double piv = ur[o];
+      if (tid == 0 && k < w && fabs(piv) <= tv) atomicMin(&smin, k + 1);
+      if (i > k && j == o) a[0] = a[0] / piv;                       // Eq 6-a
+      const double l = __shfl_sync(0xffffffffu, a[0], base + o);
+      if (i > k) {
+        if (j > o) a[0] = fma(-l, ur[j], a[0]);                      // Eq 6-c
+#pragma unroll
+        for (int q = 1; q < Q; q++) a[q] = fma(-l, ur[j + G * q], a[q]);
+      }
     }
-    __syncthreads();
-    const double piv = ur[k];
-    if (tid == 0 && k < w && fabs(piv) <= tv) atomicMin(&smin, k + 1);
-    if (i > k && j == o) a[qk] = a[qk] / piv;
-    const double l = __shfl_sync(0xffffffffu, a[qk], base + o);
-    if (i > k) {
+    const int c = j + G * qk;                        // final: store, rotate
+    if (i < w && c < w) A[i + (int64_t)c * lda] = a[0];
 #pragma unroll
-      for (int q = qk; q < Q; q++)
-        if (q > qk || j > o) a[q] = fma(-l, ur[j + G * q], a[q]);
-    }
+    for (int q = 0; q < Q - 1; q++) a[q] = a[q + 1];
+    a[Q - 1] = 0.0;
   }
   __syncthreads();
   if (tid == 0 && smin != 0x7fffffff) {
     volatile int64_t* vi = info;
     if (*vi == 0) *vi = koff + smin;
   }
-  if (i < w) {
-#pragma unroll
-    for (int q = 0; q < Q; q++) {
-      const int c = j + G * q;
-      if (c < w) A[i + (int64_t)c * lda] = a[q];
-    }
-  }
 }
 
 // ---------------------------------------------------------------- L21 = A21 U11^-1
-// Group per row: step p, the owner lane divides x_p by u_pp, broadcasts it,
-// every lane applies x_c = fma(-x_p, u_pc, x_c) to its entries c > p.
+// Group per row: step p, the owner lane forms x_p / u_pp, broadcasts it, every
+// lane applies x_c = fma(-x_p, u_pc, x_c) to its entries c > p.  The quotient
+// comes from the hoisted reciprocal RN(1/u_pp) with one Markstein correction,
+// verified exactly (the remainder test of k_solve.cu); a warp with any
+// unverified quotient redoes its rows with true division, so every entry is
+// RN(x/u) — bitwise the oracle — and the chain per step is three dependent
+// fp64 operations instead of a division.
+__device__ __forceinline__ double quot_v(double y, double u, double r, bool& ok) {
+  const double q0 = y * r;
+  const double q = fma(r, fma(-u, q0, y), q0);
+  const double rr = fma(-u, q, y);
+  const long long qb = __double_as_longlong(q);
+  const long long e = qb & 0x7ff0000000000000LL;
+  const bool normal = e > (54LL << 52) && e < (0x7feLL << 52);
+  double lim = fabs(u) * __longlong_as_double(e - (53LL << 52));
+  const bool below = (rr < 0.0) != (u < 0.0);
+  const bool pow2 = (qb & 0x000fffffffffffffLL) == 0;
+  if (pow2 && below == (q > 0.0)) lim *= 0.5;
+  // y = +0 (the identity padding): the sequence returns +0 / -0 for u > 0 /
+  // u < 0, which is RN(y/u) exactly
+  const bool pzero = __double_as_longlong(y) == 0;
+  ok = ok && (pzero || (normal && fabs(rr) < lim));
+  return q;
+}
+
 __global__ void __launch_bounds__(256) trsm_ru_kernel(int64_t m, int k, double* __restrict__ X, int64_t ldx,
                                                       const double* __restrict__ U, int64_t ldu) {
-  __shared__ __align__(16) double sU[W * S];   // sU[p*S + c] = u(p, c), identity padded
+  __shared__ __align__(16) double sU[W * S + W];   // sU[p*S + c] = u(p, c), identity padded (+ overrun pad)
+  __shared__ double srcp[W];
   for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
     const int p = idx % W, c = idx / W;
     sU[p * S + c] = (p < k && c < k) ? (p <= c ? U[p + (int64_t)c * ldu] : 0.0) : (p == c ? 1.0 : 0.0);
   }
+  for (int idx = threadIdx.x; idx < W * (S - W) + W; idx += blockDim.x)   // the pad columns of each row + tail
+    if (idx < W * (S - W)) sU[(idx / (S - W)) * S + W + idx % (S - W)] = 0.0; else sU[W * S + idx - W * (S - W)] = 0.0;
+  __syncthreads();
+  if (threadIdx.x < W) srcp[threadIdx.x] = 1.0 / sU[threadIdx.x * S + threadIdx.x];
   __syncthreads();
   const int tid = threadIdx.x, j = tid % G, lane = tid & 31, base = lane & ~(G - 1);
   const int64_t i = (int64_t)blockIdx.x * (256 / G) + tid / G;
   const bool rv = i < m;
-  double x[Q];
+  double x0[Q];
 #pragma unroll
   for (int q = 0; q < Q; q++) {
     const int c = j + G * q;
-    x[q] = (rv && c < k) ? X[i + (int64_t)c * ldx] : 0.0;
+    x0[q] = (rv && c < k) ? X[i + (int64_t)c * ldx] : 0.0;
   }
+  for (int pass = 0; pass < 2; pass++) {
+    const bool exact = pass == 1;
+    bool ok = true;
+    double x[Q];
 #pragma unroll
-  for (int p = 0; p < W; p++) {
-    const int o = p % G, qp = p / G;
-    const double* up = sU + p * S;
-    if (j == o) x[qp] = x[qp] / up[p];
-    const double xp = __shfl_sync(0xffffffffu, x[qp], base + o);
+    for (int q = 0; q < Q; q++) x[q] = x0[q];
+#pragma unroll 1
+    for (int qk = 0; qk < Q; qk++) {
 #pragma unroll
-    for (int q = qp; q < Q; q++)
-      if (q > qp || j > o) x[q] = fma(-xp, up[j + G * q], x[q]);
-  }
-  if (rv) {
+      for (int o = 0; o < G; o++) {
+        const int p = qk * G + o;
+        const double* up = sU + p * S + G * qk;     // up[j + G*q] = u(p, j + G*(q + qk))
+        if (j == o) x[0] = exact ? x[0] / up[o] : quot_v(x[0], up[o], srcp[p], ok);
+        const double xp = __shfl_sync(0xffffffffu, x[0], base + o);
+        if (j > o) x[0] = fma(-xp, up[j], x[0]);
 #pragma unroll
-    for (int q = 0; q < Q; q++) {
-      const int c = j + G * q;
-      if (c < k) X[i + (int64_t)c * ldx] = x[q];
+        for (int q = 1; q < Q; q++) x[q] = fma(-xp, up[j + G * q], x[q]);
+      }
+      const int c = j + G * qk;
+      if (rv && c < k) X[i + (int64_t)c * ldx] = x[0];
+#pragma unroll
+      for (int q = 0; q < Q - 1; q++) x[q] = x[q + 1];
+      x[Q - 1] = 0.0;
     }
+    if (!__any_sync(0xffffffffu, !ok)) break;      // every quotient verified
+  }
+}
+
+// ---------------------------------------------------------------- panel leaf
+// The leaf of the panel recursion in ONE launch: LU of the w x w diagonal
+// block and L21 = A21 U11^-1 for the M - w rows below (leaf_lu + trsm_ru
+// fused, one kernel boundary less on the panel's critical chain).  Every CTA
+// factors the diagonal block itself (the same operations in every CTA, so
+// the same bits) with the leaf_lu scheme; the CTA that arrives last (an
+// arrival counter, so every CTA has read the unfactored block before it is
+// overwritten — CTAs of one launch need not run at the same time) stores it
+// and reports info,
+// publishing each final U row into a full shared copy of U11, then solves
+// its 64 rows below with the trsm_ru scheme (verified reciprocal quotients).
+constexpr int US = 2 * W;     // shared U row stride (covers the rotation overrun)
+
+__global__ void __launch_bounds__(W * G) panel_leaf_kernel(int64_t M, int w, double* __restrict__ P, int64_t lda,
+                                                           const double* __restrict__ tau, int64_t* info,
+                                                           int64_t koff, int* count) {
+  extern __shared__ __align__(16) double sUp[];    // [W][US]: sUp[k*US + c] = u(k, c)
+  __shared__ double srcp[W];
+  __shared__ int smin, slast;
+  const int tid = threadIdx.x, i = tid / G, j = tid % G, lane = tid & 31, base = lane & ~(G - 1);
+  for (int idx = tid; idx < W * US; idx += W * G) sUp[idx] = 0.0;
+  double a[Q];
+#pragma unroll
+  for (int q = 0; q < Q; q++) {
+    const int c = j + G * q;
+    a[q] = (i < w && c < w) ? P[i + (int64_t)c * lda] : (i == c ? 1.0 : 0.0);
+  }
+  if (tid == 0) smin = 0x7fffffff;
+  const double tv = *tau;
+  __syncthreads();   // every thread's loads of the diagonal block are done (values in registers)
+  if (tid == 0) {
+    __threadfence();
+    const int old = atomicAdd(count, 1);
+    slast = old == (int)gridDim.x - 1;
+    if (slast) {
+      *count = 0;    // every CTA has arrived: reset for the next launch
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  const bool store = slast != 0;
+  // ---- diagonal block (leaf_lu, publishing into the full U copy)
+#pragma unroll 1
+  for (int qk = 0; qk < Q; qk++) {
+#pragma unroll
+    for (int o = 0; o < G; o++) {
+      const int k = qk * G + o;
+      double* ur = sUp + k * US + G * qk;           // ur[j + G*q] = u(k, j + G*(q + qk))
+      if (i == k) {
+#pragma unroll
+        for (int q = 0; q < Q; q++) ur[j + G * q] = a[q];
+      }
+      __syncthreads();
+      const double piv = ur[o];
+      if (store && tid == 0 && k < w && fabs(piv) <= tv) atomicMin(&smin, k + 1);
+      if (i > k && j == o) a[0] = a[0] / piv;                       // Eq 6-a
+      const double l = __shfl_sync(0xffffffffu, a[0], base + o);
+      if (i > k) {
+        if (j > o) a[0] = fma(-l, ur[j], a[0]);                      // Eq 6-c
+#pragma unroll
+        for (int q = 1; q < Q; q++) a[q] = fma(-l, ur[j + G * q], a[q]);
+      }
+    }
+    const int c = j + G * qk;
+    if (store && i < w && c < w) P[i + (int64_t)c * lda] = a[0];
+#pragma unroll
+    for (int q = 0; q < Q - 1; q++) a[q] = a[q + 1];
+    a[Q - 1] = 0.0;
+  }
+  __syncthreads();
+  if (store && tid == 0 && smin != 0x7fffffff) {
+    volatile int64_t* vi = info;
+    if (*vi == 0) *vi = koff + smin;
+  }
+  if (M <= w) return;
+  if (tid < W) srcp[tid] = 1.0 / sUp[tid * US + tid];
+  __syncthreads();
+  // ---- rows below (trsm_ru): this CTA's 64 rows, a group of 8 lanes each
+  const int64_t r = (int64_t)w + (int64_t)blockIdx.x * W + i;
+  const bool rv = r < M;
+  double x0[Q];
+#pragma unroll
+  for (int q = 0; q < Q; q++) {
+    const int c = j + G * q;
+    x0[q] = (rv && c < w) ? P[r + (int64_t)c * lda] : 0.0;
+  }
+  for (int pass = 0; pass < 2; pass++) {
+    const bool exact = pass == 1;
+    bool ok = true;
+    double x[Q];
+#pragma unroll
+    for (int q = 0; q < Q; q++) x[q] = x0[q];
+#pragma unroll 1
+    for (int qk = 0; qk < Q; qk++) {
+#pragma unroll
+      for (int o = 0; o < G; o++) {
+        const int p = qk * G + o;
+        const double* up = sUp + p * US + G * qk;
+        if (j == o) x[0] = exact ? x[0] / up[o] : quot_v(x[0], up[o], srcp[p], ok);
+        const double xp = __shfl_sync(0xffffffffu, x[0], base + o);
+        if (j > o) x[0] = fma(-xp, up[j], x[0]);
+#pragma unroll
+        for (int q = 1; q < Q; q++) x[q] = fma(-xp, up[j + G * q], x[q]);
+      }
+      const int c = j + G * qk;
+      if (rv && c < w) P[r + (int64_t)c * lda] = x[0];
+#pragma unroll
+      for (int q = 0; q < Q - 1; q++) x[q] = x[q + 1];
+      x[Q - 1] = 0.0;
+    }
+    if (!__any_sync(0xffffffffu, !ok)) break;
   }
 }
 
@@ -206,6 +367,22 @@ cudaError_t launch_leaf_lu(int64_t n, double* A, int64_t lda, const double* tau,
   if (n <= 0) return cudaSuccess;
   if (n > W) return cudaErrorInvalidValue;
   leaf_lu_kernel<<<1, W * G, 0, s>>>((int)n, A, lda, tau, info, koff);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_panel_leaf(int64_t M, int64_t w, double* P, int64_t lda, const double* tau, int64_t* info,
+                              int64_t koff, int* count, cudaStream_t s) {
+  if (w <= 0 || M <= 0) return cudaSuccess;
+  if (w > W || M < w) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)W * US * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(panel_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t grid = M > w ? (M - w + W - 1) / W : 1;
+  panel_leaf_kernel<<<(unsigned)grid, W * G, smem, s>>>(M, (int)w, P, lda, tau, info, koff, count);
   return cudaGetLastError();
 }
 

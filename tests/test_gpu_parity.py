@@ -87,9 +87,11 @@ def test_blocked_factor_bitwise(dev, ctx, n):
     assert bits_eq(lu_g, lu_o)
 
 
-@pytest.mark.parametrize("nb", [64, 128, 192, 512, -1])
-def test_blocked_schedules_bitwise(dev, ctx, nb):
-    n = 700
+@pytest.mark.parametrize("nb,n", [(64, 700), (128, 700), (192, 700), (512, 700), (-1, 700), (64, 1537), (64, 3000)])
+def test_blocked_schedules_bitwise(dev, ctx, nb, n):
+    """(64, 1537/3000): many panel-leaf CTAs while the lookahead update occupies
+    the GPU, so they start at different times (the diagonal block must not be
+    overwritten before every CTA has read it)."""
     d = ebv_inputs.generate(n, seed=nb + 1000, device=dev)
     A = d["At"].T
     lu_g, _ = run_factor(ctx, A, nb=nb)
