@@ -10,6 +10,7 @@
 // with a long k range, and every entry still sees its updates in ascending k
 // followed by its division (bitwise equal to the serial oracle).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -140,14 +141,28 @@ cudaError_t lu_rec(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t ko
 // L11\U11 and the rows below become L21 (Eq 6 restricted to the w steps of
 // the panel).  Recursive on the panel width; the leaves fuse nothing but are
 // a diagonal-block LU (one CTA) + a row-parallel L21 = A21 U11^-1.
+static int64_t kPanelLeafFusedRows = [] {
+  const char* e = getenv("EBV_PANEL_FUSED_ROWS");
+  return e ? (int64_t)atoll(e) : (int64_t)8192;
+}();
+
 cudaError_t panel_rec(ebv_context* c, int64_t M, int64_t w, double* P, int64_t lda, int64_t koff, int64_t* info,
                       cudaStream_t s) {
   if (w <= 0) return cudaSuccess;
   if (w <= c->leaf) {
-    // diagonal block LU and the rows below (L21 = A21 U11^-1) in one launch
-    double fl = 2.0 / 3.0 * w * w * w + (double)(M - w) * w * w, by = 16.0 * M * w;
-    return timed(c, KC_LEAF, fl, by, s, 1,
-                 [&] { return launch_panel_leaf(M, w, P, lda, c->d_tau, info, koff, c->d_pcount, s); });
+    // short panels: diagonal block LU and the rows below in one launch (each
+    // CTA factors the diagonal block itself); tall panels: one CTA for the
+    // diagonal block, then the rows below with few, fat CTAs — the panel
+    // runs beside the DMMA update, so its SM-time is what it costs there
+    if (M <= kPanelLeafFusedRows) {
+      double fl = 2.0 / 3.0 * w * w * w + (double)(M - w) * w * w, by = 16.0 * M * w;
+      return timed(c, KC_LEAF, fl, by, s, 1,
+                   [&] { return launch_panel_leaf(M, w, P, lda, c->d_tau, info, koff, c->d_pcount, s); });
+    }
+    double fl = 2.0 / 3.0 * w * w * w, by = 16.0 * w * w;
+    cudaError_t e = timed(c, KC_LEAF, fl, by, s, 1, [&] { return launch_leaf_lu(w, P, lda, c->d_tau, info, koff, s); });
+    if (e != cudaSuccess) return e;
+    return trsm_r(c, M - w, w, P + w, lda, P, lda, s);
   }
   int64_t h = split_point(w, c->leaf);
   cudaError_t e = panel_rec(c, M, h, P, lda, koff, info, s);

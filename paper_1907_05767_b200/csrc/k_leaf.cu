@@ -118,8 +118,16 @@ __device__ __forceinline__ double quot_v(double y, double u, double r, bool& ok)
   return q;
 }
 
-__global__ void __launch_bounds__(256) trsm_ru_kernel(int64_t m, int k, double* __restrict__ X, int64_t ldx,
-                                                      const double* __restrict__ U, int64_t ldu) {
+// RR rows per lane group (independent chains interleaved): a CTA of 256
+// threads covers 32*RR rows, so the kernel holds few SM slots for its
+// latency-bound duration (it runs beside the DMMA update on the lookahead
+// stream; 128 registers keep it within one update CTA's register share).
+// Each block of 8 steps is checkpointed; if any quotient of the block is
+// unverified the warp redoes that block with true division.
+constexpr int RR = 2;
+
+__global__ void __launch_bounds__(256, 2) trsm_ru_kernel(int64_t m, int k, double* __restrict__ X, int64_t ldx,
+                                                         const double* __restrict__ U, int64_t ldu) {
   __shared__ __align__(16) double sU[W * S + W];   // sU[p*S + c] = u(p, c), identity padded (+ overrun pad)
   __shared__ double srcp[W];
   for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
@@ -132,39 +140,66 @@ __global__ void __launch_bounds__(256) trsm_ru_kernel(int64_t m, int k, double* 
   if (threadIdx.x < W) srcp[threadIdx.x] = 1.0 / sU[threadIdx.x * S + threadIdx.x];
   __syncthreads();
   const int tid = threadIdx.x, j = tid % G, lane = tid & 31, base = lane & ~(G - 1);
-  const int64_t i = (int64_t)blockIdx.x * (256 / G) + tid / G;
-  const bool rv = i < m;
-  double x0[Q];
+  const int64_t i0 = (int64_t)blockIdx.x * (32 * RR) + tid / G;   // rows i0 + 32 r
+  double x[RR][Q];
 #pragma unroll
-  for (int q = 0; q < Q; q++) {
-    const int c = j + G * q;
-    x0[q] = (rv && c < k) ? X[i + (int64_t)c * ldx] : 0.0;
-  }
-  for (int pass = 0; pass < 2; pass++) {
-    const bool exact = pass == 1;
-    bool ok = true;
-    double x[Q];
+  for (int r = 0; r < RR; r++)
 #pragma unroll
-    for (int q = 0; q < Q; q++) x[q] = x0[q];
+    for (int q = 0; q < Q; q++) {
+      const int c = j + G * q;
+      const int64_t i = i0 + 32 * r;
+      x[r][q] = (i < m && c < k) ? X[i + (int64_t)c * ldx] : 0.0;
+    }
 #pragma unroll 1
-    for (int qk = 0; qk < Q; qk++) {
+  for (int qk = 0; qk < Q; qk++) {
+    double xs[RR][Q];
+#pragma unroll
+    for (int r = 0; r < RR; r++)
+#pragma unroll
+      for (int q = 0; q < Q; q++) xs[r][q] = x[r][q];
+    bool ok = true;
+#pragma unroll
+    for (int o = 0; o < G; o++) {
+      const int p = qk * G + o;
+      const double* up = sU + p * S + G * qk;     // up[j + G*q] = u(p, j + G*(q + qk))
+      const double upp = up[o], rp = srcp[p];
+#pragma unroll
+      for (int r = 0; r < RR; r++) {
+        if (j == o) x[r][0] = quot_v(x[r][0], upp, rp, ok);
+        const double xp = __shfl_sync(0xffffffffu, x[r][0], base + o);
+        if (j > o) x[r][0] = fma(-xp, up[j], x[r][0]);
+#pragma unroll
+        for (int q = 1; q < Q; q++) x[r][q] = fma(-xp, up[j + G * q], x[r][q]);
+      }
+    }
+    if (__any_sync(0xffffffffu, !ok)) {            // redo the block with true division
+#pragma unroll
+      for (int r = 0; r < RR; r++)
+#pragma unroll
+        for (int q = 0; q < Q; q++) x[r][q] = xs[r][q];
 #pragma unroll
       for (int o = 0; o < G; o++) {
         const int p = qk * G + o;
-        const double* up = sU + p * S + G * qk;     // up[j + G*q] = u(p, j + G*(q + qk))
-        if (j == o) x[0] = exact ? x[0] / up[o] : quot_v(x[0], up[o], srcp[p], ok);
-        const double xp = __shfl_sync(0xffffffffu, x[0], base + o);
-        if (j > o) x[0] = fma(-xp, up[j], x[0]);
+        const double* up = sU + p * S + G * qk;
 #pragma unroll
-        for (int q = 1; q < Q; q++) x[q] = fma(-xp, up[j + G * q], x[q]);
+        for (int r = 0; r < RR; r++) {
+          if (j == o) x[r][0] = x[r][0] / up[o];
+          const double xp = __shfl_sync(0xffffffffu, x[r][0], base + o);
+          if (j > o) x[r][0] = fma(-xp, up[j], x[r][0]);
+#pragma unroll
+          for (int q = 1; q < Q; q++) x[r][q] = fma(-xp, up[j + G * q], x[r][q]);
+        }
       }
-      const int c = j + G * qk;
-      if (rv && c < k) X[i + (int64_t)c * ldx] = x[0];
-#pragma unroll
-      for (int q = 0; q < Q - 1; q++) x[q] = x[q + 1];
-      x[Q - 1] = 0.0;
     }
-    if (!__any_sync(0xffffffffu, !ok)) break;      // every quotient verified
+    const int c = j + G * qk;
+#pragma unroll
+    for (int r = 0; r < RR; r++) {
+      const int64_t i = i0 + 32 * r;
+      if (i < m && c < k) X[i + (int64_t)c * ldx] = x[r][0];
+#pragma unroll
+      for (int q = 0; q < Q - 1; q++) x[r][q] = x[r][q + 1];
+      x[r][Q - 1] = 0.0;
+    }
   }
 }
 
@@ -390,7 +425,7 @@ cudaError_t launch_trsm_right_upper(int64_t m, int64_t k, double* X, int64_t ldx
                                     cudaStream_t s) {
   if (m <= 0 || k <= 0) return cudaSuccess;
   if (k > W) return cudaErrorInvalidValue;
-  trsm_ru_kernel<<<(unsigned)((m + 31) / 32), 256, 0, s>>>(m, (int)k, X, ldx, U, ldu);
+  trsm_ru_kernel<<<(unsigned)((m + 32 * RR - 1) / (32 * RR)), 256, 0, s>>>(m, (int)k, X, ldx, U, ldu);
   return cudaGetLastError();
 }
 
