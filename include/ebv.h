@@ -180,6 +180,17 @@ ebv_status_t ebv_lu_factor_batched(ebv_context_t ctx, int64_t n, double* A, int6
                                    int64_t strideB, int64_t nrhs, double tau, int32_t* d_info,
                                    void* stream);
 
+/* Solve only, for batched systems factored earlier by ebv_lu_factor_batched
+ * (factor once, solve many — SURVEY §8f f1): for each system s,
+ * B_s <- U_s^-1 (L_s^-1 B_s) with the packed LU_s = LU + s*strideA (read
+ * only), forward then backward substitution of Eq 1 per column in
+ * the canonical order (bitwise ebv_lu_solve / the oracle on each system).
+ * Layout, strides and limits as ebv_lu_factor_batched (n <= 32,
+ * nrhs <= 16).  Errors: INVALID_VALUE, NOT_SUPPORTED as there. */
+ebv_status_t ebv_lu_solve_batched(ebv_context_t ctx, int64_t n, const double* LU, int64_t lda,
+                                  int64_t strideA, int64_t batch, double* B, int64_t ldb,
+                                  int64_t strideB, int64_t nrhs, void* stream);
+
 /* The trailing rank-k update of Eq 6-c on its own — the DMMA
  * contraction every blocked / distributed schedule is built from:
  *     C <- C - A * B      A: M x K (lda), B: K x N (ldb), C: M x N (ldc),

@@ -48,6 +48,7 @@ SIGNATURES = {
     "ebv_lu_factor": (_int, [_vp, _i64, _vp, _i64, _d, _vp, _vp]),
     "ebv_lu_solve": (_int, [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp]),
     "ebv_lu_factor_batched": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _d, _vp, _vp]),
+    "ebv_lu_solve_batched": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp]),
     "ebv_update": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp]),
     "ebv_get_unique_id": (_int, [_vp]),
     "ebv_create_dist": (_int, [ctypes.POINTER(_vp), _int, _vp, _int, _int, _i64, _int]),
@@ -152,6 +153,10 @@ def ebv_lu_solve(ctx, n, LU, lda, B, ldb, nrhs, stream):
 
 def ebv_lu_factor_batched(ctx, n, A, lda, strideA, batch, B, ldb, strideB, nrhs, tau, d_info, stream):
     return lib().ebv_lu_factor_batched(ctx, n, A, lda, strideA, batch, B, ldb, strideB, nrhs, tau, d_info, stream)
+
+
+def ebv_lu_solve_batched(ctx, n, LU, lda, strideA, batch, B, ldb, strideB, nrhs, stream):
+    return lib().ebv_lu_solve_batched(ctx, n, LU, lda, strideA, batch, B, ldb, strideB, nrhs, stream)
 
 
 def ebv_update(ctx, M, N, K, A, lda, B, ldb, C, ldc, stream):
@@ -443,3 +448,19 @@ def lu_factor_batched(At: torch.Tensor, Bt: torch.Tensor | None = None, tau: flo
     _check(ebv_lu_factor_batched(ctx.handle, n, At.data_ptr(), max(n, 1), n * n, batch, bptr, ldb, sb, nrhs,
                                  float(tau), info.data_ptr(), _stream_handle(At.device)), "ebv_lu_factor_batched")
     return info
+
+
+def lu_solve_batched(LUt: torch.Tensor, Bt: torch.Tensor, ctx: Context | None = None) -> torch.Tensor:
+    """Solve-only for systems factored by lu_factor_batched: LUt (batch, n, n)
+    packed per-system column-major storage (read only), Bt (batch, nrhs, n)
+    overwritten with X.  Returns Bt."""
+    _require(LUt, "LUt")
+    _require(Bt, "Bt")
+    if not LUt.is_contiguous() or not Bt.is_contiguous():
+        raise EbvError("LUt (batch, n, n) and Bt (batch, nrhs, n) must be contiguous")
+    batch, n, _ = LUt.shape
+    nrhs = Bt.shape[1]
+    ctx = ctx or default_context(LUt.device.index or 0)
+    _check(ebv_lu_solve_batched(ctx.handle, n, LUt.data_ptr(), max(n, 1), n * n, batch, Bt.data_ptr(), max(n, 1),
+                                n * nrhs, nrhs, _stream_handle(LUt.device)), "ebv_lu_solve_batched")
+    return Bt

@@ -534,6 +534,29 @@ ebv_status_t ebv_lu_factor_batched(ebv_context_t c, int64_t n, double* A, int64_
   return EBV_SUCCESS;
 }
 
+ebv_status_t ebv_lu_solve_batched(ebv_context_t c, int64_t n, const double* LU, int64_t lda, int64_t strideA,
+                                  int64_t batch, double* B, int64_t ldb, int64_t strideB, int64_t nrhs, void* stream) {
+  if (!c) return invalid("ebv_lu_solve_batched: NULL ctx");
+  if (n < 0 || batch < 0 || nrhs < 0) return invalid("ebv_lu_solve_batched: negative size");
+  if (lda < (n > 1 ? n : 1)) return invalid("ebv_lu_solve_batched: lda too small");
+  if (batch > 1 && strideA < lda * n) return invalid("ebv_lu_solve_batched: strideA < lda*n");
+  if (ldb < (n > 1 ? n : 1)) return invalid("ebv_lu_solve_batched: ldb too small");
+  if (batch > 1 && strideB < ldb * nrhs) return invalid("ebv_lu_solve_batched: strideB < ldb*nrhs");
+  if (n == 0 || batch == 0 || nrhs == 0) return EBV_SUCCESS;
+  if (!LU || !B) return invalid("ebv_lu_solve_batched: NULL pointer");
+  if (n > EBV_BATCHED_MAX_N) { set_error("batched path supports n <= 32"); return EBV_ERR_NOT_SUPPORTED; }
+  if (nrhs > 16) { set_error("batched path supports nrhs <= 16"); return EBV_ERR_NOT_SUPPORTED; }
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  double fl = batch * 2.0 * n * n * nrhs, by = batch * (8.0 * n * n + 16.0 * n * nrhs);
+  cudaError_t e = timed(c, KC_BATCHED, fl, by, s, 1, [&] {
+    return launch_batched(n, const_cast<double*>(LU), lda, strideA, batch, B, ldb, strideB, nrhs, nullptr, false, 0.0,
+                          nullptr, s, /*solve_only=*/true);
+  });
+  if (e != cudaSuccess) return cuda_fail(e, "batched solve");
+  return EBV_SUCCESS;
+}
+
 ebv_status_t ebv_update(ebv_context_t c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                         const double* B, int64_t ldb, double* C, int64_t ldc, void* stream) {
   if (!c) return invalid("ebv_update: NULL ctx");

@@ -65,7 +65,8 @@ int64_t solve_block_rows();
 // Batched n <= 32 fused factor + solve.
 cudaError_t launch_batched(int64_t n, double* A, int64_t lda, int64_t strideA, int64_t batch, double* B,
                            int64_t ldb, int64_t strideB, int64_t nrhs, const double* tau, bool tau_default,
-                           double tau_value, int32_t* info, cudaStream_t s);
+                           double tau_value, int32_t* info, cudaStream_t s,
+                           bool solve_only = false);
 
 // Vector-level EbV path (persistent cooperative kernel).
 cudaError_t launch_vector_lu(int64_t n, double* A, int64_t lda, const double* tau, int64_t* info,

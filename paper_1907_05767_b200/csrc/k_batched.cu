@@ -28,12 +28,13 @@ constexpr int CH = 8;     // columns per shuffle chunk
 // around a chunk of CH fma's (a predicated fma is if-converted by ptxas into
 // an fma plus two selects, which made selects 20% of the instruction stream).
 // FULL: n == 32 (no identity padding: no predicates on loads and stores).
-template <bool FULL>
+template <bool FULL, int RG>
 __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict__ A, int64_t lda,
                                                       int64_t strideA, int64_t batch, double* __restrict__ B,
                                                       int64_t ldb, int64_t strideB, int nrhs,
                                                       const double* __restrict__ tau_ptr, int tau_default,
-                                                      double tau_value, int32_t* __restrict__ info) {
+                                                      double tau_value, int32_t* __restrict__ info,
+                                                      int solve_only) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int h = lane >> 4, t = lane & 15;
@@ -55,6 +56,8 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
     }
   }
 
+  const int hb = h << 4;
+  if (!solve_only) {   // (solve-only: ra / rb already hold the packed LU rows)
   double tv = tau_value;
   if (tau_default) {
     // n * eps * ||A_s||_inf over the real rows
@@ -72,7 +75,6 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
   }
 
   int inf = 0;
-  const int hb = h << 4;
   // ---- factor (Eq 6), k ascending.  With rows t and 31-t per lane, row
   // 31-t is below every pivot k < 16 and row t is above every pivot k >= 16,
   // so at each step only one of the lane's two rows needs a guard.
@@ -121,40 +123,64 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
   }
   if (act && t == 0 && info) info[sys] = inf;
 
-  // ---- solve (Eq 1): LY = B then UX = Y, per right-hand side
+  }
+
+  // ---- solve (Eq 1): LY = B then UX = Y.  Right-hand sides in groups of
+  // RG (1, or 4 when nrhs > 1) as independent chains (their divisions
+  // overlap); padded columns of a group are zeros and never stored.
   if (B) {
     double* Bs = B + (act ? sys : 0) * strideB;
-    for (int r = 0; r < nrhs; r++) {
-      double y0 = v0 ? Bs[r0 + (int64_t)r * ldb] : 0.0;
-      double y1 = v1 ? Bs[r1 + (int64_t)r * ldb] : 0.0;
+    for (int rb0 = 0; rb0 < nrhs; rb0 += RG) {
+      double y0[RG], y1[RG];
+#pragma unroll
+      for (int g = 0; g < RG; g++) {
+        const bool rv = rb0 + g < nrhs;
+        y0[g] = (v0 && rv) ? Bs[r0 + (int64_t)(rb0 + g) * ldb] : 0.0;
+        y1[g] = (v1 && rv) ? Bs[r1 + (int64_t)(rb0 + g) * ldb] : 0.0;
+      }
 #pragma unroll
       for (int k = 0; k < NP; k++) {   // forward: LY = B
         const int src = hb + (k < 16 ? k : NP - 1 - k);
-        const double yk = __shfl_sync(0xffffffffu, k < 16 ? y0 : y1, src);
-        if (k < 16) {
-          if (r0 > k) y0 = fma(-ra[k], yk, y0);
-          y1 = fma(-rb[k], yk, y1);
-        } else {
-          if (r1 > k) y1 = fma(-rb[k], yk, y1);
+#pragma unroll
+        for (int g = 0; g < RG; g++) {
+          const double yk = __shfl_sync(0xffffffffu, k < 16 ? y0[g] : y1[g], src);
+          if (k < 16) {
+            if (r0 > k) y0[g] = fma(-ra[k], yk, y0[g]);
+            y1[g] = fma(-rb[k], yk, y1[g]);
+          } else {
+            if (r1 > k) y1[g] = fma(-rb[k], yk, y1[g]);
+          }
         }
       }
 #pragma unroll
       for (int k = NP - 1; k >= 0; k--) {   // backward: UX = Y
         const int src = hb + (k < 16 ? k : NP - 1 - k);
-        if (k < 16) { if (t == k) y0 = y0 / ra[k]; }
-        else        { if (t == NP - 1 - k) y1 = y1 / rb[k]; }
-        const double xk = __shfl_sync(0xffffffffu, k < 16 ? y0 : y1, src);
-        if (k < 16) {
-          if (r0 < k) y0 = fma(-ra[k], xk, y0);   // rows 31-t >= 16 > k never
-        } else {
-          y0 = fma(-ra[k], xk, y0);               // rows t < 16 <= k always
-          if (r1 < k) y1 = fma(-rb[k], xk, y1);
+#pragma unroll
+        for (int g = 0; g < RG; g++) {
+          if (k < 16) { if (t == k) y0[g] = y0[g] / ra[k]; }
+          else        { if (t == NP - 1 - k) y1[g] = y1[g] / rb[k]; }
+        }
+#pragma unroll
+        for (int g = 0; g < RG; g++) {
+          const double xk = __shfl_sync(0xffffffffu, k < 16 ? y0[g] : y1[g], src);
+          if (k < 16) {
+            if (r0 < k) y0[g] = fma(-ra[k], xk, y0[g]);   // rows 31-t >= 16 > k never
+          } else {
+            y0[g] = fma(-ra[k], xk, y0[g]);               // rows t < 16 <= k always
+            if (r1 < k) y1[g] = fma(-rb[k], xk, y1[g]);
+          }
         }
       }
-      if (v0) Bs[r0 + (int64_t)r * ldb] = y0;
-      if (v1) Bs[r1 + (int64_t)r * ldb] = y1;
+#pragma unroll
+      for (int g = 0; g < RG; g++) {
+        if (rb0 + g < nrhs) {
+          if (v0) Bs[r0 + (int64_t)(rb0 + g) * ldb] = y0[g];
+          if (v1) Bs[r1 + (int64_t)(rb0 + g) * ldb] = y1[g];
+        }
+      }
     }
   }
+  if (solve_only) return;
 #pragma unroll
   for (int j = 0; j < NP; j++) {
     if (v0 && (FULL || j < n)) As[r0 + (int64_t)j * lda] = ra[j];
@@ -166,17 +192,25 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
 
 cudaError_t launch_batched(int64_t n, double* A, int64_t lda, int64_t strideA, int64_t batch, double* B,
                            int64_t ldb, int64_t strideB, int64_t nrhs, const double* tau, bool tau_default,
-                           double tau_value, int32_t* info, cudaStream_t s) {
+                           double tau_value, int32_t* info, cudaStream_t s, bool solve_only) {
   if (batch <= 0 || n <= 0) return cudaSuccess;
   if (n > NP || nrhs > MAXRHS) return cudaErrorInvalidValue;
   const int64_t warps = (batch + 1) / 2;
   const int64_t blocks = (warps * 32 + 127) / 128;
-  if (n == NP)
-    batched_kernel<true><<<(unsigned)blocks, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, ldb, strideB, (int)nrhs,
-                                                          tau, tau_default ? 1 : 0, tau_value, info);
+  const int so = solve_only ? 1 : 0, td = tau_default ? 1 : 0;
+  const unsigned g = (unsigned)blocks;
+  if (n == NP && nrhs <= 1)
+    batched_kernel<true, 1><<<g, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, ldb, strideB, (int)nrhs, tau, td,
+                                             tau_value, info, so);
+  else if (n == NP)
+    batched_kernel<true, 4><<<g, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, ldb, strideB, (int)nrhs, tau, td,
+                                             tau_value, info, so);
+  else if (nrhs <= 1)
+    batched_kernel<false, 1><<<g, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, ldb, strideB, (int)nrhs, tau, td,
+                                              tau_value, info, so);
   else
-    batched_kernel<false><<<(unsigned)blocks, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, ldb, strideB,
-                                                           (int)nrhs, tau, tau_default ? 1 : 0, tau_value, info);
+    batched_kernel<false, 4><<<g, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, ldb, strideB, (int)nrhs, tau, td,
+                                              tau_value, info, so);
   return cudaGetLastError();
 }
 

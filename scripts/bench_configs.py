@@ -104,3 +104,15 @@ by = batch * (2 * 32 * 32 * 8 + 2 * 32 * 8 + 4)
 emit(config="C5", batch=batch, n=32, what="batched factor+solve", ms=med, ms_min=lo, ms_max=hi,
      gbs=by / med / 1e6, frac_hbm=by / med / 1e6 / HBM, systems_per_s=batch / med * 1e3,
      max_err=(Bw.transpose(1, 2) - db["X"]).abs().max().item(), bytes=by)
+
+# ---------------- f1: factor once, solve many (batched solve-only on the factors above)
+for nr in (1, 16):
+    Bn = torch.randn(batch, nr, 32, dtype=torch.float64, device=dev)
+    Bw2 = torch.empty_like(Bn)
+    med, lo, hi = timeit(lambda: Bw2.copy_(Bn),
+                         lambda: ebv.ebv_lu_solve_batched(ctx.handle, 32, Aw.data_ptr(), 32, 1024, batch,
+                                                          Bw2.data_ptr(), 32, 32 * nr, nr, sh))
+    by = batch * (32 * 32 * 8 + 2 * 32 * nr * 8)
+    emit(config="C5-solve-only", batch=batch, n=32, nrhs=nr, what="batched solve (pre-factored)", ms=med,
+         ms_min=lo, ms_max=hi, gbs=by / med / 1e6, frac_hbm=by / med / 1e6 / HBM,
+         systems_per_s=batch / med * 1e3, bytes=by)

@@ -84,6 +84,7 @@ def test_argument_validation_without_gpu():
     assert L.ebv_update(None, 1, 1, 1, None, 1, None, 1, None, 1, None) == 1
     assert L.ebv_plan_owner_map(-1, 1, None) == 1
     assert L.ebv_block_width(None, 100) == 0
+    assert L.ebv_lu_solve_batched(None, 4, None, 4, 16, 1, None, 4, 4, 1, None) == 1
     assert L.ebv_stats_timeline(None, None, 0) == -1
     assert ebv.ebv_status_string(0) == "success"
     assert ebv.ebv_status_string(5) == "not supported"

@@ -242,6 +242,32 @@ def test_batched_bitwise(dev, ctx, n, batch, nrhs):
         assert bits_eq(Bt.transpose(1, 2).cpu().numpy(), x_o)
 
 
+@pytest.mark.parametrize("n,batch,nrhs", [(32, 1000, 1), (32, 333, 16), (7, 65, 3), (1, 4, 2), (31, 2, 5)])
+def test_batched_solve_only_bitwise(dev, ctx, n, batch, nrhs):
+    """Factor once, solve many: ebv_lu_solve_batched on the
+    factors of ebv_lu_factor_batched equals the oracle's solve of every
+    system bitwise, for two different right-hand-side sets, and leaves LU
+    untouched."""
+    db = ebv_inputs.generate_batched(batch, n, seed=3 * n + batch, nrhs=nrhs, device=dev)
+    LUt = db["At"].clone()
+    info = ebv.lu_factor_batched(LUt, None, ctx=ctx)
+    torch.cuda.synchronize()
+    assert not info.any().item()
+    lu_before = LUt.clone()
+    a = db["At"].transpose(1, 2).cpu().numpy()
+    lu_o = np.stack([oracle.lu_factor(a[s])[0] for s in range(batch)])
+    assert bits_eq(LUt.transpose(1, 2).cpu().numpy(), lu_o)
+    for rhs_seed in (0, 1):
+        B = db["B"] if rhs_seed == 0 else torch.flip(db["B"], dims=[1]) * 0.5
+        Bt = B.transpose(1, 2).clone(memory_format=torch.contiguous_format)
+        ebv.lu_solve_batched(LUt, Bt, ctx=ctx)
+        torch.cuda.synchronize()
+        b = B.cpu().numpy()
+        x_o = np.stack([oracle.lu_solve(lu_o[s], b[s]) for s in range(batch)])
+        assert bits_eq(Bt.transpose(1, 2).cpu().numpy(), x_o)
+    assert torch.equal(LUt, lu_before)
+
+
 def test_batched_full_size_c5(dev, ctx):
     """BASELINE.json configs[4]: 100k systems of n = 32, every system bitwise."""
     batch = 100_000
