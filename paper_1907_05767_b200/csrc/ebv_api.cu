@@ -141,6 +141,11 @@ cudaError_t lu_rec(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t ko
 // L11\U11 and the rows below become L21 (Eq 6 restricted to the w steps of
 // the panel).  Recursive on the panel width; the leaves fuse nothing but are
 // a diagonal-block LU (one CTA) + a row-parallel L21 = A21 U11^-1.
+static int64_t kSolveTrsmRhs = [] {
+  const char* e = getenv("EBV_SOLVE_TRSM_RHS");
+  return e ? (int64_t)atoll(e) : (int64_t)17;
+}();
+
 static int64_t kPanelLeafFusedRows = [] {
   const char* e = getenv("EBV_PANEL_FUSED_ROWS");
   return e ? (int64_t)atoll(e) : (int64_t)8192;
@@ -493,6 +498,16 @@ ebv_status_t ebv_lu_solve(ebv_context_t c, int64_t n, const double* LU, int64_t 
   if (!LU || !B) return invalid("ebv_lu_solve: NULL pointer");
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
+  if (nrhs >= kSolveTrsmRhs) {
+    // many right-hand sides (factor once, solve many — SURVEY §8f f1): the
+    // substitutions as recursive TRSMs, L^-1 then U^-1, whose off-diagonal
+    // blocks are DMMA updates (k ascending forward, descending backward):
+    // per entry the same fma chain and divisions as the wavefront kernel
+    cudaError_t e = trsm_l(c, n, nrhs, LU, lda, B, ldb, s);
+    if (e == cudaSuccess) e = trsm_lu(c, n, nrhs, LU, lda, B, ldb, s);
+    if (e != cudaSuccess) return cuda_fail(e, "solve (trsm)");
+    return EBV_SUCCESS;
+  }
   const int64_t NB = (n + solve_block_rows() - 1) / solve_block_rows();
   ebv_status_t st = ensure_flags(c, 2 * NB);
   if (st != EBV_SUCCESS) return st;

@@ -210,6 +210,20 @@ def test_block_width_query(dev):
     assert c.block_width(1000) == -1
 
 
+@pytest.mark.parametrize("n,nrhs", [(700, 64), (700, 16), (700, 17), (1537, 100), (129, 300), (64, 64)])
+def test_solve_many_rhs_bitwise(dev, ctx, n, nrhs):
+    """nrhs > 16 takes the recursive-TRSM (DMMA) solve, fewer the wavefront
+    kernel: both bitwise the oracle's substitutions."""
+    d = ebv_inputs.generate(n, seed=n + nrhs, nrhs=nrhs, device=dev)
+    A = d["At"].T
+    LU, info = ebv.lu_factor(A, ctx=ctx)
+    X = ebv.lu_solve(LU, d["B"], ctx=ctx)
+    torch.cuda.synchronize()
+    lu_o, _ = oracle.lu_factor(A.cpu().numpy())
+    assert bits_eq(LU.cpu().numpy(), lu_o)
+    assert bits_eq(X.cpu().numpy(), oracle.lu_solve(lu_o, d["B"].cpu().numpy()))
+
+
 # ------------------------------------------------------------------ vector path (EbV owner map)
 @pytest.mark.parametrize("n,ctas", [(1, 0), (2, 0), (3, 0), (64, 0), (255, 0), (1024, 0), (1024, 128), (1024, -128),
                                     (1000, 100), (1536, 0), (300, -7), (301, 5), (33, 1)])
