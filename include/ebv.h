@@ -159,10 +159,12 @@ ebv_status_t ebv_lu_factor(ebv_context_t ctx, int64_t n, double* A, int64_t lda,
  *   B      device, n x nrhs column-major (ldb >= max(1,n)), overwritten by X
  * Each right-hand side column is processed in the canonical order (forward:
  * y_i = fma chain over ascending k of -l_ik y_k from b_i; backward: x_k =
- * y_k / u_kk, then y_i -= u_ik x_k for i < k, k descending).  Up to 16
- * right-hand sides run in the wavefront substitution kernels; more (factor
- * once, solve many) as recursive TRSMs whose off-diagonal blocks are DMMA
- * updates — the same per-entry operations, bitwise the same X.
+ * y_k / u_kk, then y_i -= u_ik x_k for i < k, k descending).  A few
+ * right-hand sides run as interleaved single-column wavefront chains (one
+ * launch per sweep per 64 columns); many (factor once, solve many: above
+ * 128, or above 64 / 40 for n > 8192 / 16384) as recursive TRSMs whose
+ * off-diagonal blocks are DMMA updates — the same per-entry operations,
+ * bitwise the same X.
  * Errors: INVALID_VALUE for n < 0, nrhs < 0, lda/ldb < max(1,n), NULL
  * pointers when n > 0 and nrhs > 0. */
 ebv_status_t ebv_lu_solve(ebv_context_t ctx, int64_t n, const double* LU, int64_t lda, double* B,

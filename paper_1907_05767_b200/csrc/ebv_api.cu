@@ -141,10 +141,19 @@ cudaError_t lu_rec(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t ko
 // L11\U11 and the rows below become L21 (Eq 6 restricted to the w steps of
 // the panel).  Recursive on the panel width; the leaves fuse nothing but are
 // a diagonal-block LU (one CTA) + a row-parallel L21 = A21 U11^-1.
+// Solve path: interleaved wavefront chains (one launch per sweep per 64
+// columns) vs recursive TRSM with DMMA updates (flat in nrhs, latency-bound
+// by its ~n/32 launches).  Crossovers measured on B200
+// (profiles/r01_solve_rhs_sweep.jsonl): n = 8192: wavefront 5.6 ms at 64
+// columns vs TRSM 12.5; n = 32768: 42 vs 56 ms at 32 columns, 79 vs 58 at 64.
 static int64_t kSolveTrsmRhs = [] {
   const char* e = getenv("EBV_SOLVE_TRSM_RHS");
-  return e ? (int64_t)atoll(e) : (int64_t)17;
+  return e ? (int64_t)atoll(e) : (int64_t)0;
 }();
+static bool solve_use_trsm(int64_t n, int64_t nrhs) {
+  if (kSolveTrsmRhs > 0) return nrhs >= kSolveTrsmRhs;
+  return nrhs > 128 || (n > 8192 && nrhs > 64) || (n > 16384 && nrhs > 40);
+}
 
 static int64_t kPanelLeafFusedRows = [] {
   const char* e = getenv("EBV_PANEL_FUSED_ROWS");
@@ -498,7 +507,7 @@ ebv_status_t ebv_lu_solve(ebv_context_t c, int64_t n, const double* LU, int64_t 
   if (!LU || !B) return invalid("ebv_lu_solve: NULL pointer");
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
-  if (nrhs >= kSolveTrsmRhs) {
+  if (solve_use_trsm(n, nrhs)) {
     // many right-hand sides (factor once, solve many — SURVEY §8f f1): the
     // substitutions as recursive TRSMs, L^-1 then U^-1, whose off-diagonal
     // blocks are DMMA updates (k ascending forward, descending backward):
@@ -509,12 +518,12 @@ ebv_status_t ebv_lu_solve(ebv_context_t c, int64_t n, const double* LU, int64_t 
     return EBV_SUCCESS;
   }
   const int64_t NB = (n + solve_block_rows() - 1) / solve_block_rows();
-  ebv_status_t st = ensure_flags(c, 2 * NB);
+  ebv_status_t st = ensure_flags(c, 2 * NB * solve_max_interleave());   // interleaved columns per sweep
   if (st != EBV_SUCCESS) return st;
   c->solve_epoch++;
-  const int64_t groups = (nrhs + 15) / 16;
+  const int64_t groups = (nrhs + 63) / 64;
   double by = (8.0 * n * n + 4.0 * 8.0 * n * nrhs), fl = 2.0 * n * n * nrhs;
-  cudaError_t e = timed(c, KC_SOLVE, fl, by, s, (int)(4 * groups), [&] {
+  cudaError_t e = timed(c, KC_SOLVE, fl, by, s, (int)(2 * groups), [&] {
     return launch_solve(n, LU, lda, B, ldb, nrhs, c->d_ticket, c->d_flags, c->solve_epoch, s);
   });
   if (e != cudaSuccess) return cuda_fail(e, "solve");

@@ -28,6 +28,7 @@ namespace {
 constexpr int BR = 64;          // rows per block (= threads per CTA)
 constexpr int MAXR = 16;        // max right-hand sides per launch
 constexpr int TSTR = BR + 1;    // diagonal tile column stride in smem
+constexpr int kMaxInterleave = 64;   // single-column chains per launch (flags: 2 * 64 * NB)
 
 __device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
@@ -53,6 +54,7 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 #ifdef EBV_SOLVE_TRACE
 // probes/solve_trace.cu: per-block phase timestamps (%globaltimer, ns)
 __device__ unsigned long long g_trace[2][8192][6];
+__device__ int g_redo;
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -103,8 +105,8 @@ __device__ __forceinline__ double quot(double y, double u, double r, bool own, b
 // updated).  The full solve is the window [0, NB) with cbase = 0.
 template <bool FORWARD, int NR>
 __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __restrict__ LU, int64_t lda,
-                                                   double* B, int64_t ldb, int nrhs, int* ticket, int* flags,
-                                                   int epoch, int64_t jlo, int64_t jhi, int64_t cbase) {
+                                                   double* B0, int64_t ldb, int nrhs, int* ticket, int* flags0,
+                                                   int epoch, int64_t jlo, int64_t jhi, int64_t cbase, int nind) {
   __shared__ double sd[BR * TSTR];          // diagonal tile: sd[c*TSTR + r] = LU(I*BR + r, I*BR + c)
   __shared__ double sbuf[BR * MAXR];        // published values of block J (sy[k*MAXR + r]),
   double* sy = sbuf;                        // then the hand-off to the diagonal warps (sacc)
@@ -119,8 +121,16 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
     __syncthreads();
     const int64_t t = s_blk;
     __syncthreads();
-    if (t >= (FORWARD ? NB - jlo : jhi)) return;
-    const int64_t I = FORWARD ? jlo + t : jhi - 1 - t;
+    // nind > 1 (NR = 1): nind single-column solves interleaved in ticket
+    // order — ticket t is column t % nind, block t / nind — so each column's
+    // chain runs alongside the others' (a block waits only on blocks of its
+    // own column with smaller tickets: no deadlock at any residency)
+    if (t >= (FORWARD ? NB - jlo : jhi) * nind) return;
+    const int rr = (int)(t % nind);
+    const int64_t tq = t / nind;
+    double* B = B0 + (int64_t)rr * ldb;
+    int* flags = flags0 + (int64_t)rr * NB;
+    const int64_t I = FORWARD ? jlo + tq : jhi - 1 - tq;
     const bool diag = I >= jlo && I < jhi;
     const int64_t row = I * BR + i;
     const bool rv = row < n;
@@ -272,6 +282,9 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
         // any unverified quotient (checked by its owner lane) -> redo the
         // block with true division
         if (__any_sync(0xffffffffu, !ok)) {
+#ifdef EBV_SOLVE_TRACE
+          if (lane == 0) atomicAdd(&g_redo, 1);
+#endif
 #pragma unroll
           for (int q = 0; q < HR; q++) { v0[q] = w0[q]; v1[q] = w1[q]; }
           for (int k = BR - 1; k >= 32; k--) {
@@ -333,24 +346,32 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
   }
 }
 
-template <bool FWD>
-cudaError_t launch_one(int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb, int nr, int* ticket,
-                       int* flags, int ep, int64_t grid, cudaStream_t s, int64_t jlo, int64_t jhi, int64_t cbase) {
-  if (nr == 1)
-    solve_kernel<FWD, 1><<<(unsigned)grid, BR, 0, s>>>(n, LU, lda, B, ldb, nr, ticket, flags, ep, jlo, jhi, cbase);
-  else
-    solve_kernel<FWD, 0><<<(unsigned)grid, BR, 0, s>>>(n, LU, lda, B, ldb, nr, ticket, flags, ep, jlo, jhi, cbase);
-  return cudaGetLastError();
-}
-
-int64_t resident_grid(int64_t units) {
+template <class K>
+int64_t resident_grid(int64_t units, K kern) {
   int dev = 0, sms = 148, per_sm = 8;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<true, 0>, BR, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BR, 0);
   if (per_sm < 1) per_sm = 1;
   const int64_t cap = (int64_t)sms * per_sm;
   return units < cap ? units : cap;
+}
+
+// nind independent single columns interleaved (nr == 1 per column), or one
+// launch carrying nr <= MAXR columns together (nind == 1)
+template <bool FWD>
+cudaError_t launch_one(int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb, int nr, int* ticket,
+                       int* flags, int ep, int64_t units, cudaStream_t s, int64_t jlo, int64_t jhi, int64_t cbase,
+                       int nind = 1) {
+  if (nr == 1) {
+    const int64_t grid = resident_grid(units * nind, solve_kernel<FWD, 1>);
+    solve_kernel<FWD, 1><<<(unsigned)grid, BR, 0, s>>>(n, LU, lda, B, ldb, nr, ticket, flags, ep, jlo, jhi, cbase,
+                                                       nind);
+  } else {
+    const int64_t grid = resident_grid(units, solve_kernel<FWD, 0>);
+    solve_kernel<FWD, 0><<<(unsigned)grid, BR, 0, s>>>(n, LU, lda, B, ldb, nr, ticket, flags, ep, jlo, jhi, cbase, 1);
+  }
+  return cudaGetLastError();
 }
 
 }  // namespace
@@ -361,17 +382,19 @@ cudaError_t launch_solve(int64_t n, const double* LU, int64_t lda, double* B, in
                          int* ticket_ws, int* flags_ws, int64_t epoch, cudaStream_t s) {
   if (n <= 0 || nrhs <= 0) return cudaSuccess;
   const int64_t NB = (n + BR - 1) / BR;
-  const int64_t grid = resident_grid(NB);
-  for (int64_t r0 = 0; r0 < nrhs; r0 += MAXR) {
-    const int nr = (int)((nrhs - r0) < MAXR ? (nrhs - r0) : MAXR);
+  // the columns as interleaved single-column chains, up to kMaxInterleave
+  // per launch (flags: nind * NB per sweep): they run side by side instead of
+  // sharing two warps of one CTA per row block
+  for (int64_t g0 = 0; g0 < nrhs; g0 += kMaxInterleave) {
+    const int nind = (int)((nrhs - g0) < kMaxInterleave ? (nrhs - g0) : kMaxInterleave);
     for (int pass = 0; pass < 2; pass++) {
       const bool fwd = pass == 0;
-      const int ep = (int)(((epoch * 64 + (r0 / MAXR) * 2 + pass) % 0x3FFFFFFF) + 1);
+      const int ep = (int)(((epoch * 64 + (g0 / kMaxInterleave) * 2 + pass) % 0x3FFFFFFF) + 1);
       cudaError_t e = cudaMemsetAsync(ticket_ws + pass, 0, sizeof(int), s);
       if (e != cudaSuccess) return e;
-      e = fwd ? launch_one<true>(n, LU, lda, B + r0 * ldb, ldb, nr, ticket_ws, flags_ws, ep, grid, s, 0, NB, 0)
-              : launch_one<false>(n, LU, lda, B + r0 * ldb, ldb, nr, ticket_ws + 1, flags_ws + NB, ep, grid, s, 0, NB,
-                                  0);
+      e = fwd ? launch_one<true>(n, LU, lda, B + g0 * ldb, ldb, 1, ticket_ws, flags_ws, ep, NB, s, 0, NB, 0, nind)
+              : launch_one<false>(n, LU, lda, B + g0 * ldb, ldb, 1, ticket_ws + 1, flags_ws + (int64_t)nind * NB, ep,
+                                  NB, s, 0, NB, 0, nind);
       if (e != cudaSuccess) return e;
     }
   }
@@ -389,11 +412,12 @@ cudaError_t launch_solve_window(int64_t n, const double* LUw, int64_t ldl, int64
   if (nrhs > MAXR || c0 % BR) return cudaErrorInvalidValue;
   const int64_t NB = (n + BR - 1) / BR;
   const int64_t jlo = c0 / BR, jhi = (c0 + w + BR - 1) / BR;
-  const int64_t grid = resident_grid(fwd ? NB - jlo : jhi);
-  return fwd ? launch_one<true>(n, LUw, ldl, B, ldb, (int)nrhs, ticket, flags, epoch, grid, s, jlo, jhi, c0)
-             : launch_one<false>(n, LUw, ldl, B, ldb, (int)nrhs, ticket, flags, epoch, grid, s, jlo, jhi, c0);
+  const int64_t units = fwd ? NB - jlo : jhi;
+  return fwd ? launch_one<true>(n, LUw, ldl, B, ldb, (int)nrhs, ticket, flags, epoch, units, s, jlo, jhi, c0)
+             : launch_one<false>(n, LUw, ldl, B, ldb, (int)nrhs, ticket, flags, epoch, units, s, jlo, jhi, c0);
 }
 
 int64_t solve_max_rhs() { return MAXR; }
+int64_t solve_max_interleave() { return kMaxInterleave; }
 
 }  // namespace ebv

@@ -18,8 +18,8 @@ int main(int argc, char** argv) {
   cudaMalloc(&dLU, (size_t)n * n * 8);
   cudaMalloc(&dB, (size_t)n * nrhs * 8);
   cudaMalloc(&ticket, 8);
-  cudaMalloc(&flags, 2 * ((n + 63) / 64) * 4);
-  cudaMemset(flags, 0, 2 * ((n + 63) / 64) * 4);
+  cudaMalloc(&flags, 128 * ((n + 63) / 64) * 4);
+  cudaMemset(flags, 0, 128 * ((n + 63) / 64) * 4);
   cudaMemcpy(dLU, hLU.data(), (size_t)n * n * 8, cudaMemcpyHostToDevice);
   std::vector<double> hB((size_t)n * nrhs, 1.0);
   cudaEvent_t e0, e1;
@@ -35,6 +35,9 @@ int main(int argc, char** argv) {
   }
   static unsigned long long tr[2][8192][6];
   cudaMemcpyFromSymbol(tr, ebv::g_trace, sizeof(tr));
+  int redo = 0;
+  cudaMemcpyFromSymbol(&redo, ebv::g_redo, sizeof(int));
+  printf("backward blocks redone with true division (all reps, per warp): %d\n", redo);
   int64_t NB = (n + 63) / 64;
   for (int d = 0; d < 2; d++) {
     unsigned long long t0 = ~0ull;

@@ -13,7 +13,7 @@ for n in (int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "4096,8192").sp
     d = ebv_inputs.generate(n, seed=1, device=dev)
     with torch.cuda.stream(s):
         LU, info = ebv.lu_factor(d["At"].T, ctx=ctx)
-        for nr in (1, 16, 32, 64, 128, 256, 1024):
+        for nr in (1, 2, 4, 16, 32, 64, 65, 128, 256, 1024):
             B0 = torch.randn(nr, n, dtype=torch.float64, device=dev)
             Bw = torch.empty_like(B0)
             ts = []

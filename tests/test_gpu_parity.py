@@ -210,10 +210,10 @@ def test_block_width_query(dev):
     assert c.block_width(1000) == -1
 
 
-@pytest.mark.parametrize("n,nrhs", [(700, 64), (700, 16), (700, 17), (1537, 100), (129, 300), (64, 64)])
+@pytest.mark.parametrize("n,nrhs", [(700, 64), (700, 16), (700, 17), (1537, 100), (129, 300), (64, 65), (333, 2)])
 def test_solve_many_rhs_bitwise(dev, ctx, n, nrhs):
-    """nrhs > 16 takes the recursive-TRSM (DMMA) solve, fewer the wavefront
-    kernel: both bitwise the oracle's substitutions."""
+    """Up to 64 columns: interleaved wavefront chains; more: recursive TRSM
+    with DMMA updates — both bitwise the oracle's substitutions."""
     d = ebv_inputs.generate(n, seed=n + nrhs, nrhs=nrhs, device=dev)
     A = d["At"].T
     LU, info = ebv.lu_factor(A, ctx=ctx)
