@@ -318,10 +318,10 @@ ebv_status_t dist_solve(ebv_context* c, ebv_dist_state* d, std::vector<View>& vi
       if (v.plan.rank == p0.owner(J)) return &v;
     return nullptr;
   };
-  const int64_t G = solve_max_rhs();
+  const int64_t G = solve_max_interleave();
   const int64_t groups = (nrhs + G - 1) / G;
   const int64_t NBr = (n + solve_block_rows() - 1) / solve_block_rows();
-  const int64_t nflags = 2 * NBr * groups, ntick = 2 * N * groups;
+  const int64_t nflags = 2 * NBr * G * groups, ntick = 2 * N * groups;
   if (nflags + ntick > d->sws_cap) {
     if (d->sws) cudaFree(d->sws);
     d->sws = nullptr;
@@ -354,7 +354,7 @@ ebv_status_t dist_solve(ebv_context* c, ebv_dist_state* d, std::vector<View>& vi
       const double* Lk = v->A + v->plan.loc[K] * v->lda;
       for (int64_t g = 0; g < groups; g++) {
         const int64_t r0 = g * G, nr = nrhs - r0 < G ? nrhs - r0 : G;
-        int* fl = flags + (g * 2 + pass) * NBr;
+        int* fl = flags + (g * 2 + pass) * NBr * G;
         int* tk = tick + (g * 2 + pass) * N + K;
         e = timed(c, KC_SOLVE, 2.0 * w * (fwd ? n - c0 : c0 + w) * nr, 8.0 * w * (fwd ? n - c0 : c0 + w), s, 1,
                   [&] { return launch_solve_window(n, Lk, v->lda, c0, w, fwd, B + r0 * ldb, ldb, nr, tk, fl, ep, s); });

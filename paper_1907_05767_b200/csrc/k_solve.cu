@@ -357,20 +357,17 @@ int64_t resident_grid(int64_t units, K kern) {
   return units < cap ? units : cap;
 }
 
-// nind independent single columns interleaved (nr == 1 per column), or one
-// launch carrying nr <= MAXR columns together (nind == 1)
+// nind independent single columns interleaved (the kernel's NR = 1 form; the
+// several-columns-per-warp form, NR = 0, is kept in the source but no
+// longer launched: interleaved chains were 4x faster at 16 columns)
 template <bool FWD>
 cudaError_t launch_one(int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb, int nr, int* ticket,
                        int* flags, int ep, int64_t units, cudaStream_t s, int64_t jlo, int64_t jhi, int64_t cbase,
-                       int nind = 1) {
-  if (nr == 1) {
-    const int64_t grid = resident_grid(units * nind, solve_kernel<FWD, 1>);
-    solve_kernel<FWD, 1><<<(unsigned)grid, BR, 0, s>>>(n, LU, lda, B, ldb, nr, ticket, flags, ep, jlo, jhi, cbase,
-                                                       nind);
-  } else {
-    const int64_t grid = resident_grid(units, solve_kernel<FWD, 0>);
-    solve_kernel<FWD, 0><<<(unsigned)grid, BR, 0, s>>>(n, LU, lda, B, ldb, nr, ticket, flags, ep, jlo, jhi, cbase, 1);
-  }
+                       int nind) {
+  if (nr != 1) return cudaErrorInvalidValue;
+  const int64_t grid = resident_grid(units * nind, solve_kernel<FWD, 1>);
+  solve_kernel<FWD, 1><<<(unsigned)grid, BR, 0, s>>>(n, LU, lda, B, ldb, nr, ticket, flags, ep, jlo, jhi, cbase,
+                                                     nind);
   return cudaGetLastError();
 }
 
@@ -403,18 +400,20 @@ cudaError_t launch_solve(int64_t n, const double* LU, int64_t lda, double* B, in
 
 // One column window of the ring solve: forward (fwd) or backward sweep of
 // the columns [c0, c0 + w) (c0 a multiple of BR) whose entries are at
-// LUw[row + (col - c0) * ldl]; nrhs <= MAXR.  ticket: one zeroed int for this
-// launch; flags: the sweep's NB flags (released once per sweep by the block
+// LUw[row + (col - c0) * ldl]; nrhs <= kMaxInterleave right-hand sides as
+// interleaved single-column chains.  ticket: one zeroed int for this launch;
+// flags: the sweep's nrhs * NB flags (released once per sweep by the block
 // that substitutes them, so one epoch serves the whole sweep).
 cudaError_t launch_solve_window(int64_t n, const double* LUw, int64_t ldl, int64_t c0, int64_t w, bool fwd, double* B,
                                 int64_t ldb, int64_t nrhs, int* ticket, int* flags, int epoch, cudaStream_t s) {
   if (n <= 0 || nrhs <= 0 || w <= 0) return cudaSuccess;
-  if (nrhs > MAXR || c0 % BR) return cudaErrorInvalidValue;
+  if (nrhs > kMaxInterleave || c0 % BR) return cudaErrorInvalidValue;
   const int64_t NB = (n + BR - 1) / BR;
   const int64_t jlo = c0 / BR, jhi = (c0 + w + BR - 1) / BR;
   const int64_t units = fwd ? NB - jlo : jhi;
-  return fwd ? launch_one<true>(n, LUw, ldl, B, ldb, (int)nrhs, ticket, flags, epoch, units, s, jlo, jhi, c0)
-             : launch_one<false>(n, LUw, ldl, B, ldb, (int)nrhs, ticket, flags, epoch, units, s, jlo, jhi, c0);
+  const int nind = (int)nrhs;
+  return fwd ? launch_one<true>(n, LUw, ldl, B, ldb, 1, ticket, flags, epoch, units, s, jlo, jhi, c0, nind)
+             : launch_one<false>(n, LUw, ldl, B, ldb, 1, ticket, flags, epoch, units, s, jlo, jhi, c0, nind);
 }
 
 int64_t solve_max_rhs() { return MAXR; }
