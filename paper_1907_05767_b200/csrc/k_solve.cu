@@ -108,7 +108,8 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
                                                    double* B0, int64_t ldb, int nrhs, int* ticket, int* flags0,
                                                    int epoch, int64_t jlo, int64_t jhi, int64_t cbase, int nind) {
   __shared__ double sd[BR * TSTR];          // diagonal tile: sd[c*TSTR + r] = LU(I*BR + r, I*BR + c)
-  __shared__ double sbuf[BR * MAXR];        // published values of block J (sy[k*MAXR + r]),
+  constexpr int SR = NR > 0 ? NR : MAXR;    // shared stride per row (right-hand sides)
+  __shared__ double sbuf[BR * SR];          // published values of block J (sy[k*SR + r]),
   double* sy = sbuf;                        // then the hand-off to the diagonal warps (sacc)
   double* sacc = sbuf;
   __shared__ int s_blk;
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
       for (int idx = i; idx < BR * nr; idx += BR) {
         const int k = idx % BR, r = idx / BR;
         const int64_t rk = J * BR + k;
-        sy[k * MAXR + r] = (rk < n) ? __ldcg(B + rk + (int64_t)r * ldb) : 0.0;
+        sy[k * SR + r] = (rk < n) ? __ldcg(B + rk + (int64_t)r * ldb) : 0.0;
       }
       __syncthreads();
       if (FORWARD) {
@@ -173,13 +174,13 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
         for (int k = 0; k < BR; k++)
 #pragma unroll
           for (int r = 0; r < MAXR; r++)
-            if (r < nr) acc[r] = fma(-l[k], sy[k * MAXR + r], acc[r]);
+            if (r < nr) acc[r] = fma(-l[k], sy[k * SR + r], acc[r]);
       } else {
 #pragma unroll
         for (int k = BR - 1; k >= 0; k--)
 #pragma unroll
           for (int r = 0; r < MAXR; r++)
-            if (r < nr) acc[r] = fma(-l[k], sy[k * MAXR + r], acc[r]);
+            if (r < nr) acc[r] = fma(-l[k], sy[k * SR + r], acc[r]);
       }
     }
 
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
     EBV_TR(3);
 #pragma unroll
     for (int r = 0; r < MAXR; r++)
-      if (r < nr) sacc[i * MAXR + r] = acc[r];
+      if (r < nr) sacc[i * SR + r] = acc[r];
     __syncthreads();
     {
       constexpr int HR = MAXR / 2;
@@ -213,8 +214,8 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
 #pragma unroll
       for (int q = 0; q < HR; q++) {
         const int r = warp + 2 * q;
-        v0[q] = (q < myr) ? sacc[lane * MAXR + r] : 0.0;
-        v1[q] = (q < myr) ? sacc[(lane + 32) * MAXR + r] : 0.0;
+        v0[q] = (q < myr) ? sacc[lane * SR + r] : 0.0;
+        v1[q] = (q < myr) ? sacc[(lane + 32) * SR + r] : 0.0;
       }
       (void)nw;
       if (FORWARD) {
