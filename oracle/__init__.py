@@ -55,6 +55,10 @@ def _load():
         lib.oracle_lu_factor_batched.argtypes = [i64, vp, i64, i64, i64, vp, i64, i64, i64,
                                                  ctypes.c_double, vp]
         lib.oracle_lu_factor_batched.restype = None
+        lib.oracle_normalize_unit_diagonal.argtypes = [i64, vp, i64, vp, i64, i64, vp]
+        lib.oracle_normalize_unit_diagonal.restype = i64
+        lib.oracle_lu_to_ldu.argtypes = [i64, vp, i64, vp]
+        lib.oracle_lu_to_ldu.restype = None
         del dp
         _lib = lib
     return _lib
@@ -119,6 +123,38 @@ def lu_factor_batched(a: np.ndarray, b: np.ndarray | None = None, tau: float = 0
                                          info.ctypes.data)
         x = None
     return np.transpose(at, (0, 2, 1)), x, info
+
+
+def normalize_unit_diagonal(a: np.ndarray, b: np.ndarray | None = None):
+    """Row i of a (and of b) divided by a_ii (Eq 2).
+
+    Returns (a', b' or None, scales, info): a' has an exactly-1 diagonal,
+    scales[i] = 1/a_ii; info = first 1-based row with a_ii == 0 (left
+    unchanged, scale 0), else 0."""
+    an = _colmajor(a)
+    n = an.shape[0]
+    if b is None:
+        bn, nrhs, bptr = None, 0, None
+    else:
+        vec = np.ndim(b) == 1
+        bn = _colmajor(np.reshape(b, (n, -1)))
+        nrhs, bptr = bn.shape[1], bn.ctypes.data
+    scales = np.zeros(n)
+    info = _load().oracle_normalize_unit_diagonal(n, an.ctypes.data, n, bptr, n, nrhs, scales.ctypes.data)
+    if bn is not None and vec:
+        bn = bn[:, 0].copy()
+    return an, bn, scales, int(info)
+
+
+def lu_to_ldu(lu: np.ndarray):
+    """LDU form of a packed LU (Eq 3): returns (ldu, d) where ldu
+    keeps L (strict lower) and D (diagonal) and holds U' = D^-1 U (strict
+    upper, unit diagonal implicit)."""
+    ldu = _colmajor(lu)
+    n = ldu.shape[0]
+    d = np.zeros(n)
+    _load().oracle_lu_to_ldu(n, ldu.ctypes.data, n, d.ctypes.data)
+    return ldu, d
 
 
 def unpack(lu: np.ndarray):

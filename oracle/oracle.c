@@ -89,3 +89,40 @@ void oracle_lu_factor_batched(int64_t n, double* A, int64_t lda, int64_t strideA
     if (B) oracle_lu_solve(n, A + b * strideA, lda, B + b * strideB, ldb, nrhs);
   }
 }
+
+/* Unit-diagonal normalization (Eq 2: the coefficient matrix drawn
+ * with 1 on its diagonal; SPEC S:81-89 normalize_unit_diagonal; SURVEY §8f
+ * f3): row i of A and of B divided by a_ii (one correctly rounded division
+ * per entry, so the diagonal becomes exactly 1), scales[i] = 1 / a_ii.  A row
+ * with a_ii == 0 is left unchanged (scale 0) and reported: returns the first
+ * such 1-based row, else 0. */
+int64_t oracle_normalize_unit_diagonal(int64_t n, double* A, int64_t lda, double* B, int64_t ldb, int64_t nrhs,
+                                       double* scales) {
+  int64_t info = 0;
+  for (int64_t i = 0; i < n; i++) {
+    double d = A[i + i * lda];
+    if (d == 0.0) {
+      if (info == 0) info = i + 1;
+      scales[i] = 0.0;
+      continue;
+    }
+    for (int64_t j = 0; j < n; j++) A[i + j * lda] = A[i + j * lda] / d;
+    for (int64_t r = 0; r < nrhs; r++) B[i + r * ldb] = B[i + r * ldb] / d;
+    scales[i] = 1.0 / d;
+  }
+  return info;
+}
+
+/* LDU form of a packed Doolittle LU (Eq 3, where U is drawn with a
+ * unit diagonal; Eq 6-b's U_(k) row divided by its pivot; reading R1):
+ * A = L D U' with D = diag(U) and U'_kj = u_kj / u_kk (j > k, one correctly
+ * rounded division).  In place: the strict upper triangle becomes U', the
+ * diagonal keeps D (U' has an implicit unit diagonal, like L); D is also
+ * copied to d. */
+void oracle_lu_to_ldu(int64_t n, double* LU, int64_t lda, double* d) {
+  for (int64_t k = 0; k < n; k++) {
+    double p = LU[k + k * lda];
+    d[k] = p;
+    for (int64_t j = k + 1; j < n; j++) LU[k + j * lda] = LU[k + j * lda] / p;
+  }
+}

@@ -4,6 +4,8 @@ Each test names what fixes the expected value: the SPEC's worked examples
 (tests/golden, cited per entry), exact rational arithmetic, closed forms,
 LAPACK special cases, metamorphic invariants and brute force.
 """
+from fractions import Fraction
+
 import numpy as np
 import pytest
 import scipy.linalg
@@ -243,3 +245,63 @@ def test_no_pivot_failure_over_seeds():
     for seed in range(100):
         a, _, _ = gen(24, seed)
         assert oracle.lu_factor(a)[1] == 0
+
+
+# ---------------------------------------------------------------- f3: unit diagonal / LDU
+def test_spec_normalize_examples(golden):
+    for ex in golden["normalize_unit_diagonal"]:
+        a = np.array(ex["a"], dtype=np.float64)
+        out, _, scales, info = oracle.normalize_unit_diagonal(a)
+        assert info == ex["info"], ex["cite"]
+        if info == 0:
+            assert np.array_equal(out, np.array(ex["out"], dtype=np.float64)), ex["cite"]
+            assert np.array_equal(scales, np.array(ex["scales"], dtype=np.float64)), ex["cite"]
+
+
+def _ulp(x):
+    return np.spacing(np.abs(x))
+
+
+@pytest.mark.parametrize("n,seed", [(7, 1), (40, 2)])
+def test_normalize_is_correctly_rounded_and_preserves_dominance(n, seed):
+    """Each entry is within half an ulp of the exact quotient a_ij / a_ii
+    (exact rationals), the diagonal is exactly 1, strict row dominance
+    survives (Eq 2's shape), and the scaled right-hand side keeps the
+    solution up to rounding."""
+    d = ebv_inputs.generate(n, seed=seed, nrhs=1)
+    a = d["At"].T.numpy().copy()
+    b = d["B"].numpy().copy()
+    out, bn, scales, info = oracle.normalize_unit_diagonal(a, b)
+    assert info == 0
+    assert np.all(np.diag(out) == 1.0)
+    for i in range(n):
+        for j in range(n):
+            exact = Fraction(a[i, j]) / Fraction(a[i, i])
+            assert abs(Fraction(out[i, j]) - exact) <= Fraction(_ulp(out[i, j])) / 2
+        assert abs(Fraction(scales[i]) - 1 / Fraction(a[i, i])) <= Fraction(_ulp(scales[i])) / 2
+    off = np.abs(out).sum(axis=1) - 1.0
+    assert np.all(off < 1.0)
+    x = oracle.solve(out, bn)[0]
+    assert np.max(np.abs(x - d["X"].numpy())) <= 1e-12
+
+
+def test_ldu_of_symmetric_matrix_has_u_prime_equal_l_transpose():
+    """For symmetric A, A = L D U' = L D L^T, so U' = L^T (a property of the
+    factorization, not of the code): checked on the closed-form family
+    alpha I + beta s s^T to a few ulps, with D = diag(U) bitwise and L
+    untouched bitwise."""
+    n = 60
+    s_ = np.where(np.random.default_rng(3).random(n) < 0.5, -1.0, 1.0)
+    a = closed_form.matrix(n, float(n), 1.0, s_)
+    lu, _ = oracle.lu_factor(a)
+    ldu, dvec = oracle.lu_to_ldu(lu)
+    assert np.array_equal(dvec, np.diag(lu))
+    assert np.array_equal(np.tril(ldu), np.tril(lu))
+    L = np.tril(lu, -1)
+    up = np.triu(ldu, 1)
+    assert np.max(np.abs(up - L.T)) <= 4 * np.finfo(float).eps * np.max(np.abs(L))
+    # and every U' entry is the correctly rounded quotient u_kj / u_kk
+    for k in range(n):
+        for j in range(k + 1, n):
+            exact = Fraction(lu[k, j]) / Fraction(lu[k, k])
+            assert abs(Fraction(ldu[k, j]) - exact) <= Fraction(_ulp(ldu[k, j])) / 2
