@@ -196,6 +196,29 @@ ebv_status_t ebv_lu_solve_batched(ebv_context_t ctx, int64_t n, const double* LU
                                   int64_t strideA, int64_t batch, double* B, int64_t ldb,
                                   int64_t strideB, int64_t nrhs, void* stream);
 
+/* Unit-diagonal normalization (Eq 2: the coefficient matrix drawn
+ * with 1 on its diagonal): row i of A (n x n,
+ * lda) and, if B != NULL, of B (n x nrhs, ldb) divided by a_ii — one
+ * correctly rounded division per entry, so the diagonal becomes exactly 1
+ * and the solution is unchanged up to rounding; d_scales[i] = 1/a_ii (may be
+ * NULL).  A row with a_ii == 0 is left unchanged (scale 0) and reported in
+ * d_info (device int64) as the first such 1-based row, else 0.  All pointers
+ * device, column-major; asynchronous on `stream`.
+ * Errors: INVALID_VALUE for negative sizes, leading dimensions < n, NULL
+ * A / d_info. */
+ebv_status_t ebv_normalize_unit_diagonal(ebv_context_t ctx, int64_t n, double* A, int64_t lda, double* B,
+                                         int64_t ldb, int64_t nrhs, double* d_scales, int64_t* d_info,
+                                         void* stream);
+
+/* LDU form of a packed LU from ebv_lu_factor (Eq 3, which draws U
+ * with a unit diagonal; Eq 6-b's U_(k) row divided by its pivot):
+ * A = L D U' with D = diag(U) copied to d_D (device, n doubles) and, in
+ * place, u'_kj = u_kj / u_kk for j > k (one correctly rounded division); the
+ * strict lower triangle (L) and the diagonal (D) are unchanged, U' has an
+ * implicit unit diagonal.  Errors: INVALID_VALUE for n < 0, lda < n, NULL
+ * pointers. */
+ebv_status_t ebv_lu_to_ldu(ebv_context_t ctx, int64_t n, double* LU, int64_t lda, double* d_D, void* stream);
+
 /* The trailing rank-k update of Eq 6-c on its own — the DMMA
  * contraction every blocked / distributed schedule is built from:
  *     C <- C - A * B      A: M x K (lda), B: K x N (ldb), C: M x N (ldc),

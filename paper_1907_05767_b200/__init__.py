@@ -49,6 +49,8 @@ SIGNATURES = {
     "ebv_lu_solve": (_int, [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp]),
     "ebv_lu_factor_batched": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _d, _vp, _vp]),
     "ebv_lu_solve_batched": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _vp]),
+    "ebv_normalize_unit_diagonal": (_int, [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp]),
+    "ebv_lu_to_ldu": (_int, [_vp, _i64, _vp, _i64, _vp, _vp]),
     "ebv_update": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp]),
     "ebv_get_unique_id": (_int, [_vp]),
     "ebv_create_dist": (_int, [ctypes.POINTER(_vp), _int, _vp, _int, _int, _i64, _int]),
@@ -157,6 +159,30 @@ def ebv_lu_factor_batched(ctx, n, A, lda, strideA, batch, B, ldb, strideB, nrhs,
 
 def ebv_lu_solve_batched(ctx, n, LU, lda, strideA, batch, B, ldb, strideB, nrhs, stream):
     return lib().ebv_lu_solve_batched(ctx, n, LU, lda, strideA, batch, B, ldb, strideB, nrhs, stream)
+
+
+def ebv_normalize_unit_diagonal(ctx, n, A, lda, B, ldb, nrhs, d_scales, d_info, stream):
+    return lib().ebv_normalize_unit_diagonal(ctx, n, A, lda, B, ldb, nrhs, d_scales, d_info, stream)
+
+
+def ebv_lu_to_ldu(ctx, n, LU, lda, d_D, stream):
+    return lib().ebv_lu_to_ldu(ctx, n, LU, lda, d_D, stream)
+
+
+def ebv_stats_timeline(ctx, out, max_records):
+    return lib().ebv_stats_timeline(ctx, out, max_records)
+
+
+def ebv_stats_enable(ctx, enable):
+    return lib().ebv_stats_enable(ctx, enable)
+
+
+def ebv_stats_reset(ctx):
+    return lib().ebv_stats_reset(ctx)
+
+
+def ebv_stats_get(ctx, kclass, launches, ms, flops, bytes_):
+    return lib().ebv_stats_get(ctx, kclass, launches, ms, flops, bytes_)
 
 
 def ebv_update(ctx, M, N, K, A, lda, B, ldb, C, ldc, stream):
@@ -448,6 +474,44 @@ def lu_factor_batched(At: torch.Tensor, Bt: torch.Tensor | None = None, tau: flo
     _check(ebv_lu_factor_batched(ctx.handle, n, At.data_ptr(), max(n, 1), n * n, batch, bptr, ldb, sb, nrhs,
                                  float(tau), info.data_ptr(), _stream_handle(At.device)), "ebv_lu_factor_batched")
     return info
+
+
+def normalize_unit_diagonal(A: torch.Tensor, B: torch.Tensor | None = None, ctx: Context | None = None):
+    """Row i of A (and of B) divided by a_ii (Eq 2).  A: (n, n)
+    CUDA float64, logical indexing; B: (n,) or (n, nrhs) or None.  Returns
+    (A', B' or None, scales, info) with new column-major A' / B'."""
+    _require(A, "A")
+    n = A.shape[0]
+    ctx = ctx or default_context(A.device.index or 0)
+    Ac = A.mT.contiguous().mT.clone() if _colmajor_ld(A) < 0 else A.clone()
+    Bc, nrhs = None, 0
+    if B is not None:
+        _require(B, "B")
+        B2 = B.reshape(n, -1)
+        Bc = B2.mT.contiguous().mT.clone()
+        nrhs = Bc.shape[1]
+    scales = torch.empty(n, dtype=torch.float64, device=A.device)
+    info = torch.zeros((), dtype=torch.int64, device=A.device)
+    _check(lib().ebv_normalize_unit_diagonal(ctx.handle, n, Ac.data_ptr(), max(_colmajor_ld(Ac), 1),
+                                             Bc.data_ptr() if Bc is not None else None, max(n, 1), nrhs,
+                                             scales.data_ptr(), info.data_ptr(), _stream_handle(A.device)),
+           "ebv_normalize_unit_diagonal")
+    if Bc is not None and B.dim() == 1:
+        Bc = Bc[:, 0]
+    return Ac, Bc, scales, info
+
+
+def lu_to_ldu(LU: torch.Tensor, ctx: Context | None = None):
+    """LDU form of a packed LU (Eq 3): returns (LDU, D) — a column-major copy
+    with U' = D^-1 U in its strict upper triangle, and D = diag(U)."""
+    _require(LU, "LU")
+    n = LU.shape[0]
+    ctx = ctx or default_context(LU.device.index or 0)
+    Lc = LU.mT.contiguous().mT.clone() if _colmajor_ld(LU) < 0 else LU.clone()
+    D = torch.empty(n, dtype=torch.float64, device=LU.device)
+    _check(lib().ebv_lu_to_ldu(ctx.handle, n, Lc.data_ptr(), max(_colmajor_ld(Lc), 1), D.data_ptr(),
+                               _stream_handle(LU.device)), "ebv_lu_to_ldu")
+    return Lc, D
 
 
 def lu_solve_batched(LUt: torch.Tensor, Bt: torch.Tensor, ctx: Context | None = None) -> torch.Tensor:

@@ -344,6 +344,7 @@ ebv_status_t ebv_destroy(ebv_context_t c) {
   if (!c) return invalid("ebv_destroy: NULL");
   DeviceGuard g(c->device);
   dist_release(c);
+  if (c->d_vec) cudaFree(c->d_vec);
   for (auto& r : c->recs) { cudaEventDestroy(r.e0); cudaEventDestroy(r.e1); }
   for (auto e : c->pool) cudaEventDestroy(e);
   for (auto& en : c->gcache)
@@ -578,6 +579,47 @@ ebv_status_t ebv_lu_solve_batched(ebv_context_t c, int64_t n, const double* LU, 
                           nullptr, s, /*solve_only=*/true);
   });
   if (e != cudaSuccess) return cuda_fail(e, "batched solve");
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_normalize_unit_diagonal(ebv_context_t c, int64_t n, double* A, int64_t lda, double* B, int64_t ldb,
+                                         int64_t nrhs, double* d_scales, int64_t* d_info, void* stream) {
+  if (!c) return invalid("ebv_normalize_unit_diagonal: NULL ctx");
+  if (n < 0 || nrhs < 0) return invalid("ebv_normalize_unit_diagonal: negative size");
+  if (lda < (n > 1 ? n : 1)) return invalid("ebv_normalize_unit_diagonal: lda too small");
+  if (B && nrhs > 0 && ldb < (n > 1 ? n : 1)) return invalid("ebv_normalize_unit_diagonal: ldb too small");
+  if (!d_info || (n > 0 && !A)) return invalid("ebv_normalize_unit_diagonal: NULL pointer");
+  DeviceGuard g(c->device);
+  if (n > c->vec_cap) {
+    if (c->d_vec) cudaFree(c->d_vec);
+    c->d_vec = nullptr;
+    c->vec_cap = 0;
+    if (cudaMalloc(&c->d_vec, n * sizeof(double)) != cudaSuccess) { set_error("workspace alloc failed"); return EBV_ERR_ALLOC; }
+    c->vec_cap = n;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t nl = 0;
+  cudaError_t e = timed(c, KC_OTHER, (double)n * (n + nrhs), 16.0 * n * (n + (B ? nrhs : 0)), s, 0, [&] {
+    return launch_normalize_unit_diagonal(n, A, lda, B, ldb, B ? nrhs : 0, d_scales, d_info, c->d_vec,
+                                          reinterpret_cast<unsigned long long*>(c->d_scratch), s, &nl);
+  });
+  c->launches += nl;
+  if (e != cudaSuccess) return cuda_fail(e, "normalize");
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_lu_to_ldu(ebv_context_t c, int64_t n, double* LU, int64_t lda, double* d_D, void* stream) {
+  if (!c) return invalid("ebv_lu_to_ldu: NULL ctx");
+  if (n < 0) return invalid("ebv_lu_to_ldu: negative size");
+  if (lda < (n > 1 ? n : 1)) return invalid("ebv_lu_to_ldu: lda too small");
+  if (n == 0) return EBV_SUCCESS;
+  if (!LU || !d_D) return invalid("ebv_lu_to_ldu: NULL pointer");
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t nl = 0;
+  cudaError_t e = timed(c, KC_OTHER, 0.5 * n * n, 8.0 * n * n, s, 0, [&] { return launch_lu_to_ldu(n, LU, lda, d_D, s, &nl); });
+  c->launches += nl;
+  if (e != cudaSuccess) return cuda_fail(e, "ldu");
   return EBV_SUCCESS;
 }
 

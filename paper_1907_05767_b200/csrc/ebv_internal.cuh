@@ -58,6 +58,12 @@ cudaError_t launch_trsm_left_upper(int64_t k, int64_t m, const double* U, int64_
 cudaError_t launch_solve_window(int64_t n, const double* LUw, int64_t ldl, int64_t c0, int64_t w, bool fwd, double* B,
                                 int64_t ldb, int64_t nrhs, int* ticket, int* flags, int epoch, cudaStream_t s);
 int64_t solve_max_rhs();
+
+// Row scalings (k_scale.cu).  dws: n doubles of workspace.
+cudaError_t launch_normalize_unit_diagonal(int64_t n, double* A, int64_t lda, double* B, int64_t ldb, int64_t nrhs,
+                                           double* scales, int64_t* info, double* dws, unsigned long long* info_min,
+                                           cudaStream_t s, int64_t* launches);
+cudaError_t launch_lu_to_ldu(int64_t n, double* LU, int64_t lda, double* D, cudaStream_t s, int64_t* launches);
 int64_t solve_max_interleave();
 cudaError_t launch_solve(int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb, int64_t nrhs,
                          int* ticket_ws, int* flags_ws, int64_t epoch, cudaStream_t s);

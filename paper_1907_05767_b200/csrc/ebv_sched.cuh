@@ -19,7 +19,9 @@ struct ebv_context {
   unsigned long long* d_norm = nullptr;
   double* d_scratch = nullptr;
   int* d_ticket = nullptr;
-  int* d_pcount = nullptr;  // panel-leaf arrival counter (zero between launches; self-resetting)
+  int* d_pcount = nullptr;
+  double* d_vec = nullptr;  // n-vector workspace (row scalings)
+  int64_t vec_cap = 0;  // panel-leaf arrival counter (zero between launches; self-resetting)
   int* d_flags = nullptr;
   int64_t flags_cap = 0;
   int* d_vflags = nullptr;

@@ -116,3 +116,25 @@ for nr in (1, 16):
     emit(config="C5-solve-only", batch=batch, n=32, nrhs=nr, what="batched solve (pre-factored)", ms=med,
          ms_min=lo, ms_max=hi, gbs=by / med / 1e6, frac_hbm=by / med / 1e6 / HBM,
          systems_per_s=batch / med * 1e3, bytes=by)
+
+# ---------------- f3: unit-diagonal normalization and LDU form at n = 32768 (HBM-bound)
+del A0, B0, Aw, Bw, db
+n = 32768
+d = ebv_inputs.generate(n, seed=1, nrhs=1, device=dev)
+A0 = d["At"]
+Aw = torch.empty_like(A0)
+Bw = d["B"].T.clone(memory_format=torch.contiguous_format)
+scales = torch.empty(n, dtype=torch.float64, device=dev)
+info1 = torch.zeros((), dtype=torch.int64, device=dev)
+med, lo, hi = timeit(lambda: Aw.copy_(A0),
+                     lambda: ebv.ebv_normalize_unit_diagonal(ctx.handle, n, Aw.data_ptr(), n, Bw.data_ptr(), n, 1,
+                                                             scales.data_ptr(), info1.data_ptr(), sh))
+by = 16.0 * n * n + 16.0 * n
+emit(config="f3-normalize", n=n, what="unit-diagonal normalization (A and b)", ms=med, ms_min=lo, ms_max=hi,
+     gbs=by / med / 1e6, frac_hbm=by / med / 1e6 / HBM)
+D = torch.empty(n, dtype=torch.float64, device=dev)
+med, lo, hi = timeit(lambda: Aw.copy_(A0),
+                     lambda: ebv.ebv_lu_to_ldu(ctx.handle, n, Aw.data_ptr(), n, D.data_ptr(), sh))
+by = 16.0 * n * (n - 1) / 2
+emit(config="f3-ldu", n=n, what="LDU form (strict upper / pivot)", ms=med, ms_min=lo, ms_max=hi,
+     gbs=by / med / 1e6, frac_hbm=by / med / 1e6 / HBM)

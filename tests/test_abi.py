@@ -44,6 +44,7 @@ def test_binding_signatures_cover_the_header():
     L = ebv.lib()
     for name in ebv.SIGNATURES:
         assert getattr(L, name) is not None
+        assert callable(getattr(ebv, name, None)), f"no Python binding named {name}"
 
 
 def test_plan_units_match_oracle():
@@ -86,6 +87,8 @@ def test_argument_validation_without_gpu():
     assert L.ebv_block_width(None, 100) == 0
     assert L.ebv_lu_solve_batched(None, 4, None, 4, 16, 1, None, 4, 4, 1, None) == 1
     assert L.ebv_stats_timeline(None, None, 0) == -1
+    assert L.ebv_normalize_unit_diagonal(None, 4, None, 4, None, 4, 1, None, None, None) == 1
+    assert L.ebv_lu_to_ldu(None, 4, None, 4, None, None) == 1
     assert ebv.ebv_status_string(0) == "success"
     assert ebv.ebv_status_string(5) == "not supported"
 

@@ -224,6 +224,47 @@ def test_solve_many_rhs_bitwise(dev, ctx, n, nrhs):
     assert bits_eq(X.cpu().numpy(), oracle.lu_solve(lu_o, d["B"].cpu().numpy()))
 
 
+# ------------------------------------------------------------------ f3: unit diagonal, LDU
+@pytest.mark.parametrize("n,nrhs", [(1, 1), (2, 0), (300, 3), (1537, 1)])
+def test_normalize_unit_diagonal_bitwise(dev, ctx, n, nrhs):
+    d = ebv_inputs.generate(n, seed=n + 5, nrhs=max(nrhs, 1), device=dev)
+    A = d["At"].T
+    B = d["B"] if nrhs else None
+    An, Bn, scales, info = ebv.normalize_unit_diagonal(A, B, ctx=ctx)
+    torch.cuda.synchronize()
+    a_o, b_o, s_o, info_o = oracle.normalize_unit_diagonal(A.cpu().numpy(), B.cpu().numpy() if nrhs else None)
+    assert int(info) == info_o == 0
+    assert bits_eq(An.cpu().numpy(), a_o)
+    assert bits_eq(scales.cpu().numpy(), s_o)
+    if nrhs:
+        assert bits_eq(Bn.cpu().numpy(), b_o)
+    # the normalized system is factored and solved like any other (Eq 2 shape)
+    LU, inf2 = ebv.lu_factor(An, ctx=ctx)
+    torch.cuda.synchronize()
+    assert int(inf2) == 0 and bits_eq(LU.cpu().numpy(), oracle.lu_factor(a_o)[0])
+
+
+def test_normalize_zero_diagonal_reported(dev, ctx):
+    A = torch.eye(5, dtype=torch.float64, device=dev) * 2.0
+    A[3, 3] = 0.0
+    A[4, 4] = 0.0
+    An, _, scales, info = ebv.normalize_unit_diagonal(A, None, ctx=ctx)
+    torch.cuda.synchronize()
+    assert int(info) == 4
+    assert scales[3].item() == 0.0 and An[3, 3].item() == 0.0 and An[0, 0].item() == 1.0
+
+
+@pytest.mark.parametrize("n", [1, 2, 65, 700, 3000])
+def test_lu_to_ldu_bitwise(dev, ctx, n):
+    d = ebv_inputs.generate(n, seed=n + 9, device=dev)
+    LU, _ = ebv.lu_factor(d["At"].T, ctx=ctx)
+    LDU, D = ebv.lu_to_ldu(LU, ctx=ctx)
+    torch.cuda.synchronize()
+    ldu_o, d_o = oracle.lu_to_ldu(LU.cpu().numpy())
+    assert bits_eq(LDU.cpu().numpy(), ldu_o)
+    assert bits_eq(D.cpu().numpy(), d_o)
+
+
 # ------------------------------------------------------------------ vector path (EbV owner map)
 @pytest.mark.parametrize("n,ctas", [(1, 0), (2, 0), (3, 0), (64, 0), (255, 0), (1024, 0), (1024, 128), (1024, -128),
                                     (1000, 100), (1536, 0), (300, -7), (301, 5), (33, 1)])
