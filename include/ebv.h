@@ -78,7 +78,7 @@ typedef struct ebv_context* ebv_context_t;
 typedef enum { EBV_PATH_AUTO = 0, EBV_PATH_VECTOR = 1, EBV_PATH_BLOCKED = 2 } ebv_path_t;
 
 #define EBV_VECTOR_MAX_N 1536
-#define EBV_BATCHED_MAX_N 32
+#define EBV_BATCHED_MAX_N 64
 
 /* Column-block -> rank layouts for a 1D distribution:
  * CYCLIC = J mod P; EBVPAIR = block pairs (J, N-1-J) dealt round-robin

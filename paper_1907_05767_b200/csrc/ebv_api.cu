@@ -544,7 +544,7 @@ ebv_status_t ebv_lu_factor_batched(ebv_context_t c, int64_t n, double* A, int64_
   }
   if (n == 0 || batch == 0) return EBV_SUCCESS;
   if (!A || !d_info) return invalid("ebv_lu_factor_batched: NULL pointer");
-  if (n > EBV_BATCHED_MAX_N) { set_error("batched path supports n <= 32"); return EBV_ERR_NOT_SUPPORTED; }
+  if (n > EBV_BATCHED_MAX_N) { set_error("batched path supports n <= 64"); return EBV_ERR_NOT_SUPPORTED; }
   if (nrhs > 16) { set_error("batched path supports nrhs <= 16"); return EBV_ERR_NOT_SUPPORTED; }
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
@@ -569,7 +569,7 @@ ebv_status_t ebv_lu_solve_batched(ebv_context_t c, int64_t n, const double* LU, 
   if (batch > 1 && strideB < ldb * nrhs) return invalid("ebv_lu_solve_batched: strideB < ldb*nrhs");
   if (n == 0 || batch == 0 || nrhs == 0) return EBV_SUCCESS;
   if (!LU || !B) return invalid("ebv_lu_solve_batched: NULL pointer");
-  if (n > EBV_BATCHED_MAX_N) { set_error("batched path supports n <= 32"); return EBV_ERR_NOT_SUPPORTED; }
+  if (n > EBV_BATCHED_MAX_N) { set_error("batched path supports n <= 64"); return EBV_ERR_NOT_SUPPORTED; }
   if (nrhs > 16) { set_error("batched path supports nrhs <= 16"); return EBV_ERR_NOT_SUPPORTED; }
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;

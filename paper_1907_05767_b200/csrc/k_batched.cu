@@ -188,13 +188,121 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
   }
 }
 
+// ---------------------------------------------------------------- 33 <= n <= 64
+// SURVEY §8f f2 (batched medium systems, CTA per system).  One CTA of 128
+// threads per system: row i is owned by the lane pair (2i, 2i+1), lane j of
+// the pair holding the columns c = j + 2q.  Step k: the pair owning row k
+// publishes its final row (the U_(k) vector, Eq 6-b) to shared memory; every
+// row i > k forms l_ik = a_ik / u_kk in the lane holding column k (Eq 6-a),
+// shuffles it to its partner and both update their columns (Eq 6-c).  The
+// solve (Eq 1) keeps y_i in both lanes of the pair (identical arithmetic),
+// y_k / x_k published through shared memory.  Padding to 64 with identity
+// rows / columns is exactly neutral.  Per entry the oracle's operations.
+constexpr int N64 = 64, QB = N64 / 2;
+
+__global__ void __launch_bounds__(128, 3) batched64_kernel(int n, double* __restrict__ A, int64_t lda, int64_t strideA,
+                                                        int64_t batch, double* __restrict__ B, int64_t ldb,
+                                                        int64_t strideB, int nrhs, int tau_default, double tau_value,
+                                                        int32_t* __restrict__ info, int solve_only) {
+  __shared__ double urow[2][N64];
+  __shared__ double sval[2];
+  __shared__ double snorm[4];
+  const int64_t sys = blockIdx.x;
+  if (sys >= batch) return;
+  const int tid = threadIdx.x, i = tid >> 1, j = tid & 1, lane = tid & 31;
+  const int pair = lane & ~1;
+  double* As = A + sys * strideA;
+  const bool rv = i < n;
+  double a[QB];
+#pragma unroll
+  for (int q = 0; q < QB; q++) {
+    const int c = j + 2 * q;
+    a[q] = (rv && c < n) ? As[i + (int64_t)c * lda] : (i == c ? 1.0 : 0.0);
+  }
+  if (!solve_only) {
+    double tv = tau_value;
+    if (tau_default) {   // n * eps * ||A_s||_inf
+      double rs = 0.0;
+#pragma unroll
+      for (int q = 0; q < QB; q++)
+        if (j + 2 * q < n) rs += fabs(a[q]);
+      rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+      double m = rv ? rs : 0.0;
+#pragma unroll
+      for (int o = 16; o >= 2; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) snorm[tid >> 5] = m;
+      __syncthreads();
+      m = fmax(fmax(snorm[0], snorm[1]), fmax(snorm[2], snorm[3]));
+      tv = (double)n * 2.220446049250313e-16 * m;
+    }
+    int inf = 0;
+#pragma unroll
+    for (int k = 0; k < N64; k++) {
+      double* ur = urow[k & 1];
+      if (i == k) {
+#pragma unroll
+        for (int q = 0; q < QB; q++)
+          if (j + 2 * q >= k) ur[j + 2 * q] = a[q];
+      }
+      __syncthreads();
+      const double piv = ur[k];
+      if (k < n && inf == 0 && fabs(piv) <= tv) inf = k + 1;
+      const int qk = k >> 1;
+      if (i > k && j == (k & 1)) a[qk] = a[qk] / piv;                       // Eq 6-a
+      const double l = __shfl_sync(0xffffffffu, a[qk], pair | (k & 1));
+      if (i > k) {
+#pragma unroll
+        for (int q = qk; q < QB; q++)
+          if (j + 2 * q > k) a[q] = fma(-l, ur[j + 2 * q], a[q]);             // Eq 6-c
+      }
+    }
+    if (tid == 0 && info) info[sys] = inf;
+  }
+  if (B) {
+    double* Bs = B + sys * strideB;
+    for (int r = 0; r < nrhs; r++) {
+      double y = rv ? Bs[i + (int64_t)r * ldb] : 0.0;
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < N64; k++) {            // forward: LY = B
+        if (tid == 2 * k) sval[k & 1] = y;
+        __syncthreads();
+        const double yk = sval[k & 1];
+        const double l = __shfl_sync(0xffffffffu, a[k >> 1], pair | (k & 1));
+        if (i > k) y = fma(-l, yk, y);
+      }
+#pragma unroll
+      for (int k = N64 - 1; k >= 0; k--) {       // backward: UX = Y
+        const double u = __shfl_sync(0xffffffffu, a[k >> 1], pair | (k & 1));
+        if (i == k) y = y / u;
+        if (tid == 2 * k) sval[k & 1] = y;
+        __syncthreads();
+        const double xk = sval[k & 1];
+        if (i < k) y = fma(-u, xk, y);
+      }
+      if (rv && j == 0) Bs[i + (int64_t)r * ldb] = y;
+    }
+  }
+  if (solve_only) return;
+#pragma unroll
+  for (int q = 0; q < QB; q++) {
+    const int c = j + 2 * q;
+    if (rv && c < n) As[i + (int64_t)c * lda] = a[q];
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_batched(int64_t n, double* A, int64_t lda, int64_t strideA, int64_t batch, double* B,
                            int64_t ldb, int64_t strideB, int64_t nrhs, const double* tau, bool tau_default,
                            double tau_value, int32_t* info, cudaStream_t s, bool solve_only) {
   if (batch <= 0 || n <= 0) return cudaSuccess;
-  if (n > NP || nrhs > MAXRHS) return cudaErrorInvalidValue;
+  if (n > N64 || nrhs > MAXRHS) return cudaErrorInvalidValue;
+  if (n > NP) {
+    batched64_kernel<<<(unsigned)batch, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, ldb, strideB, (int)nrhs,
+                                                     tau_default ? 1 : 0, tau_value, info, solve_only ? 1 : 0);
+    return cudaGetLastError();
+  }
   const int64_t warps = (batch + 1) / 2;
   const int64_t blocks = (warps * 32 + 127) / 128;
   const int so = solve_only ? 1 : 0, td = tau_default ? 1 : 0;

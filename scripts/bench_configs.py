@@ -117,6 +117,26 @@ for nr in (1, 16):
          ms_min=lo, ms_max=hi, gbs=by / med / 1e6, frac_hbm=by / med / 1e6 / HBM,
          systems_per_s=batch / med * 1e3, bytes=by)
 
+# ---------------- f2: batched medium systems (n = 64, CTA per system)
+db = ebv_inputs.generate_batched(batch, 64, seed=1, nrhs=1, device=dev)
+A64 = db["At"]
+B64 = db["B"].transpose(1, 2).clone(memory_format=torch.contiguous_format)
+Aw64, Bw64 = torch.empty_like(A64), torch.empty_like(B64)
+
+
+def prep64():
+    Aw64.copy_(A64)
+    Bw64.copy_(B64)
+
+
+med, lo, hi = timeit(prep64, lambda: ebv.ebv_lu_factor_batched(ctx.handle, 64, Aw64.data_ptr(), 64, 64 * 64, batch,
+                                                                Bw64.data_ptr(), 64, 64, 1, 0.0, binfo.data_ptr(), sh))
+by = batch * (2 * 64 * 64 * 8 + 2 * 64 * 8 + 4)
+emit(config="f2-batched64", batch=batch, n=64, what="batched factor+solve", ms=med, ms_min=lo, ms_max=hi,
+     gbs=by / med / 1e6, frac_hbm=by / med / 1e6 / HBM, systems_per_s=batch / med * 1e3,
+     max_err=(Bw64.transpose(1, 2) - db["X"]).abs().max().item(), bytes=by)
+del db, A64, B64, Aw64, Bw64
+
 # ---------------- f3: unit-diagonal normalization and LDU form at n = 32768 (HBM-bound)
 del A0, B0, Aw, Bw, db
 n = 32768

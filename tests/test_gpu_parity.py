@@ -171,7 +171,7 @@ def test_argument_errors(dev, ctx):
     assert L.ebv_lu_factor(ctx.handle, 4, None, 4, 0.0, info.data_ptr(), None) == 1
     assert L.ebv_lu_factor(ctx.handle, 0, None, 1, 0.0, info.data_ptr(), None) == 0
     assert L.ebv_lu_solve(ctx.handle, 4, A.data_ptr(), 4, None, 4, 1, None) == 1
-    assert L.ebv_lu_factor_batched(ctx.handle, 33, A.data_ptr(), 33, 33 * 33, 1, None, 33, 0, 0, 0.0,
+    assert L.ebv_lu_factor_batched(ctx.handle, 65, A.data_ptr(), 65, 65 * 65, 1, None, 65, 0, 0, 0.0,
                                    info.data_ptr(), None) == 5
     torch.cuda.synchronize()
 
@@ -279,7 +279,8 @@ def test_vector_path_bitwise(dev, ctx, n, ctas):
 
 # ------------------------------------------------------------------ batched
 @pytest.mark.parametrize("n,batch,nrhs", [(32, 1000, 1), (32, 1, 1), (32, 7, 2), (1, 5, 1), (7, 33, 3),
-                                          (31, 64, 16), (32, 257, 0)])
+                                          (31, 64, 16), (32, 257, 0), (33, 50, 1), (48, 31, 3), (64, 200, 1),
+                                          (64, 3, 16), (64, 9, 0)])
 def test_batched_bitwise(dev, ctx, n, batch, nrhs):
     db = ebv_inputs.generate_batched(batch, n, seed=n + batch, nrhs=max(nrhs, 1), device=dev)
     At = db["At"].clone()
@@ -297,7 +298,8 @@ def test_batched_bitwise(dev, ctx, n, batch, nrhs):
         assert bits_eq(Bt.transpose(1, 2).cpu().numpy(), x_o)
 
 
-@pytest.mark.parametrize("n,batch,nrhs", [(32, 1000, 1), (32, 333, 16), (7, 65, 3), (1, 4, 2), (31, 2, 5)])
+@pytest.mark.parametrize("n,batch,nrhs", [(32, 1000, 1), (32, 333, 16), (7, 65, 3), (1, 4, 2), (31, 2, 5),
+                                          (64, 100, 2), (40, 7, 1)])
 def test_batched_solve_only_bitwise(dev, ctx, n, batch, nrhs):
     """Factor once, solve many: ebv_lu_solve_batched on the
     factors of ebv_lu_factor_batched equals the oracle's solve of every
