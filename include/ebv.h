@@ -111,8 +111,8 @@ ebv_status_t ebv_set_leaf(ebv_context_t ctx, int64_t leaf);
 
 /* Blocked path schedule: nb > 0 = right-looking with column blocks of nb
  * (a multiple of the leaf) — panel LU, U12 substitution, DMMA trailing
- * update per block; nb = 0 (default) = size-adaptive (128 below n = 12288,
- * 256 below 24576, else 512: the best measured on B200); nb = -1 = fully
+ * update per block; nb = 0 (default) = size-adaptive (64 below n = 6144, 128
+ * below 12288, 256 below 24576, else 512: the best measured on B200); nb = -1 = fully
  * recursive 2 x 2 splitting.  All are bitwise identical. */
 ebv_status_t ebv_set_block(ebv_context_t ctx, int64_t nb);
 

@@ -196,10 +196,11 @@ cudaError_t panel_rec(ebv_context* c, int64_t M, int64_t w, double* P, int64_t l
 // This is also the per-step structure of the 1D block-cyclic multi-GPU
 // schedule (only the owner of block K factors the panel).
 // Block width: the caller's choice, else size-adaptive (measured on B200:
-// 128 at n = 8192, 512 at n = 32768; profiles/r01_sweep_nb.jsonl).
+// 64 up to n = 4096, 128 at 8192, 256 at 16384, 512 at 32768;
+// profiles/r01_sweep_nb*.jsonl).
 int64_t block_width(const ebv_context* c, int64_t n) {
   if (c->nb > 0) return c->nb;
-  int64_t nb = n >= 24576 ? 512 : (n >= 12288 ? 256 : 128);
+  int64_t nb = n >= 24576 ? 512 : (n >= 12288 ? 256 : (n >= 6144 ? 128 : 64));
   return ((nb + c->leaf - 1) / c->leaf) * c->leaf;
 }
 

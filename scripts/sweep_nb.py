@@ -15,7 +15,10 @@ for n in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "8192,32768").s
     A0 = d["At"]
     Aw = torch.empty_like(A0)
     del d
-    for nb, la in (((0, 1), (128, 1), (256, 1), (512, 1), (-1, 0)) if len(sys.argv) < 3 else ((0, 1),)):
+    nbs = ((0, 1), (128, 1), (256, 1), (512, 1), (-1, 0))
+    if len(sys.argv) >= 3:
+        nbs = tuple((int(x), 1) for x in sys.argv[2].split(","))
+    for nb, la in nbs:
         ctx.set_block(nb)
         ctx.set_lookahead(bool(la))
         ts = []

@@ -203,7 +203,8 @@ def test_solve_vector_rhs_and_backward_error(dev, ctx):
 
 def test_block_width_query(dev):
     c = ebv.Context(0)
-    assert c.block_width(8192) == 128 and c.block_width(16384) == 256 and c.block_width(32768) == 512
+    assert c.block_width(1024) == 64 and c.block_width(8192) == 128
+    assert c.block_width(16384) == 256 and c.block_width(32768) == 512
     c.set_block(192)
     assert c.block_width(32768) == 192
     c.set_block(-1)
