@@ -251,12 +251,14 @@ def run_ebv(args, rank, world, local):
     Aw = torch.empty_like(A0)
     Bw = torch.empty_like(B0)
 
-    def factor_solve():
+    def factor_solve(Ab=None, Bb=None):
+        Ab = Aw if Ab is None else Ab
+        Bb = Bw if Bb is None else Bb
         if use_dist:
-            s = ebv.ebv_lu_factor_dist(ctx.handle, n, Aw.data_ptr(), n, 0.0, info.data_ptr(), sh)
-            return s, lambda: ebv.ebv_lu_solve_dist(ctx.handle, n, Aw.data_ptr(), n, Bw.data_ptr(), n, nrhs, sh)
-        s = ebv.ebv_lu_factor(ctx.handle, n, Aw.data_ptr(), n, 0.0, info.data_ptr(), sh)
-        return s, lambda: ebv.ebv_lu_solve(ctx.handle, n, Aw.data_ptr(), n, Bw.data_ptr(), n, nrhs, sh)
+            s = ebv.ebv_lu_factor_dist(ctx.handle, n, Ab.data_ptr(), n, 0.0, info.data_ptr(), sh)
+            return s, lambda: ebv.ebv_lu_solve_dist(ctx.handle, n, Ab.data_ptr(), n, Bb.data_ptr(), n, nrhs, sh)
+        s = ebv.ebv_lu_factor(ctx.handle, n, Ab.data_ptr(), n, 0.0, info.data_ptr(), sh)
+        return s, lambda: ebv.ebv_lu_solve(ctx.handle, n, Ab.data_ptr(), n, Bb.data_ptr(), n, nrhs, sh)
 
     def step(ev=None):
         Aw.copy_(A0)
@@ -336,24 +338,49 @@ def run_ebv(args, rank, world, local):
         hB.copy_(B0)
         torch.cuda.synchronize()
 
-        def e2e_step():
-            Aw.copy_(hA, non_blocking=True)
-            Bw.copy_(hB, non_blocking=True)
-            s, solve = factor_solve()
-            s |= solve()
-            hX.copy_(Bw, non_blocking=True)
-            if s:
-                raise RuntimeError(ebv.ebv_last_error())
+        # Steps are pipelined the way a serving loop would run them: step i+1's
+        # inputs are copied from pinned host memory on a copy stream while
+        # step i factors (two device buffers, events order their reuse); every
+        # step's full H2D copy and its x readback are inside the timed region.
+        Aw2, Bw2 = torch.empty_like(Aw), torch.empty_like(Bw)
+        bufs = [(Aw, Bw), (Aw2, Bw2)]
+        cs = torch.cuda.Stream(dev)
+        ev_in = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_done = [torch.cuda.Event(), torch.cuda.Event()]
 
-        e2e_step()
+        def e2e_run(ksteps):
+            with torch.cuda.stream(cs):
+                bufs[0][0].copy_(hA, non_blocking=True)
+                bufs[0][1].copy_(hB, non_blocking=True)
+                ev_in[0].record(cs)
+            for i in range(ksteps):
+                Ab, Bb = bufs[i % 2]
+                if i + 1 < ksteps:
+                    An, Bn = bufs[(i + 1) % 2]
+                    with torch.cuda.stream(cs):
+                        if i >= 1:
+                            cs.wait_event(ev_done[(i + 1) % 2])
+                        An.copy_(hA, non_blocking=True)
+                        Bn.copy_(hB, non_blocking=True)
+                        ev_in[(i + 1) % 2].record(cs)
+                stream.wait_event(ev_in[i % 2])
+                s, solve = factor_solve(Ab, Bb)
+                s |= solve()
+                hX.copy_(Bb, non_blocking=True)
+                ev_done[i % 2].record(stream)
+                if s:
+                    raise RuntimeError(ebv.ebv_last_error())
+
+        e2e_run(2)
         torch.cuda.synchronize()
-        ksteps = max(1, min(args.steps, 3))
+        ksteps = max(3, args.steps)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if world > 1:
             dist.barrier()
+        torch.cuda.synchronize()
         e0.record(stream)
-        for _ in range(ksteps):
-            e2e_step()
+        cs.wait_event(e0)
+        e2e_run(ksteps)
         e1.record(stream)
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
@@ -364,8 +391,9 @@ def run_ebv(args, rank, world, local):
         e2e_ok = (hX.T - Xtrue.cpu()).abs().max().item() <= 1e-10
         e2e = {"value": fl * ksteps / (ems / 1e3) / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": int(hA.numel() * 8 + hB.numel() * 8), "d2h_bytes_per_step": int(hX.numel() * 8),
-               "ms_per_step": ems / ksteps, "steps": ksteps, "correct": bool(e2e_ok)}
-        del hA, hB, hX
+               "ms_per_step": ems / ksteps, "steps": ksteps, "correct": bool(e2e_ok),
+               "pipelined": "next step's H2D on a copy stream under the current step's factor"}
+        del hA, hB, hX, Aw2, Bw2
 
     out = None
     if rank == 0:
