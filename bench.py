@@ -12,6 +12,10 @@ value = nominal factor flops (2/3 n^3) per step * steps / timed seconds, in
 GFLOP/s — the "LU factor GFLOP/s" of the metric, charged with the solve and
 the restore copy; factor_ms / solve_ms are reported beside it ("solve ms").
 
+e2e: the same step through the C ABI from pinned host memory (H2D copy of A
+and b and the readback of x inside the timed region every step), pipelined:
+step i+1's copy runs on a copy stream under step i's factorization.
+
 --impl reference runs the serial CPU oracle (oracle/, the test
 infrastructure) on a bounded sample of the same workload: the leading
 m x m principal submatrix of the same n = 32768 matrix (bit-identical
