@@ -155,6 +155,11 @@ static bool solve_use_trsm(int64_t n, int64_t nrhs) {
   return nrhs > 128 || (n > 8192 && nrhs > 64) || (n > 16384 && nrhs > 40);
 }
 
+static int64_t kU12SplitRows = [] {
+  const char* e = getenv("EBV_U12_SPLIT_ROWS");
+  return e ? (int64_t)atoll(e) : (int64_t)-1;   // -1: split for n >= 16384 (same-box A/B:
+}();                                              // n = 32768 -0.3%, n = 8192 +3% if split)
+
 static int64_t kTailRows = [] {
   const char* e = getenv("EBV_TAIL_ROWS");
   return e ? (int64_t)atoll(e) : (int64_t)0;
@@ -242,22 +247,27 @@ cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_
       e = cudaStreamWaitEvent(s, c->ev_p, 0);
       if (e != cudaSuccess) return e;
     }
-    e = trsm_l(c, w, rest, P, lda, P + w * lda, lda, s);
-    if (e != cudaSuccess) return e;
     const int64_t w1 = step_width(c, n, c0 + w);     // width of panel K+1
     double* P1 = P + w + w * lda;
     if (la && rest > w1) {
-      // lookahead: update panel K+1's columns first, factor it on the side
-      // stream while the rest of the trailing matrix is updated
-      e = gemm(c, rest, w1, w, P + w, lda, P + w * lda, lda, P1, lda, false, s);
+      // lookahead: the update of panel K+1's columns first, then factor it on
+      // the side stream while the rest of the trailing matrix is updated.
+      // For large n U12 is split too, so panel K+1 need not wait for all of
+      // U12 (columns are independent: same bits).
+      const bool split = kU12SplitRows >= 0 ? rest < kU12SplitRows : n >= 16384;
+      e = trsm_l(c, w, split ? w1 : rest, P, lda, P + w * lda, lda, s);
+      if (e == cudaSuccess) e = gemm(c, rest, w1, w, P + w, lda, P + w * lda, lda, P1, lda, false, s);
       if (e == cudaSuccess) e = cudaEventRecord(c->ev_a, s);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_a, 0);
       if (e == cudaSuccess) e = panel_rec(c, rest, w1, P1, lda, c0 + w, info, c->side);
       if (e == cudaSuccess) e = cudaEventRecord(c->ev_p, c->side);
+      if (e == cudaSuccess && split) e = trsm_l(c, w, rest - w1, P, lda, P + (w + w1) * lda, lda, s);
       if (e == cudaSuccess)
         e = gemm(c, rest, rest - w1, w, P + w, lda, P + (w + w1) * lda, lda, P1 + w1 * lda, lda, false, s);
       if (e != cudaSuccess) return e;
     } else {
+      e = trsm_l(c, w, rest, P, lda, P + w * lda, lda, s);
+      if (e != cudaSuccess) return e;
       e = gemm(c, rest, rest, w, P + w, lda, P + w * lda, lda, P1, lda, false, s);
       if (e != cudaSuccess) return e;
       if (la) {   // keep the event protocol: the next panel is factored in order
