@@ -64,18 +64,25 @@ typedef struct ebv_context* ebv_context_t;
 
 /* Which factorization path ebv_lu_factor takes.
  *   EBV_PATH_VECTOR  — the paper's vector-level elimination (Eq 6 step by
- *                      step) as one persistent kernel: each CTA owns
- *                      EbV-paired columns (j, n-1-j) (Eq 7) resident
- *                      in shared memory; per step the owner of column k
- *                      publishes L_(k) and every CTA applies the rank-1 update
- *                      to its columns.  n <= EBV_VECTOR_MAX_N.
- *   EBV_PATH_BLOCKED — recursive blocked form of the same recurrences: the
- *                      trailing rank-k updates run as FP64 tensor-core (DMMA)
- *                      contractions, triangular blocks by row/column-parallel
- *                      substitution.  Any n.
- *   EBV_PATH_AUTO    — the blocked path (the faster one at every n measured;
- *                      DESIGN.md §Paths).                                    */
-typedef enum { EBV_PATH_AUTO = 0, EBV_PATH_VECTOR = 1, EBV_PATH_BLOCKED = 2 } ebv_path_t;
+ *                      step) as one persistent kernel: blocks of up
+ *                      to 8 consecutive columns, EbV-paired blocks (J, Nb-1-J)
+ *                      (Eq 7) dealt to CTAs and resident in shared
+ *                      memory; the owner of block J factors it and releases
+ *                      one flag, every CTA applies its L_(k) vectors to its
+ *                      later columns.  n <= EBV_VECTOR_MAX_N.
+ *   EBV_PATH_BLOCKED — right-looking blocked form of the same recurrences:
+ *                      the trailing rank-nb updates run as FP64 tensor-core
+ *                      (DMMA) contractions, triangular blocks by row/column-
+ *                      parallel substitution, lookahead on a side stream.
+ *   EBV_PATH_LEFT    — left-looking blocked form (block J takes all earlier
+ *                      panels' updates — a trsm with L[0:c, 0:c] and one DMMA
+ *                      contraction — before its own panel); it can stream a
+ *                      host-resident matrix (ebv_lu_factor_host) but its
+ *                      per-block triangular solves are launch-heavy: slower
+ *                      than EBV_PATH_BLOCKED at every n measured.
+ *   EBV_PATH_AUTO    — the blocked (right-looking) path.
+ * All paths give bitwise the same factors.                                   */
+typedef enum { EBV_PATH_AUTO = 0, EBV_PATH_VECTOR = 1, EBV_PATH_BLOCKED = 2, EBV_PATH_LEFT = 3 } ebv_path_t;
 
 #define EBV_VECTOR_MAX_N 1536
 #define EBV_BATCHED_MAX_N 64
@@ -153,6 +160,18 @@ ebv_status_t ebv_set_vector_ctas(ebv_context_t ctx, int64_t ctas);
  * n > EBV_VECTOR_MAX_N. */
 ebv_status_t ebv_lu_factor(ebv_context_t ctx, int64_t n, double* A, int64_t lda, double tau,
                            int64_t* d_info, void* stream);
+
+/* A = LU from a HOST-resident matrix: hA (host, column-major, ldh >= n;
+ * page-locked memory for full copy speed) is copied to A (device, lda >= n)
+ * on `stream` and factored there; A holds the packed LU (bitwise
+ * ebv_lu_factor's).  With EBV_PATH_LEFT (and tau >= 0) the column blocks
+ * stream in on an internal copy stream under the left-looking factorization
+ * instead — every transfer but the first block's hidden, but that schedule
+ * is slower on B200 (n = 32768: 1.21 s vs 0.88 s for copy + right-looking;
+ * DESIGN.md), so the default copies first.  Errors as ebv_lu_factor, plus
+ * INVALID_VALUE for ldh < n or hA NULL. */
+ebv_status_t ebv_lu_factor_host(ebv_context_t ctx, int64_t n, const double* hA, int64_t ldh, double* A,
+                                int64_t lda, double tau, int64_t* d_info, void* stream);
 
 /* X from LY = B then UX = Y (Eq 1; "UX = B" read as UX = Y, R6).
  *   LU     device, the packed output of ebv_lu_factor (column-major, lda)

@@ -26,7 +26,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libebv.so")
 
 EBV_SUCCESS = 0
-EBV_PATH_AUTO, EBV_PATH_VECTOR, EBV_PATH_BLOCKED = 0, 1, 2
+EBV_PATH_AUTO, EBV_PATH_VECTOR, EBV_PATH_BLOCKED, EBV_PATH_LEFT = 0, 1, 2, 3
 EBV_LAYOUT_CYCLIC, EBV_LAYOUT_EBVPAIR, EBV_LAYOUT_SNAKE = 0, 1, 2
 KCLASSES = ["gemm_dmma", "leaf_lu", "trsm", "solve", "batched", "vector", "other"]
 
@@ -42,6 +42,7 @@ SIGNATURES = {
     "ebv_set_vector_ctas": (_int, [_vp, _i64]),
     "ebv_set_block": (_int, [_vp, _i64]),
     "ebv_block_width": (_i64, [_vp, _i64]),
+    "ebv_lu_factor_host": (_int, [_vp, _i64, _vp, _i64, _vp, _i64, _d, _vp, _vp]),
     "ebv_stats_timeline": (_i64, [_vp, _vp, _i64]),
     "ebv_set_lookahead": (_int, [_vp, _int]),
     "ebv_set_graphs": (_int, [_vp, _int]),
@@ -159,6 +160,10 @@ def ebv_lu_factor_batched(ctx, n, A, lda, strideA, batch, B, ldb, strideB, nrhs,
 
 def ebv_lu_solve_batched(ctx, n, LU, lda, strideA, batch, B, ldb, strideB, nrhs, stream):
     return lib().ebv_lu_solve_batched(ctx, n, LU, lda, strideA, batch, B, ldb, strideB, nrhs, stream)
+
+
+def ebv_lu_factor_host(ctx, n, hA, ldh, A, lda, tau, d_info, stream):
+    return lib().ebv_lu_factor_host(ctx, n, hA, ldh, A, lda, tau, d_info, stream)
 
 
 def ebv_normalize_unit_diagonal(ctx, n, A, lda, B, ldb, nrhs, d_scales, d_info, stream):
@@ -474,6 +479,27 @@ def lu_factor_batched(At: torch.Tensor, Bt: torch.Tensor | None = None, tau: flo
     _check(ebv_lu_factor_batched(ctx.handle, n, At.data_ptr(), max(n, 1), n * n, batch, bptr, ldb, sb, nrhs,
                                  float(tau), info.data_ptr(), _stream_handle(At.device)), "ebv_lu_factor_batched")
     return info
+
+
+def lu_factor_host(hA: torch.Tensor, tau: float = 0.0, ctx: Context | None = None, device: int = 0,
+                   out: torch.Tensor | None = None):
+    """A = LU of a host-resident matrix (ebv_lu_factor_host): hA (n, n) CPU
+    float64 in logical indexing, column-major storage (hA.mT contiguous;
+    pinned memory lets the block copies overlap the factorization).  Returns
+    (LU, info) on cuda:device (LU column-major; `out` may supply it)."""
+    if hA.device.type != "cpu" or hA.dtype != torch.float64 or hA.dim() != 2:
+        raise EbvError("hA must be a 2-D float64 CPU tensor")
+    n = hA.shape[0]
+    ldh = _colmajor_ld(hA)
+    if ldh < 0:
+        raise EbvError("hA must be column-major (hA.mT contiguous)")
+    ctx = ctx or default_context(device)
+    dev = torch.device("cuda", ctx.device)
+    LU = out if out is not None else torch.empty(n, n, dtype=torch.float64, device=dev).mT
+    info = torch.zeros((), dtype=torch.int64, device=dev)
+    _check(ebv_lu_factor_host(ctx.handle, n, hA.data_ptr(), max(ldh, 1), LU.data_ptr(), max(_colmajor_ld(LU), 1),
+                              float(tau), info.data_ptr(), _stream_handle(dev)), "ebv_lu_factor_host")
+    return LU, info
 
 
 def normalize_unit_diagonal(A: torch.Tensor, B: torch.Tensor | None = None, ctx: Context | None = None):

@@ -286,6 +286,76 @@ cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_
   return e;
 }
 
+// Left-looking schedule (EBV_PATH_LEFT, and ebv_lu_factor_host): column
+// block J receives all earlier panels' updates when its turn comes —
+//     X[0:c]   = L[0:c, 0:c]^-1 X[0:c]      (U rows of block J, trsm)
+//     X[c:n]  -= L[c:n, 0:c] X[0:c]         (one DMMA update, K = c)
+// then its panel is factored.  Per entry the same fma chain over ascending k
+// and the same division as the right-looking schedule (bitwise the oracle).
+// Lookahead: block J's update by panels 0..J-2 runs on the caller's stream
+// while panel J-1 is factored on the side stream; only the update by panel
+// J-1 (a w x w trsm and a K = nb update) waits for it.  With hA != NULL the
+// column blocks are copied from host memory on a copy stream, block J+1's
+// copy overlapping block J's work: the factorization of a host-resident
+// matrix hides all but the first block's transfer.
+cudaError_t lu_left(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s,
+                    const double* hA, int64_t ldh) {
+  const int64_t nb = block_width(c, n);
+  const int64_t N = (n + nb - 1) / nb;
+  cudaError_t e = cudaSuccess;
+  if (hA) {
+    if (!c->copy) {
+      e = cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return e;
+    }
+    while ((int64_t)c->copy_ev.size() < N) {
+      cudaEvent_t ev = nullptr;
+      e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+      c->copy_ev.push_back(ev);
+    }
+    // the copies start after the caller's earlier work on A
+    e = cudaEventRecord(c->ev_start, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->copy, c->ev_start, 0);
+    for (int64_t J = 0; J < N && e == cudaSuccess; J++) {
+      const int64_t c0 = J * nb, w = (n - c0) < nb ? (n - c0) : nb;
+      e = cudaMemcpy2DAsync(A + c0 * lda, lda * sizeof(double), hA + c0 * ldh, ldh * sizeof(double),
+                            n * sizeof(double), w, cudaMemcpyHostToDevice, c->copy);
+      if (e == cudaSuccess) e = cudaEventRecord(c->copy_ev[J], c->copy);
+    }
+    if (e != cudaSuccess) return e;
+  }
+  e = cudaEventRecord(c->ev_start, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_start, 0);
+  if (e != cudaSuccess) return e;
+  for (int64_t J = 0; J < N; J++) {
+    const int64_t c0 = J * nb, w = (n - c0) < nb ? (n - c0) : nb;
+    double* X = A + c0 * lda;
+    if (hA) {
+      e = cudaStreamWaitEvent(s, c->copy_ev[J], 0);
+      if (e != cudaSuccess) return e;
+    }
+    if (J >= 1) {
+      const int64_t cp = c0 - nb;                       // panel J-1 = columns [cp, c0)
+      if (cp > 0) {                                     // panels 0..J-2
+        e = trsm_l(c, cp, w, A, lda, X, lda, s);
+        if (e == cudaSuccess) e = gemm(c, n - cp, w, cp, A + cp, lda, X, lda, X + cp, lda, false, s);
+        if (e != cudaSuccess) return e;
+      }
+      e = cudaStreamWaitEvent(s, c->ev_p, 0);          // panel J-1 factored (side stream)
+      if (e == cudaSuccess) e = trsm_l(c, nb, w, A + cp + cp * lda, lda, X + cp, lda, s);
+      if (e == cudaSuccess) e = gemm(c, n - c0, w, nb, A + c0 + cp * lda, lda, X + cp, lda, X + c0, lda, false, s);
+      if (e != cudaSuccess) return e;
+    }
+    e = cudaEventRecord(c->ev_a, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_a, 0);
+    if (e == cudaSuccess) e = panel_rec(c, n - c0, w, A + c0 + c0 * lda, lda, c0, info, c->side);
+    if (e == cudaSuccess) e = cudaEventRecord(c->ev_p, c->side);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaStreamWaitEvent(s, c->ev_p, 0);           // the caller's stream sees the last panel
+}
+
 }  // namespace sched
 }  // namespace ebv
 
@@ -381,6 +451,8 @@ ebv_status_t ebv_destroy(ebv_context_t c) {
   if (c->d_vflags) cudaFree(c->d_vflags);
   cudaFree(c->d_tau);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->copy) cudaStreamDestroy(c->copy);
+  for (auto ev : c->copy_ev) cudaEventDestroy(ev);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_p) cudaEventDestroy(c->ev_p);
@@ -390,7 +462,8 @@ ebv_status_t ebv_destroy(ebv_context_t c) {
 
 ebv_status_t ebv_set_path(ebv_context_t c, ebv_path_t path) {
   if (!c) return invalid("ebv_set_path: NULL ctx");
-  if (path != EBV_PATH_AUTO && path != EBV_PATH_VECTOR && path != EBV_PATH_BLOCKED) return invalid("bad path");
+  if (path != EBV_PATH_AUTO && path != EBV_PATH_VECTOR && path != EBV_PATH_BLOCKED && path != EBV_PATH_LEFT)
+    return invalid("bad path");
   c->path = path;
   return EBV_SUCCESS;
 }
@@ -449,7 +522,7 @@ ebv_status_t ebv_lu_factor(ebv_context_t c, int64_t n, double* A, int64_t lda, d
   // arguments captures it, later calls replay one graph (the schedule is
   // static; replay removes per-launch CPU cost and inter-kernel gaps).
   ebv_context::GraphEntry* ge = nullptr;
-  const bool use_graph = c->graphs && !c->stats && s != nullptr && n > c->leaf && c->path != EBV_PATH_VECTOR &&
+  const bool use_graph = c->graphs && !c->stats && s != nullptr && n > c->leaf && (c->path == EBV_PATH_AUTO || c->path == EBV_PATH_BLOCKED) &&
                          c->nb != -1;
   if (use_graph) {
     for (auto& en : c->gcache)
@@ -522,9 +595,40 @@ static ebv_status_t factor_body(ebv_context_t c, int64_t n, double* A, int64_t l
     if (e != cudaSuccess) return cuda_fail(e, "vector path");
     return EBV_SUCCESS;
   }
+  if (c->path == EBV_PATH_LEFT) {
+    e = lu_left(c, n, A, lda, d_info, s, nullptr, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "left-looking factor");
+    return EBV_SUCCESS;
+  }
   e = (c->nb != -1) ? lu_blocked(c, n, A, lda, d_info, s) : lu_rec(c, n, A, lda, 0, d_info, s);
   if (e != cudaSuccess) return cuda_fail(e, "blocked factor");
   return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_lu_factor_host(ebv_context_t c, int64_t n, const double* hA, int64_t ldh, double* A, int64_t lda,
+                                double tau, int64_t* d_info, void* stream) {
+  if (!c) return invalid("ebv_lu_factor_host: NULL ctx");
+  if (n < 0) return invalid("ebv_lu_factor_host: n < 0");
+  if (lda < (n > 1 ? n : 1) || ldh < (n > 1 ? n : 1)) return invalid("ebv_lu_factor_host: leading dimension < n");
+  if (!d_info) return invalid("ebv_lu_factor_host: d_info is NULL");
+  if (n > 0 && (!A || !hA)) return invalid("ebv_lu_factor_host: NULL matrix pointer");
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = timed(c, KC_OTHER, 0, 0, s, 1, [&] { return launch_set_info0(d_info, s); });
+  if (e != cudaSuccess) return cuda_fail(e, "info init");
+  if (n == 0) return EBV_SUCCESS;
+  if (c->path == EBV_PATH_LEFT && tau >= 0) {
+    // left-looking: the column blocks stream in under the factorization
+    e = timed(c, KC_OTHER, 0, 0, s, 1, [&] { return launch_tau(n, A, lda, tau, c->d_tau, c->d_norm, s); });
+    if (e == cudaSuccess) e = lu_left(c, n, A, lda, d_info, s, hA, ldh);
+    if (e != cudaSuccess) return cuda_fail(e, "host factor (left-looking)");
+    return EBV_SUCCESS;
+  }
+  // default: one copy, then the (faster) right-looking schedule
+  e = cudaMemcpy2DAsync(A, lda * sizeof(double), hA, ldh * sizeof(double), n * sizeof(double), n,
+                        cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "host copy");
+  return factor_body(c, n, A, lda, tau, d_info, s);
 }
 
 ebv_status_t ebv_lu_solve(ebv_context_t c, int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb,

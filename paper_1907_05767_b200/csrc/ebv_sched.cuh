@@ -32,6 +32,8 @@ struct ebv_context {
   bool lookahead = true;    // factor panel K+1 on a side stream under the update of step K
   cudaStream_t side = nullptr;
   cudaEvent_t ev_start = nullptr, ev_a = nullptr, ev_p = nullptr;
+  cudaStream_t copy = nullptr;            // host -> device column blocks (ebv_lu_factor_host)
+  std::vector<cudaEvent_t> copy_ev;       // one per column block
   bool stats = false;
   struct Rec {
     int cls;
@@ -108,6 +110,8 @@ cudaError_t lu_rec(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t ko
 cudaError_t panel_rec(ebv_context* c, int64_t M, int64_t w, double* P, int64_t lda, int64_t koff, int64_t* info,
                       cudaStream_t s);
 cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s);
+cudaError_t lu_left(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s,
+                    const double* hA, int64_t ldh);
 void dist_release(ebv_context* c);   // ebv_dist.cu
 
 }  // namespace sched

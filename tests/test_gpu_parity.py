@@ -225,6 +225,40 @@ def test_solve_many_rhs_bitwise(dev, ctx, n, nrhs):
     assert bits_eq(X.cpu().numpy(), oracle.lu_solve(lu_o, d["B"].cpu().numpy()))
 
 
+# ------------------------------------------------------------------ left-looking / host-resident
+@pytest.mark.parametrize("n,nb", [(1, 0), (64, 0), (65, 64), (700, 64), (700, 128), (1537, 64), (3000, 0),
+                                  (2100, 256)])
+def test_left_looking_bitwise(dev, ctx, n, nb):
+    d = ebv_inputs.generate(n, seed=n + 77, device=dev)
+    A = d["At"].T
+    c = ebv.Context(0, path=ebv.EBV_PATH_LEFT)
+    c.set_block(nb)
+    LU, info = ebv.lu_factor(A, ctx=c)
+    torch.cuda.synchronize()
+    lu_o, info_o = oracle.lu_factor(A.cpu().numpy())
+    assert int(info) == info_o
+    assert bits_eq(LU.cpu().numpy(), lu_o)
+
+
+@pytest.mark.parametrize("n,pinned,tau", [(700, True, 0.0), (1537, False, 0.0), (3000, True, 0.0), (513, True, -1.0)])
+def test_factor_host_bitwise(dev, ctx, n, pinned, tau):
+    """ebv_lu_factor_host: the matrix streamed from host memory block by block
+    under the left-looking factorization — bitwise the oracle."""
+    d = ebv_inputs.generate(n, seed=n + 78)
+    hA = d["At"].T                      # CPU, column-major storage
+    if pinned:
+        hA = hA.mT.contiguous().pin_memory().mT
+    LU, info = ebv.lu_factor_host(hA, tau=tau, ctx=ctx)
+    cl = ebv.Context(0, path=ebv.EBV_PATH_LEFT)          # the streamed (left-looking) form
+    LU2, info2 = ebv.lu_factor_host(hA, tau=tau, ctx=cl)
+    torch.cuda.synchronize()
+    assert bits_eq(LU2.cpu().numpy(), LU.cpu().numpy()) and int(info2) == int(info)
+    lu_o, info_o = oracle.lu_factor(d["At"].T.numpy(), tau=(n * np.finfo(float).eps *
+                                                            np.abs(d["At"].T.numpy()).sum(1).max()) if tau < 0 else 0.0)
+    assert int(info) == info_o
+    assert bits_eq(LU.cpu().numpy(), lu_o)
+
+
 # ------------------------------------------------------------------ f3: unit diagonal, LDU
 @pytest.mark.parametrize("n,nrhs", [(1, 1), (2, 0), (300, 3), (1537, 1)])
 def test_normalize_unit_diagonal_bitwise(dev, ctx, n, nrhs):
