@@ -323,12 +323,13 @@ int64_t ebv_block_owner(int64_t J, int64_t N, int64_t nranks, ebv_layout_t layou
 /* ---- measurement --------------------------------------------------------- */
 
 /* Per-kernel-class statistics, recorded with CUDA events on the launching
- * stream while enabled (off by default).  Classes: 0 = DMMA trailing update
- * (GEMM), 1 = diagonal-block LU, 2 = TRSM, 3 = solve, 4 = batched,
- * 5 = vector path, 6 = other.  ebv_stats_get synchronizes the events and
+ * stream while enabled (off by default).  Classes: 0 = other DMMA launches
+ * (inside the recursive TRSMs and panels), 1 = diagonal-block LU (panel
+ * leaves), 2 = TRSM, 3 = solve, 4 = batched, 5 = vector path, 6 = other,
+ * 7 = the trailing rank-nb update of Eq 6-c (DMMA; the dominant kernel).  ebv_stats_get synchronizes the events and
  * returns for class c: launches, total milliseconds, algorithmic flops and
  * algorithmic bytes. */
-#define EBV_NUM_KCLASSES 7
+#define EBV_NUM_KCLASSES 8
 ebv_status_t ebv_stats_enable(ebv_context_t ctx, int enable);
 ebv_status_t ebv_stats_reset(ebv_context_t ctx);
 ebv_status_t ebv_stats_get(ebv_context_t ctx, int kclass, int64_t* launches, double* ms,

@@ -28,7 +28,7 @@ LIB_PATH = os.path.join(_HERE, "libebv.so")
 EBV_SUCCESS = 0
 EBV_PATH_AUTO, EBV_PATH_VECTOR, EBV_PATH_BLOCKED, EBV_PATH_LEFT = 0, 1, 2, 3
 EBV_LAYOUT_CYCLIC, EBV_LAYOUT_EBVPAIR, EBV_LAYOUT_SNAKE = 0, 1, 2
-KCLASSES = ["gemm_dmma", "leaf_lu", "trsm", "solve", "batched", "vector", "other"]
+KCLASSES = ["gemm_dmma", "leaf_lu", "trsm", "solve", "batched", "vector", "other", "update"]
 
 # every exported symbol of include/ebv.h with its ctypes signature
 _i64, _i32, _vp, _d, _int = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_double, ctypes.c_int

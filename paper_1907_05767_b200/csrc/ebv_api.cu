@@ -54,10 +54,10 @@ cudaEvent_t get_event(ebv_context* c) {
 }
 
 cudaError_t gemm(ebv_context* c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
-                 int64_t ldb, double* C, int64_t ldc, bool rev, cudaStream_t s) {
+                 int64_t ldb, double* C, int64_t ldc, bool rev, cudaStream_t s, int cls) {
   if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
   double fl = 2.0 * M * N * K, by = 8.0 * (M * K + K * N + 2.0 * M * N);
-  return timed(c, KC_GEMM, fl, by, s, 1, [&] { return launch_gemm_sub(M, N, K, A, lda, B, ldb, C, ldc, rev, s); });
+  return timed(c, cls, fl, by, s, 1, [&] { return launch_gemm_sub(M, N, K, A, lda, B, ldb, C, ldc, rev, s); });
 }
 
 int64_t split_point(int64_t n, int64_t leaf) {
@@ -256,19 +256,19 @@ cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_
       // U12 (columns are independent: same bits).
       const bool split = kU12SplitRows >= 0 ? rest < kU12SplitRows : n >= 16384;
       e = trsm_l(c, w, split ? w1 : rest, P, lda, P + w * lda, lda, s);
-      if (e == cudaSuccess) e = gemm(c, rest, w1, w, P + w, lda, P + w * lda, lda, P1, lda, false, s);
+      if (e == cudaSuccess) e = gemm(c, rest, w1, w, P + w, lda, P + w * lda, lda, P1, lda, false, s, KC_UPDATE);
       if (e == cudaSuccess) e = cudaEventRecord(c->ev_a, s);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_a, 0);
       if (e == cudaSuccess) e = panel_rec(c, rest, w1, P1, lda, c0 + w, info, c->side);
       if (e == cudaSuccess) e = cudaEventRecord(c->ev_p, c->side);
       if (e == cudaSuccess && split) e = trsm_l(c, w, rest - w1, P, lda, P + (w + w1) * lda, lda, s);
       if (e == cudaSuccess)
-        e = gemm(c, rest, rest - w1, w, P + w, lda, P + (w + w1) * lda, lda, P1 + w1 * lda, lda, false, s);
+        e = gemm(c, rest, rest - w1, w, P + w, lda, P + (w + w1) * lda, lda, P1 + w1 * lda, lda, false, s, KC_UPDATE);
       if (e != cudaSuccess) return e;
     } else {
       e = trsm_l(c, w, rest, P, lda, P + w * lda, lda, s);
       if (e != cudaSuccess) return e;
-      e = gemm(c, rest, rest, w, P + w, lda, P + w * lda, lda, P1, lda, false, s);
+      e = gemm(c, rest, rest, w, P + w, lda, P + w * lda, lda, P1, lda, false, s, KC_UPDATE);
       if (e != cudaSuccess) return e;
       if (la) {   // keep the event protocol: the next panel is factored in order
         e = panel_rec(c, rest, w1, P1, lda, c0 + w, info, s);
@@ -339,12 +339,13 @@ cudaError_t lu_left(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* 
       const int64_t cp = c0 - nb;                       // panel J-1 = columns [cp, c0)
       if (cp > 0) {                                     // panels 0..J-2
         e = trsm_l(c, cp, w, A, lda, X, lda, s);
-        if (e == cudaSuccess) e = gemm(c, n - cp, w, cp, A + cp, lda, X, lda, X + cp, lda, false, s);
+        if (e == cudaSuccess) e = gemm(c, n - cp, w, cp, A + cp, lda, X, lda, X + cp, lda, false, s, KC_UPDATE);
         if (e != cudaSuccess) return e;
       }
       e = cudaStreamWaitEvent(s, c->ev_p, 0);          // panel J-1 factored (side stream)
       if (e == cudaSuccess) e = trsm_l(c, nb, w, A + cp + cp * lda, lda, X + cp, lda, s);
-      if (e == cudaSuccess) e = gemm(c, n - c0, w, nb, A + c0 + cp * lda, lda, X + cp, lda, X + c0, lda, false, s);
+      if (e == cudaSuccess)
+        e = gemm(c, n - c0, w, nb, A + c0 + cp * lda, lda, X + cp, lda, X + c0, lda, false, s, KC_UPDATE);
       if (e != cudaSuccess) return e;
     }
     e = cudaEventRecord(c->ev_a, s);
@@ -764,7 +765,7 @@ ebv_status_t ebv_update(ebv_context_t c, int64_t M, int64_t N, int64_t K, const 
   if (M == 0 || N == 0 || K == 0) return EBV_SUCCESS;
   if (!A || !B || !C) return invalid("ebv_update: NULL pointer");
   DeviceGuard g(c->device);
-  cudaError_t e = gemm(c, M, N, K, A, lda, B, ldb, C, ldc, false, (cudaStream_t)stream);
+  cudaError_t e = gemm(c, M, N, K, A, lda, B, ldb, C, ldc, false, (cudaStream_t)stream, KC_UPDATE);
   if (e != cudaSuccess) return cuda_fail(e, "update");
   return EBV_SUCCESS;
 }

@@ -258,7 +258,7 @@ ebv_status_t dist_factor(ebv_context* c, ebv_dist_state* d, std::vector<View>& v
       if (has_next && v.plan.rank == owner1) {
         const int64_t w1 = p0.width(K + 1);    // block K+1 is the first local block after K
         e = trsm_l(c, w, w1, pbuf(K), M, X, v.lda, s);
-        if (e == cudaSuccess) e = gemm(c, M - w, w1, w, pbuf(K) + w, M, X, v.lda, X + w, v.lda, false, s);
+        if (e == cudaSuccess) e = gemm(c, M - w, w1, w, pbuf(K) + w, M, X, v.lda, X + w, v.lda, false, s, KC_UPDATE);
         if (e == cudaSuccess) e = cudaEventRecord(d->ev_next, s);
         if (e != cudaSuccess) return cuda_fail(e, "dist update(next)");
         first = w1;
@@ -267,7 +267,7 @@ ebv_status_t dist_factor(ebv_context* c, ebv_dist_state* d, std::vector<View>& v
         double* X2 = X + first * v.lda;
         e = trsm_l(c, w, ncols - first, pbuf(K), M, X2, v.lda, s);
         if (e == cudaSuccess)
-          e = gemm(c, M - w, ncols - first, w, pbuf(K) + w, M, X2, v.lda, X2 + w, v.lda, false, s);
+          e = gemm(c, M - w, ncols - first, w, pbuf(K) + w, M, X2, v.lda, X2 + w, v.lda, false, s, KC_UPDATE);
         if (e != cudaSuccess) return cuda_fail(e, "dist update");
       }
     }

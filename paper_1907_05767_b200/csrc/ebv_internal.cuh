@@ -11,7 +11,7 @@ namespace ebv {
 
 // Kernel classes for the measurement hooks (ebv_stats_*).
 enum KClass { KC_GEMM = 0, KC_LEAF = 1, KC_TRSM = 2, KC_SOLVE = 3, KC_BATCHED = 4, KC_VECTOR = 5,
-              KC_OTHER = 6 };
+              KC_OTHER = 6, KC_UPDATE = 7 };
 
 void set_error(const std::string& msg);
 

@@ -98,7 +98,7 @@ cudaError_t timed(ebv_context* c, int cls, double flops, double bytes, cudaStrea
 }
 
 cudaError_t gemm(ebv_context* c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
-                 int64_t ldb, double* C, int64_t ldc, bool rev, cudaStream_t s);
+                 int64_t ldb, double* C, int64_t ldc, bool rev, cudaStream_t s, int cls = KC_GEMM);
 int64_t split_point(int64_t n, int64_t leaf);
 cudaError_t trsm_r(ebv_context* c, int64_t m, int64_t k, double* X, int64_t ldx, const double* U, int64_t ldu,
                    cudaStream_t s);
