@@ -263,7 +263,10 @@ cudaError_t launch_gemm_sub(int64_t M, int64_t N, int64_t K, const double* A, in
   if (!reverse_k && tma_variant() >= 0 && cfg_override() < 0 &&
       gemm_tma_eligible(M, N, K, A, lda, B, ldb)) {
     int v = tma_variant();
-    if (v == 0 && M <= 64) v = 3;
+    // default: 128x64 tiles, 2 CTAs/SM; a 3-stage ring for the factorization's
+    // K <= 1024 updates (B200: 28.8 -> 31.2 TF/s at 8064^2 x 128, equal at
+    // K = 512), 4 stages for long K; 64 x 128 tiles for M <= 64
+    if (v == 0) v = (M <= 64) ? 3 : (K <= 1024 ? 5 : 0);
     cudaError_t e = launch_gemm_sub_tma(M, N, K, A, lda, B, ldb, Cm, ldc, v, s);
     if (e != cudaErrorNotSupported) return e;
     (void)cudaGetLastError();

@@ -263,6 +263,8 @@ using TMid = TCfg<128, 64, 4, 2, 16, 4, 2>;     // 8 warps (32x32 warp tiles), 2
 using TBig = TCfg<128, 128, 4, 4, 16, 4, 1>;    // 16 warps (32x32), 1 CTA/SM
 using TBig8 = TCfg<128, 128, 2, 4, 16, 4, 1>;   // 8 warps (64x32), 1 CTA/SM
 using TWide = TCfg<64, 128, 2, 4, 16, 4, 2>;    // 8 warps (32x32), 2 CTAs/SM
+using TBig6 = TCfg<128, 128, 4, 4, 16, 6, 1>;   // 16 warps (32x32), 1 CTA/SM, 6-stage ring
+using TMid3 = TCfg<128, 64, 4, 2, 16, 3, 2>;    // TMid with a 3-stage ring (less smem)
 
 }  // namespace
 
@@ -279,6 +281,8 @@ cudaError_t launch_gemm_sub_tma(int64_t M, int64_t N, int64_t K, const double* A
     case 1: return run_tma<TBig>(M, N, K, A, lda, B, ldb, Cm, ldc, s);
     case 2: return run_tma<TBig8>(M, N, K, A, lda, B, ldb, Cm, ldc, s);
     case 3: return run_tma<TWide>(M, N, K, A, lda, B, ldb, Cm, ldc, s);
+    case 4: return run_tma<TBig6>(M, N, K, A, lda, B, ldb, Cm, ldc, s);
+    case 5: return run_tma<TMid3>(M, N, K, A, lda, B, ldb, Cm, ldc, s);
     default: return run_tma<TMid>(M, N, K, A, lda, B, ldb, Cm, ldc, s);
   }
 }

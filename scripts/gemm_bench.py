@@ -9,9 +9,10 @@ dev = torch.device("cuda:0")
 ctx = ebv.Context(0)
 def cm(r, c):
     return torch.randn(c, r, dtype=torch.float64, device=dev).T
-shapes = [(16384, 16384, 16384), (8192, 8192, 8192), (4096, 4096, 4096), (32512, 32512, 256),
+shapes = [tuple(int(v) for v in x.split("x")) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [(16384, 16384, 16384), (8192, 8192, 8192), (4096, 4096, 4096), (32512, 32512, 256),
           (16384, 16384, 256), (8064, 8064, 128), (8192, 8192, 64), (16384, 64, 64), (64, 16384, 64),
           (4096, 4096, 64), (2048, 2048, 2048), (1024, 1024, 1024)]
+print(json.dumps({"variant_env": os.environ.get("EBV_GEMM_TMA", "0")}), flush=True)
 for M, N, K in shapes:
     C, A, B = cm(M, N), cm(M, K), cm(K, N)
     ebv.update(C, A, B, ctx=ctx)
