@@ -249,6 +249,14 @@ ebv_status_t ebv_lu_to_ldu(ebv_context_t ctx, int64_t n, double* LU, int64_t lda
 ebv_status_t ebv_update(ebv_context_t ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                         const double* B, int64_t ldb, double* C, int64_t ldc, void* stream);
 
+/* ---- multi-GPU: batched systems (C5) sharded over P GPUs --- */
+/* Contiguous, balanced system range of `rank` among `nranks` (host only):
+ * ranks < batch % nranks take one extra system.  Each rank then calls
+ * ebv_lu_factor_batched on its range — no collective on the data path.
+ * Errors: INVALID_VALUE for batch < 0, nranks < 1, rank out of range, NULL
+ * outputs. */
+ebv_status_t ebv_batched_shard(int64_t batch, int rank, int nranks, int64_t* first, int64_t* count);
+
 /* ---- multi-GPU: one system over P GPUs -------- */
 /* 1D block-cyclic columns: column block J (width nb, the last one ragged)
  * lives on rank ebv_block_owner(J, N, P, layout); a rank stores its blocks

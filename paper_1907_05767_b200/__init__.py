@@ -42,6 +42,7 @@ SIGNATURES = {
     "ebv_set_vector_ctas": (_int, [_vp, _i64]),
     "ebv_set_block": (_int, [_vp, _i64]),
     "ebv_block_width": (_i64, [_vp, _i64]),
+    "ebv_batched_shard": (_int, [_i64, _int, _int, _vp, _vp]),
     "ebv_lu_factor_host": (_int, [_vp, _i64, _vp, _i64, _vp, _i64, _d, _vp, _vp]),
     "ebv_stats_timeline": (_i64, [_vp, _vp, _i64]),
     "ebv_set_lookahead": (_int, [_vp, _int]),
@@ -160,6 +161,17 @@ def ebv_lu_factor_batched(ctx, n, A, lda, strideA, batch, B, ldb, strideB, nrhs,
 
 def ebv_lu_solve_batched(ctx, n, LU, lda, strideA, batch, B, ldb, strideB, nrhs, stream):
     return lib().ebv_lu_solve_batched(ctx, n, LU, lda, strideA, batch, B, ldb, strideB, nrhs, stream)
+
+
+def ebv_batched_shard(batch, rank, nranks, first, count):
+    return lib().ebv_batched_shard(batch, rank, nranks, first, count)
+
+
+def batched_shard(batch: int, rank: int, nranks: int):
+    """(first, count) of rank's contiguous share of `batch` systems (C5 sharding)."""
+    f, c = ctypes.c_int64(), ctypes.c_int64()
+    _check(ebv_batched_shard(batch, rank, nranks, ctypes.byref(f), ctypes.byref(c)), "ebv_batched_shard")
+    return f.value, c.value
 
 
 def ebv_lu_factor_host(ctx, n, hA, ldh, A, lda, tau, d_info, stream):

@@ -770,6 +770,15 @@ ebv_status_t ebv_update(ebv_context_t c, int64_t M, int64_t N, int64_t K, const 
   return EBV_SUCCESS;
 }
 
+ebv_status_t ebv_batched_shard(int64_t batch, int rank, int nranks, int64_t* first, int64_t* count) {
+  if (batch < 0 || nranks < 1 || rank < 0 || rank >= nranks || !first || !count)
+    return invalid("ebv_batched_shard: bad arguments");
+  const int64_t q = batch / nranks, r = batch % nranks;
+  *count = q + (rank < r ? 1 : 0);
+  *first = rank * q + (rank < r ? rank : r);
+  return EBV_SUCCESS;
+}
+
 // ---- EbV plan ----------------------------------------------------------------
 
 ebv_status_t ebv_plan_owner_map(int64_t n, int64_t workers, int32_t* owner) {

@@ -90,6 +90,9 @@ def test_argument_validation_without_gpu():
     assert L.ebv_normalize_unit_diagonal(None, 4, None, 4, None, 4, 1, None, None, None) == 1
     assert L.ebv_lu_to_ldu(None, 4, None, 4, None, None) == 1
     assert L.ebv_lu_factor_host(None, 4, None, 4, None, 4, 0.0, None, None) == 1
+    assert ebv.batched_shard(10, 2, 3) == (7, 3) and ebv.batched_shard(0, 0, 4) == (0, 0)
+    with pytest.raises(ebv.EbvError):
+        ebv.batched_shard(10, 3, 3)
     assert ebv.ebv_status_string(0) == "success"
     assert ebv.ebv_status_string(5) == "not supported"
 

@@ -106,3 +106,51 @@ def test_gloo_world2_block_cyclic_schedule(n, nb, layout):
     A = ebv_inputs.generate(n, seed=3)["At"].T.numpy()
     lu_o, _ = oracle.lu_factor(A)
     assert np.max(np.abs(full - lu_o)) <= 1e-12 * np.max(np.abs(lu_o))
+
+
+def _batched_worker(rank, world, port, batch, n, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import ebv_inputs
+        import oracle
+        import paper_1907_05767_b200 as ebv
+        first, count = ebv.batched_shard(batch, rank, world)
+        d = ebv_inputs.generate_batched(count, n, seed=5, nrhs=1, first_system=first)
+        lu, x, info = oracle.lu_factor_batched(d["At"].transpose(1, 2).numpy(), d["B"].numpy())
+        # no collective on the data path; results gathered only to check them
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (first, count, x))
+        if rank == 0:
+            q.put(gathered)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("batch,n", [(7, 32), (10, 5)])
+def test_gloo_world2_batched_sharding(batch, n):
+    """C5 sharding: each rank takes ebv_batched_shard's
+    contiguous range, generates its systems (generator offset by the first
+    system index) and solves them alone; the union equals the unsharded
+    computation bitwise and the ranges partition the batch."""
+    import ebv_inputs
+    import oracle
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batched_worker, args=(r, world, port, batch, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    gathered = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    firsts = sorted((f, c) for f, c, _ in gathered)
+    assert firsts[0][0] == 0 and sum(c for _, c in firsts) == batch
+    assert all(firsts[i][0] + firsts[i][1] == firsts[i + 1][0] for i in range(len(firsts) - 1))
+    full = ebv_inputs.generate_batched(batch, n, seed=5, nrhs=1)
+    _, x_full, _ = oracle.lu_factor_batched(full["At"].transpose(1, 2).numpy(), full["B"].numpy())
+    x_sh = np.concatenate([x for f, c, x in sorted(gathered, key=lambda g: g[0])])
+    assert np.array_equal(x_sh.view(np.uint64), x_full.view(np.uint64))
