@@ -27,6 +27,7 @@
 // dependent divisions), rows below ~3.5 us.
 #include "ebv_internal.cuh"
 
+#include <cstdlib>
 #include <type_traits>
 
 namespace ebv {
@@ -65,9 +66,14 @@ __device__ __forceinline__ double quot(double y, double u, double r, bool& ok) {
   return q;
 }
 
-__device__ __forceinline__ int block_owner(int J, int Nb, int C, int cyclic) {
-  if (cyclic) return J % C;
-  int p = J < Nb - 1 - J ? J : Nb - 1 - J;
+// owner CTA of column block J: blocks are grouped in chunks of cb
+// consecutive blocks (a chunk's blocks hand over to each other inside one
+// CTA, from shared memory); chunk pairs {i, Nc-1-i} (first with last) are
+// dealt round-robin, or chunk i -> i mod C (cyclic)
+__device__ __forceinline__ int block_owner(int J, int Nb, int C, int cyclic, int cb) {
+  const int ch = J / cb, Nc = (Nb + cb - 1) / cb;
+  if (cyclic) return ch % C;
+  const int p = ch < Nc - 1 - ch ? ch : Nc - 1 - ch;
   return p % C;
 }
 
@@ -97,7 +103,8 @@ constexpr int BWMAX = 8;   // block width limit
 // SASS instructions and 8x slower per block).
 __global__ void __launch_bounds__(VT, 1)
     vector_lu_kernel(int n, double* __restrict__ A, int64_t lda, const double* __restrict__ tau,
-                     unsigned long long* info_min, int* flags, int epoch, int cyclic, int bw, int maxcols) {
+                     unsigned long long* info_min, int* flags, int epoch, int cyclic, int bw, int maxcols,
+                     int cb) {
   extern __shared__ double scol[];         // owned columns [maxcols][n]
   __shared__ int cols[1024];               // owned global column indices (ascending)
   __shared__ double srcp[BWMAX];           // RN(1/u_kk) of the block being factored
@@ -107,7 +114,7 @@ __global__ void __launch_bounds__(VT, 1)
   if (tid == 0) {
     int c = 0;
     for (int J = 0; J < Nb; J++)
-      if (block_owner(J, Nb, C, cyclic) == me)
+      if (block_owner(J, Nb, C, cyclic, cb) == me)
         for (int j = J * bw; j < n && j < (J + 1) * bw; j++) cols[c++] = j;
     ncols_s = c;
   }
@@ -284,14 +291,14 @@ __global__ void __launch_bounds__(VT, 1)
     EBV_VTR(J, 4);
   };
 
-  if (block_owner(0, Nb, C, cyclic) == me) factor_block(0);
+  if (block_owner(0, Nb, C, cyclic, cb) == me) factor_block(0);
   for (int J = 0; J < Nb - 1; J++) {
     const int k0 = J * bw, k1 = min(n, (J + 1) * bw);
     const int c1 = first_slot(k1);                  // first owned column after block J
     if (c1 >= ncols) break;                         // nothing of mine is updated by block J or later
     const double* lsrc;
     int64_t lstr = n;
-    if (block_owner(J, Nb, C, cyclic) == me) {
+    if (block_owner(J, Nb, C, cyclic, cb) == me) {
       lsrc = scol + (size_t)first_slot(k0) * n;    // block J's columns, final here
     } else {
       if (tid == 0) wait_flag(flags + J, epoch);
@@ -302,7 +309,7 @@ __global__ void __launch_bounds__(VT, 1)
       lsrc = A + (int64_t)k0 * lda;
       lstr = lda;
     }
-    if (block_owner(J + 1, Nb, C, cyclic) == me) {
+    if (block_owner(J + 1, Nb, C, cyclic, cb) == me) {
       EBV_VTR(J + 1, 0);
       // lookahead: block J+1 first, factor + publish it, then the rest
       const int c2 = first_slot(min(n, (J + 2) * bw));
@@ -325,18 +332,29 @@ __global__ void info_finalize_kernel(const unsigned long long* info_min, int64_t
   *info = (v == ~0ull) ? 0 : (int64_t)v;
 }
 
+int chunk_blocks() {   // EBV_VECTOR_CHUNK: consecutive blocks per owner chunk (default 1)
+  static int v = [] {
+    const char* e = getenv("EBV_VECTOR_CHUNK");
+    const int c = e ? atoi(e) : 1;
+    return c > 0 ? c : 1;
+  }();
+  return v;
+}
+
 int max_cols(int64_t n, int C, int cyclic, int bw) {
-  const int64_t Nb = (n + bw - 1) / bw;
-  if (cyclic) return (int)(((Nb + C - 1) / C) * bw);
-  const int64_t pairs = (Nb + 1) / 2;
-  return (int)(2 * ((pairs + C - 1) / C) * bw);
+  const int64_t cb = chunk_blocks();
+  const int64_t Nb = (n + bw - 1) / bw, Nc = (Nb + cb - 1) / cb;
+  if (cyclic) return (int)(((Nc + C - 1) / C) * cb * bw);
+  const int64_t pairs = (Nc + 1) / 2;
+  return (int)(2 * ((pairs + C - 1) / C) * cb * bw);
 }
 
 int clamp_ctas(int64_t n, int num_ctas, int bw) {
   const int cyclic = num_ctas < 0 ? 1 : 0;
   int C = num_ctas < 0 ? -num_ctas : num_ctas;
-  const int64_t Nb = (n + bw - 1) / bw;
-  const int64_t units = cyclic ? Nb : (Nb + 1) / 2;
+  const int64_t cb = chunk_blocks();
+  const int64_t Nb = (n + bw - 1) / bw, Nc = (Nb + cb - 1) / cb;
+  const int64_t units = cyclic ? Nc : (Nc + 1) / 2;
   if (C > units) C = (int)units;
   if (C < 1) C = 1;
   return C;
@@ -394,8 +412,8 @@ cudaError_t launch_vector_lu(int64_t n, double* A, int64_t lda, const double* ta
   if (e != cudaSuccess) return e;
   static int epoch = 0;
   epoch = (epoch % 0x3FFFFFF0) + 1;
-  int nn = (int)n, ep = epoch, cy = cyclic, bwv = bw, mcv = mc;
-  void* args[] = {&nn, &A, &lda, (void*)&tau, &info_min, &flags_ws, &ep, &cy, &bwv, &mcv};
+  int nn = (int)n, ep = epoch, cy = cyclic, bwv = bw, mcv = mc, cbv = chunk_blocks();
+  void* args[] = {&nn, &A, &lda, (void*)&tau, &info_min, &flags_ws, &ep, &cy, &bwv, &mcv, &cbv};
   e = cudaLaunchCooperativeKernel((void*)vector_lu_kernel, dim3(C), dim3(VT), args, smem, s);
   if (e != cudaSuccess) return e;
   info_finalize_kernel<<<1, 1, 0, s>>>(info_min, info);
