@@ -328,21 +328,9 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
     }
     // every thread's stores of this block precede thread 0's release (bar.sync
     // orders them at CTA scope; the gpu-scope release is cumulative)
-#ifndef EBV_RELEASE_VARIANT
-#define EBV_RELEASE_VARIANT 0
-#endif
-    if (EBV_RELEASE_VARIANT == 1) __threadfence();
     __syncthreads();
     EBV_TR(4);
-    if (i == 0) {
-      if (EBV_RELEASE_VARIANT == 2) {
-        asm volatile("st.relaxed.gpu.global.b32 [%0], %1;\n" ::"l"(flags + I), "r"(epoch) : "memory");
-      } else if (EBV_RELEASE_VARIANT == 1) {
-        asm volatile("st.relaxed.gpu.global.b32 [%0], %1;\n" ::"l"(flags + I), "r"(epoch) : "memory");
-      } else {
-        st_release(flags + I, epoch);
-      }
-    }
+    if (i == 0) st_release(flags + I, epoch);
     EBV_TR(5);
   }
 }
