@@ -70,13 +70,19 @@ def xtrue_units(base, rows: torch.Tensor, rhs: torch.Tensor, n: int) -> torch.Te
 
 
 def generate(n: int, seed: int = 1, nrhs: int = 1, device="cpu", system: int = 0,
-             cols: torch.Tensor | None = None, chunk: int = 2048, with_b: bool = True):
-    """Dense strictly row-diagonally-dominant system on the 2^-30 grid.
+             cols: torch.Tensor | None = None, chunk: int = 2048, with_b: bool = True,
+             kl: int | None = None, ku: int | None = None, stencil_m: int | None = None):
+    """Strictly row-diagonally-dominant system on the 2^-30 grid.
 
     Returns dict(At=(ncols, n) float64 column-major storage of A[:, cols],
     X=(n, nrhs) float64 exact solution, B=(n, nrhs) float64 = A X exactly).
     ``cols`` selects a subset of columns (a rank's local slab); row sums are
-    always taken over all n columns."""
+    always taken over all n columns.  Sparsity (the paper's
+    banded / sparse workload, synthetic): ``kl`` / ``ku`` keep only
+    the entries with i - j <= kl and j - i <= ku (a band); ``stencil_m``
+    keeps the 2D five-point pattern of an m x m grid (n = m^2: neighbours
+    i +- 1 within a grid row and i +- m).  Zeros are exact; the diagonal
+    stays row abs-sum + 1."""
     dev = torch.device(device)
     base = system_base(seed, system)
     rows = torch.arange(n, dtype=torch.int64, device=dev)
@@ -96,6 +102,20 @@ def generate(n: int, seed: int = 1, nrhs: int = 1, device="cpu", system: int = 0
         K = offdiag_units(base, rows[None, :], jj[:, None])            # (cj, n): K[c, i] = k_{i, j0+c}
         diag = (rows[None, :] == jj[:, None])
         K = torch.where(diag, torch.zeros_like(K), K)
+        if kl is not None or ku is not None:
+            d = jj[:, None] - rows[None, :]                              # j - i
+            keep_b = torch.ones_like(diag)
+            if kl is not None:
+                keep_b &= (-d) <= kl
+            if ku is not None:
+                keep_b &= d <= ku
+            K = torch.where(keep_b, K, torch.zeros_like(K))
+        if stencil_m is not None:
+            m = stencil_m
+            d = (jj[:, None] - rows[None, :]).abs()
+            same_row = (jj[:, None] // m) == (rows[None, :] // m)
+            keep_s = ((d == 1) & same_row) | (d == m)
+            K = torch.where(keep_s, K, torch.zeros_like(K))
         rowsum += K.abs().sum(0)
         if with_b:
             rowdot += K.t() @ X_u[j0:j1] if dev.type == "cpu" else _int_matmul(K.t(), X_u[j0:j1])

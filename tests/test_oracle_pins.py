@@ -305,3 +305,40 @@ def test_ldu_of_symmetric_matrix_has_u_prime_equal_l_transpose():
         for j in range(k + 1, n):
             exact = Fraction(lu[k, j]) / Fraction(lu[k, k])
             assert abs(Fraction(ldu[k, j]) - exact) <= Fraction(_ulp(ldu[k, j])) / 2
+
+
+# ---------------------------------------------------------------- f4: banded / stencil inputs
+@pytest.mark.parametrize("n,kl,ku", [(40, 3, 5), (33, 0, 4), (30, 6, 0), (25, 24, 1)])
+def test_banded_lu_keeps_the_band(n, kl, ku):
+    """No-pivot LU of a (kl, ku)-banded matrix has L of lower bandwidth kl and
+    U of upper bandwidth ku (Golub & Van Loan Thm 4.3.1): every entry of the
+    oracle's packed factors outside the band is exactly zero, and inside it
+    the factors equal the exact rational LU to ~1e-14."""
+    d = ebv_inputs.generate(n, seed=n + kl, kl=kl, ku=ku)
+    a = d["At"].T.numpy().copy()
+    i, j = np.indices((n, n))
+    assert np.all(a[(i - j > kl) | (j - i > ku)] == 0.0)
+    lu, info = oracle.lu_factor(a)
+    assert info == 0
+    assert np.all(lu[(i - j > kl) | (j - i > ku)] == 0.0)
+    L, U = exact.lu_exact(a)
+    Lf = np.array([[float(v) for v in r] for r in L])
+    Uf = np.array([[float(v) for v in r] for r in U])
+    Lo, Uo = oracle.unpack(lu)
+    assert np.max(np.abs(Lo - Lf)) <= 1e-14 * max(1.0, np.max(np.abs(Lf)))
+    assert np.max(np.abs(Uo - Uf)) <= 1e-14 * np.max(np.abs(Uf))
+
+
+def test_stencil_fill_stays_in_the_band():
+    """The 2D five-point pattern on an m x m grid: the LU fills in only within
+    the bandwidth m (the profile of the outermost nonzeros), exactly zero
+    outside; the solution is x_true to rounding."""
+    m = 6
+    n = m * m
+    d = ebv_inputs.generate(n, seed=4, stencil_m=m)
+    a = d["At"].T.numpy().copy()
+    lu, info = oracle.lu_factor(a)
+    i, j = np.indices((n, n))
+    assert info == 0 and np.all(lu[np.abs(i - j) > m] == 0.0)
+    x = oracle.lu_solve(lu, d["B"].numpy())
+    assert np.max(np.abs(x - d["X"].numpy())) <= 1e-13
