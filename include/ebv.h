@@ -204,6 +204,22 @@ ebv_status_t ebv_lu_factor_batched(ebv_context_t ctx, int64_t n, double* A, int6
                                    int64_t strideB, int64_t nrhs, double tau, int32_t* d_info,
                                    void* stream);
 
+/* Banded / sparse inputs (the paper's second workload, P:93-103, P:119;
+ * SURVEY §8f f4): A (dense column-major storage, lda >= n) has a_ij = 0 for
+ * i - j > kl and j - i > ku.  No-pivot LU keeps that band (L lower bandwidth
+ * kl, U upper bandwidth ku), so the blocked schedule clips every panel, U12
+ * and DMMA update to it (zero-skip: work ~ n*kl*ku instead of n^3); entries
+ * outside the band are not touched.  The factors are bitwise ebv_lu_factor's
+ * (the skipped operations are exact no-ops on zeros) for inputs with positive
+ * pivots (a negative pivot would give -0 instead of +0 below the band in the
+ * dense algorithm).  ebv_lu_solve_banded skips the zero tiles of the
+ * substitutions.  Errors as ebv_lu_factor / ebv_lu_solve, plus
+ * INVALID_VALUE for kl < 0 or ku < 0. */
+ebv_status_t ebv_lu_factor_banded(ebv_context_t ctx, int64_t n, int64_t kl, int64_t ku, double* A,
+                                  int64_t lda, double tau, int64_t* d_info, void* stream);
+ebv_status_t ebv_lu_solve_banded(ebv_context_t ctx, int64_t n, int64_t kl, int64_t ku, const double* LU,
+                                 int64_t lda, double* B, int64_t ldb, int64_t nrhs, void* stream);
+
 /* Solve only, for batched systems factored earlier by ebv_lu_factor_batched
  * (factor once, solve many — SURVEY §8f f1): for each system s,
  * B_s <- U_s^-1 (L_s^-1 B_s) with the packed LU_s = LU + s*strideA (read

@@ -42,6 +42,8 @@ SIGNATURES = {
     "ebv_set_vector_ctas": (_int, [_vp, _i64]),
     "ebv_set_block": (_int, [_vp, _i64]),
     "ebv_block_width": (_i64, [_vp, _i64]),
+    "ebv_lu_factor_banded": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _d, _vp, _vp]),
+    "ebv_lu_solve_banded": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _vp]),
     "ebv_batched_shard": (_int, [_i64, _int, _int, _vp, _vp]),
     "ebv_lu_factor_host": (_int, [_vp, _i64, _vp, _i64, _vp, _i64, _d, _vp, _vp]),
     "ebv_stats_timeline": (_i64, [_vp, _vp, _i64]),
@@ -172,6 +174,39 @@ def batched_shard(batch: int, rank: int, nranks: int):
     f, c = ctypes.c_int64(), ctypes.c_int64()
     _check(ebv_batched_shard(batch, rank, nranks, ctypes.byref(f), ctypes.byref(c)), "ebv_batched_shard")
     return f.value, c.value
+
+
+def ebv_lu_factor_banded(ctx, n, kl, ku, A, lda, tau, d_info, stream):
+    return lib().ebv_lu_factor_banded(ctx, n, kl, ku, A, lda, tau, d_info, stream)
+
+
+def ebv_lu_solve_banded(ctx, n, kl, ku, LU, lda, B, ldb, nrhs, stream):
+    return lib().ebv_lu_solve_banded(ctx, n, kl, ku, LU, lda, B, ldb, nrhs, stream)
+
+
+def lu_factor_banded(A: torch.Tensor, kl: int, ku: int, tau: float = 0.0, ctx: Context | None = None):
+    """Zero-skip LU of a banded A (entries outside the band must be zero):
+    returns (LU, info) like lu_factor."""
+    _require(A, "A")
+    n = A.shape[0]
+    ctx = ctx or default_context(A.device.index or 0)
+    LU = A.mT.contiguous().mT.clone() if _colmajor_ld(A) < 0 else A.clone()
+    info = torch.zeros((), dtype=torch.int64, device=A.device)
+    _check(ebv_lu_factor_banded(ctx.handle, n, kl, ku, LU.data_ptr(), max(_colmajor_ld(LU), 1), float(tau),
+                                info.data_ptr(), _stream_handle(A.device)), "ebv_lu_factor_banded")
+    return LU, info
+
+
+def lu_solve_banded(LU: torch.Tensor, B: torch.Tensor, kl: int, ku: int, ctx: Context | None = None):
+    """X from the banded factors (zero tiles skipped); B (n,) or (n, nrhs)."""
+    _require(LU, "LU")
+    n = LU.shape[0]
+    ctx = ctx or default_context(LU.device.index or 0)
+    vec = B.dim() == 1
+    X = B.reshape(n, -1).mT.contiguous().mT.clone()
+    _check(ebv_lu_solve_banded(ctx.handle, n, kl, ku, LU.data_ptr(), max(_colmajor_ld(LU), 1), X.data_ptr(),
+                               max(n, 1), X.shape[1], _stream_handle(LU.device)), "ebv_lu_solve_banded")
+    return X[:, 0] if vec else X
 
 
 def ebv_lu_factor_host(ctx, n, hA, ldh, A, lda, tau, d_info, stream):

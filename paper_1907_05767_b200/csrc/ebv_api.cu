@@ -226,8 +226,21 @@ static int64_t step_width(const ebv_context* c, int64_t n, int64_t c0) {
   return (n - c0) < w ? (n - c0) : w;
 }
 
-cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s) {
-  const int64_t nb = block_width(c, n);
+// kl / ku (banded inputs): entries with i - j > kl or
+// j - i > ku are zero and stay zero under no-pivot LU (Golub & Van Loan
+// Thm 4.3.1), so the panel, U12 and the update are clipped to the band —
+// the skipped operations of the dense algorithm are exact no-ops on zeros
+// (fma(-0, u, +0) == +0), so the factors inside the band are bitwise the
+// dense ones.  kl = ku = n - 1 is the dense schedule.
+cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s,
+                       int64_t kl, int64_t ku) {
+  if (kl < 0 || kl > n) kl = n;
+  if (ku < 0 || ku > n) ku = n;
+  // narrow bands: 64-wide panels (the per-step windows are ~band-sized;
+  // measured n = 65536, kl = ku = 256: 61.8 ms at nb = 64, 98.9 at 512)
+  const bool narrow = c->nb <= 0 && kl + ku < n / 4;
+  const int64_t nb = narrow ? ((64 + c->leaf - 1) / c->leaf) * c->leaf : block_width(c, n);
+  auto step_w = [&](int64_t c0) { return narrow ? ((n - c0) < nb ? (n - c0) : nb) : step_width(c, n, c0); };
   const bool la = c->lookahead && n > 2 * nb;
   cudaError_t e = cudaSuccess;
   if (la) {
@@ -236,10 +249,14 @@ cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_
     if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_start, 0);
     if (e != cudaSuccess) return e;
   }
-  e = panel_rec(c, n, step_width(c, n, 0), A, lda, 0, info, s);
-  if (e != cudaSuccess) return e;
+  auto clip = [](int64_t a, int64_t b) { return a < b ? a : b; };
+  {
+    const int64_t w0 = step_w(0);
+    e = panel_rec(c, clip(n, w0 + kl), w0, A, lda, 0, info, s);
+    if (e != cudaSuccess) return e;
+  }
   for (int64_t c0 = 0, w = 0; c0 < n; c0 += w) {
-    w = step_width(c, n, c0);
+    w = step_w(c0);
     double* P = A + c0 + c0 * lda;
     const int64_t rest = n - c0 - w;
     if (rest <= 0) break;
@@ -247,34 +264,36 @@ cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_
       e = cudaStreamWaitEvent(s, c->ev_p, 0);
       if (e != cudaSuccess) return e;
     }
-    const int64_t w1 = step_width(c, n, c0 + w);     // width of panel K+1
+    const int64_t Mb = clip(rest, kl), Nbw = clip(rest, ku);   // nonzero L21 rows / U12 columns
+    const int64_t w1 = step_w(c0 + w);              // width of panel K+1
+    const int64_t Mp1 = clip(rest, w1 + kl);         // its rows that can be nonzero
     double* P1 = P + w + w * lda;
-    if (la && rest > w1) {
+    if (la && Nbw > w1) {
       // lookahead: the update of panel K+1's columns first, then factor it on
       // the side stream while the rest of the trailing matrix is updated.
       // For large n U12 is split too, so panel K+1 need not wait for all of
       // U12 (columns are independent: same bits).
       const bool split = kU12SplitRows >= 0 ? rest < kU12SplitRows : n >= 16384;
-      e = trsm_l(c, w, split ? w1 : rest, P, lda, P + w * lda, lda, s);
-      if (e == cudaSuccess) e = gemm(c, rest, w1, w, P + w, lda, P + w * lda, lda, P1, lda, false, s, KC_UPDATE);
+      e = trsm_l(c, w, split ? w1 : Nbw, P, lda, P + w * lda, lda, s);
+      if (e == cudaSuccess) e = gemm(c, Mb, w1, w, P + w, lda, P + w * lda, lda, P1, lda, false, s, KC_UPDATE);
       if (e == cudaSuccess) e = cudaEventRecord(c->ev_a, s);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_a, 0);
-      if (e == cudaSuccess) e = panel_rec(c, rest, w1, P1, lda, c0 + w, info, c->side);
+      if (e == cudaSuccess) e = panel_rec(c, Mp1, w1, P1, lda, c0 + w, info, c->side);
       if (e == cudaSuccess) e = cudaEventRecord(c->ev_p, c->side);
-      if (e == cudaSuccess && split) e = trsm_l(c, w, rest - w1, P, lda, P + (w + w1) * lda, lda, s);
+      if (e == cudaSuccess && split) e = trsm_l(c, w, Nbw - w1, P, lda, P + (w + w1) * lda, lda, s);
       if (e == cudaSuccess)
-        e = gemm(c, rest, rest - w1, w, P + w, lda, P + (w + w1) * lda, lda, P1 + w1 * lda, lda, false, s, KC_UPDATE);
+        e = gemm(c, Mb, Nbw - w1, w, P + w, lda, P + (w + w1) * lda, lda, P1 + w1 * lda, lda, false, s, KC_UPDATE);
       if (e != cudaSuccess) return e;
     } else {
-      e = trsm_l(c, w, rest, P, lda, P + w * lda, lda, s);
+      e = trsm_l(c, w, Nbw, P, lda, P + w * lda, lda, s);
       if (e != cudaSuccess) return e;
-      e = gemm(c, rest, rest, w, P + w, lda, P + w * lda, lda, P1, lda, false, s, KC_UPDATE);
+      e = gemm(c, Mb, Nbw, w, P + w, lda, P + w * lda, lda, P1, lda, false, s, KC_UPDATE);
       if (e != cudaSuccess) return e;
       if (la) {   // keep the event protocol: the next panel is factored in order
-        e = panel_rec(c, rest, w1, P1, lda, c0 + w, info, s);
+        e = panel_rec(c, Mp1, w1, P1, lda, c0 + w, info, s);
         if (e == cudaSuccess) e = cudaEventRecord(c->ev_p, s);
       } else {
-        e = panel_rec(c, rest, w1, P1, lda, c0 + w, info, s);
+        e = panel_rec(c, Mp1, w1, P1, lda, c0 + w, info, s);
       }
       if (e != cudaSuccess) return e;
     }
@@ -601,7 +620,7 @@ static ebv_status_t factor_body(ebv_context_t c, int64_t n, double* A, int64_t l
     if (e != cudaSuccess) return cuda_fail(e, "left-looking factor");
     return EBV_SUCCESS;
   }
-  e = (c->nb != -1) ? lu_blocked(c, n, A, lda, d_info, s) : lu_rec(c, n, A, lda, 0, d_info, s);
+  e = (c->nb != -1) ? lu_blocked(c, n, A, lda, d_info, s, n, n) : lu_rec(c, n, A, lda, 0, d_info, s);
   if (e != cudaSuccess) return cuda_fail(e, "blocked factor");
   return EBV_SUCCESS;
 }
@@ -661,6 +680,48 @@ ebv_status_t ebv_lu_solve(ebv_context_t c, int64_t n, const double* LU, int64_t 
     return launch_solve(n, LU, lda, B, ldb, nrhs, c->d_ticket, c->d_flags, c->solve_epoch, s);
   });
   if (e != cudaSuccess) return cuda_fail(e, "solve");
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_lu_factor_banded(ebv_context_t c, int64_t n, int64_t kl, int64_t ku, double* A, int64_t lda,
+                                  double tau, int64_t* d_info, void* stream) {
+  if (!c) return invalid("ebv_lu_factor_banded: NULL ctx");
+  if (n < 0 || kl < 0 || ku < 0) return invalid("ebv_lu_factor_banded: negative size");
+  if (lda < (n > 1 ? n : 1)) return invalid("ebv_lu_factor_banded: lda < max(1, n)");
+  if (!d_info) return invalid("ebv_lu_factor_banded: d_info is NULL");
+  if (n > 0 && !A) return invalid("ebv_lu_factor_banded: A is NULL");
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = timed(c, KC_OTHER, 0, 0, s, 1, [&] { return launch_set_info0(d_info, s); });
+  if (e != cudaSuccess) return cuda_fail(e, "info init");
+  if (n == 0) return EBV_SUCCESS;
+  e = timed(c, KC_OTHER, 0, 8.0 * n * n, s, tau < 0 ? 3 : 1,
+            [&] { return launch_tau(n, A, lda, tau, c->d_tau, c->d_norm, s); });
+  if (e != cudaSuccess) return cuda_fail(e, "tau");
+  e = (c->nb != -1) ? lu_blocked(c, n, A, lda, d_info, s, kl, ku) : lu_rec(c, n, A, lda, 0, d_info, s);
+  if (e != cudaSuccess) return cuda_fail(e, "banded factor");
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_lu_solve_banded(ebv_context_t c, int64_t n, int64_t kl, int64_t ku, const double* LU, int64_t lda,
+                                 double* B, int64_t ldb, int64_t nrhs, void* stream) {
+  if (!c) return invalid("ebv_lu_solve_banded: NULL ctx");
+  if (n < 0 || nrhs < 0 || kl < 0 || ku < 0) return invalid("ebv_lu_solve_banded: negative size");
+  if (lda < (n > 1 ? n : 1) || ldb < (n > 1 ? n : 1)) return invalid("ebv_lu_solve_banded: leading dimension");
+  if (n == 0 || nrhs == 0) return EBV_SUCCESS;
+  if (!LU || !B) return invalid("ebv_lu_solve_banded: NULL pointer");
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t NB = (n + solve_block_rows() - 1) / solve_block_rows();
+  ebv_status_t st = ensure_flags(c, 2 * NB * solve_max_interleave());
+  if (st != EBV_SUCCESS) return st;
+  c->solve_epoch++;
+  const int64_t groups = (nrhs + 63) / 64;
+  const double bw = (double)(kl + ku + 1) < n ? (double)(kl + ku + 1) : (double)n;
+  cudaError_t e = timed(c, KC_SOLVE, 2.0 * n * bw * nrhs, 8.0 * n * bw + 32.0 * n * nrhs, s, (int)(2 * groups), [&] {
+    return launch_solve(n, LU, lda, B, ldb, nrhs, c->d_ticket, c->d_flags, c->solve_epoch, s, kl, ku);
+  });
+  if (e != cudaSuccess) return cuda_fail(e, "banded solve");
   return EBV_SUCCESS;
 }
 

@@ -66,7 +66,8 @@ cudaError_t launch_normalize_unit_diagonal(int64_t n, double* A, int64_t lda, do
 cudaError_t launch_lu_to_ldu(int64_t n, double* LU, int64_t lda, double* D, cudaStream_t s, int64_t* launches);
 int64_t solve_max_interleave();
 cudaError_t launch_solve(int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb, int64_t nrhs,
-                         int* ticket_ws, int* flags_ws, int64_t epoch, cudaStream_t s);
+                         int* ticket_ws, int* flags_ws, int64_t epoch, cudaStream_t s,
+                         int64_t kl = -1, int64_t ku = -1);
 int64_t solve_block_rows();
 
 // Batched n <= 32 fused factor + solve.

@@ -109,7 +109,8 @@ cudaError_t trsm_lu(ebv_context* c, int64_t k, int64_t m, const double* U, int64
 cudaError_t lu_rec(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t koff, int64_t* info, cudaStream_t s);
 cudaError_t panel_rec(ebv_context* c, int64_t M, int64_t w, double* P, int64_t lda, int64_t koff, int64_t* info,
                       cudaStream_t s);
-cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s);
+cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s,
+                       int64_t kl, int64_t ku);
 cudaError_t lu_left(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s,
                     const double* hA, int64_t ldh);
 void dist_release(ebv_context* c);   // ebv_dist.cu

@@ -106,7 +106,8 @@ __device__ __forceinline__ double quot(double y, double u, double r, bool own, b
 template <bool FORWARD, int NR>
 __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __restrict__ LU, int64_t lda,
                                                    double* B0, int64_t ldb, int nrhs, int* ticket, int* flags0,
-                                                   int epoch, int64_t jlo, int64_t jhi, int64_t cbase, int nind) {
+                                                   int epoch, int64_t jlo, int64_t jhi, int64_t cbase, int nind,
+                                                   int64_t kl, int64_t ku) {
   __shared__ double sd[BR * TSTR];          // diagonal tile: sd[c*TSTR + r] = LU(I*BR + r, I*BR + c)
   constexpr int SR = NR > 0 ? NR : MAXR;    // shared stride per row (right-hand sides)
   __shared__ double sbuf[BR * SR];          // published values of block J (sy[k*SR + r]),
@@ -147,9 +148,18 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
 #pragma unroll
     for (int r = 0; r < MAXR; r++) acc[r] = (rv && r < nr) ? B[row + (int64_t)r * ldb] : 0.0;
 
-    const int64_t nJ = FORWARD ? (I < jhi ? I : jhi) - jlo : jhi - (I + 1 > jlo ? I + 1 : jlo);
+    // banded factors (kl / ku): tiles outside the band are exact zeros and
+    // are skipped (fma(-0, y, acc) == acc)
+    int64_t jf = jlo, jt = jhi;
+    if (FORWARD && I * BR > kl) jf = (I * BR - kl) / BR > jlo ? (I * BR - kl) / BR : jlo;
+    if (!FORWARD) {
+      const int64_t top = (I * BR + BR - 1 + ku) / BR + 1;
+      jt = top < jhi ? top : jhi;
+    }
+    int64_t nJ = FORWARD ? (I < jhi ? I : jhi) - jf : jt - (I + 1 > jlo ? I + 1 : jlo);
+    if (nJ < 0) nJ = 0;
     for (int64_t jj = 0; jj < nJ; jj++) {
-      const int64_t J = FORWARD ? jlo + jj : jhi - 1 - jj;
+      const int64_t J = FORWARD ? jf + jj : jt - 1 - jj;
       // this thread's row segment of tile (I, J): issued before the wait
       double l[BR];
       const double* src = LU + (rv ? row : 0) + (J * BR - cbase) * lda;
@@ -352,11 +362,13 @@ int64_t resident_grid(int64_t units, K kern) {
 template <bool FWD>
 cudaError_t launch_one(int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb, int nr, int* ticket,
                        int* flags, int ep, int64_t units, cudaStream_t s, int64_t jlo, int64_t jhi, int64_t cbase,
-                       int nind) {
+                       int nind, int64_t kl = -1, int64_t ku = -1) {
   if (nr != 1) return cudaErrorInvalidValue;
+  if (kl < 0) kl = n;
+  if (ku < 0) ku = n;
   const int64_t grid = resident_grid(units * nind, solve_kernel<FWD, 1>);
   solve_kernel<FWD, 1><<<(unsigned)grid, BR, 0, s>>>(n, LU, lda, B, ldb, nr, ticket, flags, ep, jlo, jhi, cbase,
-                                                     nind);
+                                                     nind, kl, ku);
   return cudaGetLastError();
 }
 
@@ -365,7 +377,7 @@ cudaError_t launch_one(int64_t n, const double* LU, int64_t lda, double* B, int6
 int64_t solve_block_rows() { return BR; }
 
 cudaError_t launch_solve(int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb, int64_t nrhs,
-                         int* ticket_ws, int* flags_ws, int64_t epoch, cudaStream_t s) {
+                         int* ticket_ws, int* flags_ws, int64_t epoch, cudaStream_t s, int64_t kl, int64_t ku) {
   if (n <= 0 || nrhs <= 0) return cudaSuccess;
   const int64_t NB = (n + BR - 1) / BR;
   // the columns as interleaved single-column chains, up to kMaxInterleave
@@ -378,9 +390,10 @@ cudaError_t launch_solve(int64_t n, const double* LU, int64_t lda, double* B, in
       const int ep = (int)(((epoch * 64 + (g0 / kMaxInterleave) * 2 + pass) % 0x3FFFFFFF) + 1);
       cudaError_t e = cudaMemsetAsync(ticket_ws + pass, 0, sizeof(int), s);
       if (e != cudaSuccess) return e;
-      e = fwd ? launch_one<true>(n, LU, lda, B + g0 * ldb, ldb, 1, ticket_ws, flags_ws, ep, NB, s, 0, NB, 0, nind)
+      e = fwd ? launch_one<true>(n, LU, lda, B + g0 * ldb, ldb, 1, ticket_ws, flags_ws, ep, NB, s, 0, NB, 0, nind, kl,
+                                 ku)
               : launch_one<false>(n, LU, lda, B + g0 * ldb, ldb, 1, ticket_ws + 1, flags_ws + (int64_t)nind * NB, ep,
-                                  NB, s, 0, NB, 0, nind);
+                                  NB, s, 0, NB, 0, nind, kl, ku);
       if (e != cudaSuccess) return e;
     }
   }

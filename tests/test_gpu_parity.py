@@ -259,6 +259,26 @@ def test_factor_host_bitwise(dev, ctx, n, pinned, tau):
     assert bits_eq(LU.cpu().numpy(), lu_o)
 
 
+# ------------------------------------------------------------------ f4: banded / stencil (zero-skip)
+@pytest.mark.parametrize("n,kl,ku,stencil", [(700, 30, 50, 0), (1537, 200, 64, 0), (3000, 1, 600, 0),
+                                             (64 * 64, 64, 64, 64), (5, 1, 1, 0), (1000, 0, 0, 0)])
+def test_banded_bitwise(dev, ctx, n, kl, ku, stencil):
+    """Zero-skip banded factor + solve equal the dense oracle bitwise (the
+    band is preserved; entries outside it stay exactly zero)."""
+    if stencil:
+        d = ebv_inputs.generate(n, seed=n, nrhs=2, device=dev, stencil_m=stencil)
+    else:
+        d = ebv_inputs.generate(n, seed=n + kl, nrhs=2, device=dev, kl=kl, ku=ku)
+    A = d["At"].T
+    LU, info = ebv.lu_factor_banded(A, kl, ku, ctx=ctx)
+    X = ebv.lu_solve_banded(LU, d["B"], kl, ku, ctx=ctx)
+    torch.cuda.synchronize()
+    lu_o, info_o = oracle.lu_factor(A.cpu().numpy())
+    assert int(info) == info_o == 0
+    assert bits_eq(LU.cpu().numpy(), lu_o)
+    assert bits_eq(X.cpu().numpy(), oracle.lu_solve(lu_o, d["B"].cpu().numpy()))
+
+
 # ------------------------------------------------------------------ f3: unit diagonal, LDU
 @pytest.mark.parametrize("n,nrhs", [(1, 1), (2, 0), (300, 3), (1537, 1)])
 def test_normalize_unit_diagonal_bitwise(dev, ctx, n, nrhs):
