@@ -3,7 +3,8 @@
  * path of the "Equal bi-Vectorized" (EbV) method, arXiv 1907.05767.
  *
  * Citations: P:<line> = PAPER.md (the paper text), DESIGN.md = this repo's
- * design notes (readings R1..R16 of the garbled passages).
+ * design notes (readings R1..R17 of the garbled passages), SURVEY §8 = the
+ * scope table (rows A1-A13 and the "next" rows f1-f4).
  *
  * The problem statement followed by every call (Eq 1):
  *     AX = B  <=>  (LU)X = B  <=>  L(UX) = B  <=>  LY = B, then UX = Y.
@@ -23,8 +24,9 @@
  *     factorization is packed in place: strict lower triangle = L multipliers
  *     (unit diagonal implicit), diagonal + upper triangle = U.
  *   - All matrix / vector / info pointers are DEVICE pointers owned by the
- *     caller; the library never frees them.  The library owns only its
- *     context (workspace, streams, events).
+ *     caller (except the host matrix of ebv_lu_factor_host); the library
+ *     never frees them.  The library owns only its context (workspace,
+ *     streams, events, NCCL communicator).
  *   - Calls are asynchronous on the caller's `stream` (a cudaStream_t passed
  *     as void*; NULL = legacy default stream).  The library never
  *     synchronizes the caller's stream.
@@ -55,7 +57,7 @@ typedef enum {
                                  callers that map a nonzero info word        */
   EBV_ERR_CUDA = 3,           /* a CUDA runtime error (see ebv_last_error)    */
   EBV_ERR_NCCL = 4,           /* reserved for the multi-GPU context           */
-  EBV_ERR_NOT_SUPPORTED = 5,  /* valid but unsupported (e.g. batched n > 32)  */
+  EBV_ERR_NOT_SUPPORTED = 5,  /* valid but unsupported (e.g. batched n > 64)  */
   EBV_ERR_ALLOC = 6           /* workspace allocation failed                  */
 } ebv_status_t;
 
