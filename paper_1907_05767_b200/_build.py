@@ -15,7 +15,7 @@ LIB = os.path.join(HERE, "libebv.so")
 OBJ = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo",
-         "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"]
+         "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"] + os.environ.get("EBV_EXTRA_NVCC_FLAGS", "").split()
 
 
 def nccl_include() -> str:

@@ -45,28 +45,30 @@ constexpr int Q = W / G;      // entries per lane
 // row i > k forms l_ik = a_ik / u_kk (Eq 6-a, owner lane), broadcasts it in
 // the group and updates its row (Eq 6-c).  A narrower block is identity
 // padded (exactly neutral).
-__global__ void __launch_bounds__(W * G) leaf_lu_kernel(int w, double* __restrict__ A, int64_t lda,
+template <int GD>
+__global__ void __launch_bounds__(W * GD) leaf_lu_kernel(int w, double* __restrict__ A, int64_t lda,
                                                         const double* __restrict__ tau, int64_t* info, int64_t koff) {
+  constexpr int QD = W / GD;
   __shared__ __align__(16) double urow[2][2 * W];
   __shared__ int smin;
-  const int tid = threadIdx.x, i = tid / G, j = tid % G, lane = tid & 31, base = lane & ~(G - 1);
-  double a[Q];
+  const int tid = threadIdx.x, i = tid / GD, j = tid % GD, lane = tid & 31, base = lane & ~(GD - 1);
+  double a[QD];
 #pragma unroll
-  for (int q = 0; q < Q; q++) {
-    const int c = j + G * q;
+  for (int q = 0; q < QD; q++) {
+    const int c = j + GD * q;
     a[q] = (i < w && c < w) ? A[i + (int64_t)c * lda] : (i == c ? 1.0 : 0.0);
   }
   if (tid == 0) smin = 0x7fffffff;
   const double tv = *tau;
 #pragma unroll 1
-  for (int qk = 0; qk < Q; qk++) {
+  for (int qk = 0; qk < QD; qk++) {
 #pragma unroll
-    for (int o = 0; o < G; o++) {
-      const int k = qk * G + o;
-      double* ur = urow[o & 1] + G * qk;           // ur[j + G*q] = u(k, j + G*(q + qk))
+    for (int o = 0; o < GD; o++) {
+      const int k = qk * GD + o;
+      double* ur = urow[o & 1] + GD * qk;           // ur[j + GD*q] = u(k, j + GD*(q + qk))
       if (i == k) {
 #pragma unroll
-        for (int q = 0; q < Q; q++) ur[j + G * q] = a[q];
+        for (int q = 0; q < QD; q++) ur[j + GD * q] = a[q];
       }
       __syncthreads();
       const double piv = ur[o];
@@ -76,14 +78,14 @@ __global__ void __launch_bounds__(W * G) leaf_lu_kernel(int w, double* __restric
       if (i > k) {
         if (j > o) a[0] = fma(-l, ur[j], a[0]);                      // Eq 6-c
 #pragma unroll
-        for (int q = 1; q < Q; q++) a[q] = fma(-l, ur[j + G * q], a[q]);
+        for (int q = 1; q < QD; q++) a[q] = fma(-l, ur[j + GD * q], a[q]);
       }
     }
-    const int c = j + G * qk;                        // final: store, rotate
+    const int c = j + GD * qk;                        // final: store, rotate
     if (i < w && c < w) A[i + (int64_t)c * lda] = a[0];
 #pragma unroll
-    for (int q = 0; q < Q - 1; q++) a[q] = a[q + 1];
-    a[Q - 1] = 0.0;
+    for (int q = 0; q < QD - 1; q++) a[q] = a[q + 1];
+    a[QD - 1] = 0.0;
   }
   __syncthreads();
   if (tid == 0 && smin != 0x7fffffff) {
@@ -125,6 +127,10 @@ __device__ __forceinline__ double quot_v(double y, double u, double r, bool& ok)
 // Each block of 8 steps is checkpointed; if any quotient of the block is
 // unverified the warp redoes that block with true division.
 constexpr int RR = 2;
+#ifndef EBV_LEAF_G
+#define EBV_LEAF_G 4
+#endif
+constexpr int kLeafG = EBV_LEAF_G;   // lanes per row in the diagonal-block kernels
 
 __global__ void __launch_bounds__(256, 2) trsm_ru_kernel(int64_t m, int k, double* __restrict__ X, int64_t ldx,
                                                          const double* __restrict__ U, int64_t ldu) {
@@ -216,18 +222,20 @@ __global__ void __launch_bounds__(256, 2) trsm_ru_kernel(int64_t m, int k, doubl
 // its 64 rows below with the trsm_ru scheme (verified reciprocal quotients).
 constexpr int US = 2 * W;     // shared U row stride (covers the rotation overrun)
 
-__global__ void __launch_bounds__(W * G) panel_leaf_kernel(int64_t M, int w, double* __restrict__ P, int64_t lda,
+template <int GD>
+__global__ void __launch_bounds__(W * GD) panel_leaf_kernel(int64_t M, int w, double* __restrict__ P, int64_t lda,
                                                            const double* __restrict__ tau, int64_t* info,
                                                            int64_t koff, int* count) {
+  constexpr int QD = W / GD;
   extern __shared__ __align__(16) double sUp[];    // [W][US]: sUp[k*US + c] = u(k, c)
   __shared__ double srcp[W];
   __shared__ int smin, slast;
-  const int tid = threadIdx.x, i = tid / G, j = tid % G, lane = tid & 31, base = lane & ~(G - 1);
-  for (int idx = tid; idx < W * US; idx += W * G) sUp[idx] = 0.0;
-  double a[Q];
+  const int tid = threadIdx.x, i = tid / GD, j = tid % GD, lane = tid & 31, base = lane & ~(GD - 1);
+  for (int idx = tid; idx < W * US; idx += W * GD) sUp[idx] = 0.0;
+  double a[QD];
 #pragma unroll
-  for (int q = 0; q < Q; q++) {
-    const int c = j + G * q;
+  for (int q = 0; q < QD; q++) {
+    const int c = j + GD * q;
     a[q] = (i < w && c < w) ? P[i + (int64_t)c * lda] : (i == c ? 1.0 : 0.0);
   }
   if (tid == 0) smin = 0x7fffffff;
@@ -246,14 +254,14 @@ __global__ void __launch_bounds__(W * G) panel_leaf_kernel(int64_t M, int w, dou
   const bool store = slast != 0;
   // ---- diagonal block (leaf_lu, publishing into the full U copy)
 #pragma unroll 1
-  for (int qk = 0; qk < Q; qk++) {
+  for (int qk = 0; qk < QD; qk++) {
 #pragma unroll
-    for (int o = 0; o < G; o++) {
-      const int k = qk * G + o;
-      double* ur = sUp + k * US + G * qk;           // ur[j + G*q] = u(k, j + G*(q + qk))
+    for (int o = 0; o < GD; o++) {
+      const int k = qk * GD + o;
+      double* ur = sUp + k * US + GD * qk;           // ur[j + GD*q] = u(k, j + GD*(q + qk))
       if (i == k) {
 #pragma unroll
-        for (int q = 0; q < Q; q++) ur[j + G * q] = a[q];
+        for (int q = 0; q < QD; q++) ur[j + GD * q] = a[q];
       }
       __syncthreads();
       const double piv = ur[o];
@@ -263,14 +271,14 @@ __global__ void __launch_bounds__(W * G) panel_leaf_kernel(int64_t M, int w, dou
       if (i > k) {
         if (j > o) a[0] = fma(-l, ur[j], a[0]);                      // Eq 6-c
 #pragma unroll
-        for (int q = 1; q < Q; q++) a[q] = fma(-l, ur[j + G * q], a[q]);
+        for (int q = 1; q < QD; q++) a[q] = fma(-l, ur[j + GD * q], a[q]);
       }
     }
-    const int c = j + G * qk;
+    const int c = j + GD * qk;
     if (store && i < w && c < w) P[i + (int64_t)c * lda] = a[0];
 #pragma unroll
-    for (int q = 0; q < Q - 1; q++) a[q] = a[q + 1];
-    a[Q - 1] = 0.0;
+    for (int q = 0; q < QD - 1; q++) a[q] = a[q + 1];
+    a[QD - 1] = 0.0;
   }
   __syncthreads();
   if (store && tid == 0 && smin != 0x7fffffff) {
@@ -283,35 +291,35 @@ __global__ void __launch_bounds__(W * G) panel_leaf_kernel(int64_t M, int w, dou
   // ---- rows below (trsm_ru): this CTA's 64 rows, a group of 8 lanes each
   const int64_t r = (int64_t)w + (int64_t)blockIdx.x * W + i;
   const bool rv = r < M;
-  double x0[Q];
+  double x0[QD];
 #pragma unroll
-  for (int q = 0; q < Q; q++) {
-    const int c = j + G * q;
+  for (int q = 0; q < QD; q++) {
+    const int c = j + GD * q;
     x0[q] = (rv && c < w) ? P[r + (int64_t)c * lda] : 0.0;
   }
   for (int pass = 0; pass < 2; pass++) {
     const bool exact = pass == 1;
     bool ok = true;
-    double x[Q];
+    double x[QD];
 #pragma unroll
-    for (int q = 0; q < Q; q++) x[q] = x0[q];
+    for (int q = 0; q < QD; q++) x[q] = x0[q];
 #pragma unroll 1
-    for (int qk = 0; qk < Q; qk++) {
+    for (int qk = 0; qk < QD; qk++) {
 #pragma unroll
-      for (int o = 0; o < G; o++) {
-        const int p = qk * G + o;
-        const double* up = sUp + p * US + G * qk;
+      for (int o = 0; o < GD; o++) {
+        const int p = qk * GD + o;
+        const double* up = sUp + p * US + GD * qk;
         if (j == o) x[0] = exact ? x[0] / up[o] : quot_v(x[0], up[o], srcp[p], ok);
         const double xp = __shfl_sync(0xffffffffu, x[0], base + o);
         if (j > o) x[0] = fma(-xp, up[j], x[0]);
 #pragma unroll
-        for (int q = 1; q < Q; q++) x[q] = fma(-xp, up[j + G * q], x[q]);
+        for (int q = 1; q < QD; q++) x[q] = fma(-xp, up[j + GD * q], x[q]);
       }
-      const int c = j + G * qk;
+      const int c = j + GD * qk;
       if (rv && c < w) P[r + (int64_t)c * lda] = x[0];
 #pragma unroll
-      for (int q = 0; q < Q - 1; q++) x[q] = x[q + 1];
-      x[Q - 1] = 0.0;
+      for (int q = 0; q < QD - 1; q++) x[q] = x[q + 1];
+      x[QD - 1] = 0.0;
     }
     if (!__any_sync(0xffffffffu, !ok)) break;
   }
@@ -401,7 +409,7 @@ cudaError_t launch_leaf_lu(int64_t n, double* A, int64_t lda, const double* tau,
                            cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   if (n > W) return cudaErrorInvalidValue;
-  leaf_lu_kernel<<<1, W * G, 0, s>>>((int)n, A, lda, tau, info, koff);
+  leaf_lu_kernel<kLeafG><<<1, W * kLeafG, 0, s>>>((int)n, A, lda, tau, info, koff);
   return cudaGetLastError();
 }
 
@@ -412,12 +420,13 @@ cudaError_t launch_panel_leaf(int64_t M, int64_t w, double* P, int64_t lda, cons
   const size_t smem = (size_t)W * US * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(panel_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(panel_leaf_kernel<kLeafG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int64_t grid = M > w ? (M - w + W - 1) / W : 1;
-  panel_leaf_kernel<<<(unsigned)grid, W * G, smem, s>>>(M, (int)w, P, lda, tau, info, koff, count);
+  panel_leaf_kernel<kLeafG><<<(unsigned)grid, W * kLeafG, smem, s>>>(M, (int)w, P, lda, tau, info, koff, count);
   return cudaGetLastError();
 }
 
