@@ -501,3 +501,34 @@ def test_graph_replay_bitwise(dev, ctx):
             assert bits_eq(Aw.T.cpu().numpy(), lu_o), rep
             assert int(info) == 0
     assert counts[0] == counts[2] == counts[3] > 10
+
+
+# ------------------------------------------------------------------ randomized schedule stress
+_RNG_CASES = []
+_rs = np.random.default_rng(20261018)
+for _ in range(14):
+    _n = int(_rs.integers(1, 1400))
+    _RNG_CASES.append((_n, int(_rs.choice([0, 64, 128, 192, 256, -1])), int(_rs.choice([8, 16, 32, 64])),
+                       int(_rs.choice([ebv.EBV_PATH_BLOCKED, ebv.EBV_PATH_LEFT])), bool(_rs.integers(0, 2)),
+                       int(_rs.integers(1, 70))))
+
+
+@pytest.mark.parametrize("n,nb,leaf,path,la,nrhs", _RNG_CASES)
+def test_random_schedules_bitwise(dev, n, nb, leaf, path, la, nrhs):
+    """Random sizes x block widths x leaf sizes x schedules x lookahead x
+    right-hand-side counts: factors and solutions bitwise the oracle's."""
+    c = ebv.Context(0, path=path)
+    c.set_leaf(leaf)
+    if nb > 0:
+        nb = max(leaf, (nb // leaf) * leaf)
+    c.set_block(nb if path == ebv.EBV_PATH_BLOCKED or nb >= 0 else 0)
+    c.set_lookahead(la)
+    d = ebv_inputs.generate(n, seed=n * 7 + nrhs, nrhs=nrhs, device=dev)
+    A = d["At"].T
+    LU, info = ebv.lu_factor(A, ctx=c)
+    X = ebv.lu_solve(LU, d["B"], ctx=c)
+    torch.cuda.synchronize()
+    lu_o, info_o = oracle.lu_factor(A.cpu().numpy())
+    assert int(info) == info_o == 0
+    assert bits_eq(LU.cpu().numpy(), lu_o)
+    assert bits_eq(X.cpu().numpy(), oracle.lu_solve(lu_o, d["B"].cpu().numpy()))
