@@ -398,6 +398,28 @@ def run_ebv(args, rank, world, local):
                "h2d_bytes_per_step": int(hA.numel() * 8 + hB.numel() * 8), "d2h_bytes_per_step": int(hX.numel() * 8),
                "ms_per_step": ems / ksteps, "steps": ksteps, "correct": bool(e2e_ok),
                "pipelined": "next step's H2D on a copy stream under the current step's factor"}
+        if not use_dist:
+            # one system from host memory through ebv_lu_factor_host (the
+            # matrix streams in block by block under the factorization):
+            # single-system latency, no cross-step overlap
+            def host_step():
+                Bw.copy_(hB, non_blocking=True)
+                st = ebv.ebv_lu_factor_host(ctx.handle, n, hA.data_ptr(), n, Aw.data_ptr(), n, 0.0, info.data_ptr(),
+                                            sh)
+                st |= ebv.ebv_lu_solve(ctx.handle, n, Aw.data_ptr(), n, Bw.data_ptr(), n, nrhs, sh)
+                hX.copy_(Bw, non_blocking=True)
+                if st:
+                    raise RuntimeError(ebv.ebv_last_error())
+            host_step()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            host_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            hms = e0.elapsed_time(e1)
+            e2e["single_system"] = {"api": "ebv_lu_factor_host + ebv_lu_solve", "ms": hms,
+                                    "value": fl / (hms / 1e3) / 1e9,
+                                    "correct": bool((hX.T - Xtrue.cpu()).abs().max().item() <= 1e-10)}
         del hA, hB, hX, Aw2, Bw2
 
     out = None

@@ -160,6 +160,9 @@ static int64_t kU12SplitRows = [] {
   return e ? (int64_t)atoll(e) : (int64_t)-1;   // -1: split for n >= 16384 (same-box A/B:
 }();                                              // n = 32768 -0.3%, n = 8192 +3% if split)
 
+// streamed host factor plan: PCIe copy rate and DMMA update rate (B200)
+static const double kHostCopyBps = 55e9, kUpdateFlops = 33e12;
+
 static int64_t kTailRows = [] {
   const char* e = getenv("EBV_TAIL_ROWS");
   return e ? (int64_t)atoll(e) : (int64_t)0;
@@ -299,6 +302,126 @@ cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_
     }
   }
   if (la) {   // the caller's stream sees the last side-stream work
+    e = cudaEventRecord(c->ev_p, c->side);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, c->ev_p, 0);
+  }
+  return e;
+}
+
+// Right-looking schedule over a HOST-resident matrix (ebv_lu_factor_host):
+// the column blocks are copied in order on a copy stream, and block J
+// joins the right-looking updates at step K_J — planned from the copy rate
+// and the update flop rate so that it has arrived by then — after a
+// catch-up that applies steps 0..K_J-1 to it in order (trsm with each
+// panel's L11, then its DMMA update): per entry the same operation sequence
+// as lu_blocked, bitwise.  Until then the steps' updates cover only the
+// blocks already joined, so the transfer overlaps the first steps' work.
+// A block that arrives later than planned only stalls the stream (its
+// catch-up waits on its copy event); correctness never depends on timing.
+cudaError_t lu_blocked_stream(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s,
+                              const double* hA, int64_t ldh) {
+  const int64_t nb = block_width(c, n);
+  const int64_t N = (n + nb - 1) / nb;
+  auto wid = [&](int64_t J) { return (J + 1) * nb <= n ? nb : n - J * nb; };
+  cudaError_t e = cudaSuccess;
+  if (!c->copy) {
+    e = cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return e;
+  }
+  while ((int64_t)c->copy_ev.size() < N) {
+    cudaEvent_t ev = nullptr;
+    e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+    c->copy_ev.push_back(ev);
+  }
+  e = cudaEventRecord(c->ev_start, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(c->copy, c->ev_start, 0);
+  for (int64_t J = 0; J < N && e == cudaSuccess; J++) {
+    e = cudaMemcpy2DAsync(A + J * nb * lda, lda * sizeof(double), hA + J * nb * ldh, ldh * sizeof(double),
+                          n * sizeof(double), wid(J), cudaMemcpyHostToDevice, c->copy);
+    if (e == cudaSuccess) e = cudaEventRecord(c->copy_ev[J], c->copy);
+  }
+  if (e != cudaSuccess) return e;
+  // join plan: block J (copied by ~ (J+1) * t_copy) joins at the first step
+  // whose start (cumulative update time) is later; never after step J-1
+  const double t_copy = (double)n * nb * 8.0 / kHostCopyBps, rate = kUpdateFlops;
+  std::vector<int64_t> join(N, 0);
+  {
+    std::vector<double> T(N + 1, 0.0);
+    for (int64_t k = 0; k < N; k++) {
+      const double rest = (double)(n - (k + 1) * nb);
+      T[k + 1] = T[k] + (rest > 0 ? 2.0 * rest * rest * nb / rate : 0.0);
+    }
+    for (int64_t J = 2; J < N; J++) {
+      int64_t K = 0;
+      while (K < J - 1 && T[K] < (double)(J + 1) * t_copy) K++;
+      join[J] = K < join[J - 1] ? join[J - 1] : K;   // nondecreasing: joined blocks form a prefix
+    }
+  }
+  const bool la = c->lookahead && n > 2 * nb;
+  if (la) {
+    e = cudaEventRecord(c->ev_start, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_start, 0);
+    if (e != cudaSuccess) return e;
+  }
+  e = cudaStreamWaitEvent(s, c->copy_ev[0], 0);
+  if (e == cudaSuccess) e = panel_rec(c, n, wid(0), A, lda, 0, info, s);
+  if (e != cudaSuccess) return e;
+  int64_t joined = N > 1 ? 2 : 1;                     // blocks [0, joined) take part in the updates
+  for (int64_t J = 1; J < joined; J++) {
+    e = cudaStreamWaitEvent(s, c->copy_ev[J], 0);
+    if (e != cudaSuccess) return e;
+  }
+  for (int64_t K = 0; K + 1 < N; K++) {
+    const int64_t c0 = K * nb, w = wid(K);
+    double* P = A + c0 + c0 * lda;
+    const int64_t rest = n - c0 - w;
+    // blocks joining at this step: wait for them, then catch up steps 0..K-1
+    int64_t jn = joined;
+    while (jn < N && join[jn] <= K) jn++;
+    if (jn > joined) {
+      for (int64_t J = joined; J < jn; J++) {
+        e = cudaStreamWaitEvent(s, c->copy_ev[J], 0);
+        if (e != cudaSuccess) return e;
+      }
+      const int64_t x0 = joined * nb, xn = (jn * nb < n ? jn * nb : n) - x0;   // their columns
+      for (int64_t k = 0; k < K; k++) {
+        const int64_t ck = k * nb, wk = wid(k);
+        double* Pk = A + ck + ck * lda;
+        e = trsm_l(c, wk, xn, Pk, lda, A + ck + x0 * lda, lda, s);
+        if (e == cudaSuccess)
+          e = gemm(c, n - ck - wk, xn, wk, Pk + wk, lda, A + ck + x0 * lda, lda, A + ck + wk + x0 * lda, lda, false,
+                   s, KC_UPDATE);
+        if (e != cudaSuccess) return e;
+      }
+      joined = jn;
+    }
+    if (la && c0 > 0) {   // panel K (factored on the side stream) must be complete
+      e = cudaStreamWaitEvent(s, c->ev_p, 0);
+      if (e != cudaSuccess) return e;
+    }
+    const int64_t ncols = (joined * nb < n ? joined * nb : n) - (c0 + w);   // joined trailing columns
+    const int64_t w1 = wid(K + 1);
+    double* P1 = P + w + w * lda;
+    e = trsm_l(c, w, ncols, P, lda, P + w * lda, lda, s);
+    if (e != cudaSuccess) return e;
+    if (la && ncols > w1) {
+      e = gemm(c, rest, w1, w, P + w, lda, P + w * lda, lda, P1, lda, false, s, KC_UPDATE);
+      if (e == cudaSuccess) e = cudaEventRecord(c->ev_a, s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_a, 0);
+      if (e == cudaSuccess) e = panel_rec(c, rest, w1, P1, lda, c0 + w, info, c->side);
+      if (e == cudaSuccess) e = cudaEventRecord(c->ev_p, c->side);
+      if (e == cudaSuccess)
+        e = gemm(c, rest, ncols - w1, w, P + w, lda, P + (w + w1) * lda, lda, P1 + w1 * lda, lda, false, s, KC_UPDATE);
+      if (e != cudaSuccess) return e;
+    } else {
+      e = gemm(c, rest, ncols, w, P + w, lda, P + w * lda, lda, P1, lda, false, s, KC_UPDATE);
+      if (e == cudaSuccess) e = panel_rec(c, rest, w1, P1, lda, c0 + w, info, s);
+      if (e == cudaSuccess && la) e = cudaEventRecord(c->ev_p, s);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  if (la) {
     e = cudaEventRecord(c->ev_p, c->side);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, c->ev_p, 0);
   }
@@ -644,7 +767,15 @@ ebv_status_t ebv_lu_factor_host(ebv_context_t c, int64_t n, const double* hA, in
     if (e != cudaSuccess) return cuda_fail(e, "host factor (left-looking)");
     return EBV_SUCCESS;
   }
-  // default: one copy, then the (faster) right-looking schedule
+  if (tau >= 0 && c->nb != -1 && (c->path == EBV_PATH_AUTO || c->path == EBV_PATH_BLOCKED) &&
+      n >= 16384) {   // (smaller n: copy + factor is faster — measured n = 8192: 28 vs 44 ms)
+    // default: right-looking with the column blocks joining as they arrive
+    e = timed(c, KC_OTHER, 0, 0, s, 1, [&] { return launch_tau(n, A, lda, tau, c->d_tau, c->d_norm, s); });
+    if (e == cudaSuccess) e = lu_blocked_stream(c, n, A, lda, d_info, s, hA, ldh);
+    if (e != cudaSuccess) return cuda_fail(e, "host factor (streamed)");
+    return EBV_SUCCESS;
+  }
+  // otherwise: one copy, then the device schedule
   e = cudaMemcpy2DAsync(A, lda * sizeof(double), hA, ldh * sizeof(double), n * sizeof(double), n,
                         cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "host copy");

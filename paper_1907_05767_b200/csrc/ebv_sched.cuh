@@ -113,6 +113,8 @@ cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_
                        int64_t kl, int64_t ku);
 cudaError_t lu_left(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s,
                     const double* hA, int64_t ldh);
+cudaError_t lu_blocked_stream(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s,
+                              const double* hA, int64_t ldh);
 void dist_release(ebv_context* c);   // ebv_dist.cu
 
 }  // namespace sched

@@ -60,6 +60,6 @@ for n in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "8192,32768").s
                                st.cuda_stream)
     ms = timed(run_host)
     assert int(info) == 0
-    print(json.dumps({"n": n, "schedule": "left (host-streamed)", "what": "ebv_lu_factor_host (pinned)", "ms": ms,
+    print(json.dumps({"n": n, "schedule": "default host path", "what": "ebv_lu_factor_host (pinned)", "ms": ms,
                       "tflops": fl / ms / 1e9}), flush=True)
     del A0, Aw, hA

@@ -240,7 +240,8 @@ def test_left_looking_bitwise(dev, ctx, n, nb):
     assert bits_eq(LU.cpu().numpy(), lu_o)
 
 
-@pytest.mark.parametrize("n,pinned,tau", [(700, True, 0.0), (1537, False, 0.0), (3000, True, 0.0), (513, True, -1.0)])
+@pytest.mark.parametrize("n,pinned,tau", [(700, True, 0.0), (1537, False, 0.0), (3000, True, 0.0), (513, True, -1.0),
+                                          (16384, True, 0.0)])
 def test_factor_host_bitwise(dev, ctx, n, pinned, tau):
     """ebv_lu_factor_host: the matrix streamed from host memory block by block
     under the left-looking factorization — bitwise the oracle."""
@@ -253,6 +254,15 @@ def test_factor_host_bitwise(dev, ctx, n, pinned, tau):
     LU2, info2 = ebv.lu_factor_host(hA, tau=tau, ctx=cl)
     torch.cuda.synchronize()
     assert bits_eq(LU2.cpu().numpy(), LU.cpu().numpy()) and int(info2) == int(info)
+    if n > 4096:   # the streamed right-looking form: compare with the device factorization (same bits)
+        LUd, infod = ebv.lu_factor(d["At"].T.to(dev), ctx=ctx)
+        torch.cuda.synchronize()
+        assert int(info) == int(infod) == 0
+        assert torch.equal(LU.view(torch.int64), LUd.view(torch.int64))
+        lead = 1024   # and the leading block with the oracle (the same computation)
+        lu_o, _ = oracle.lu_factor(d["At"].T.numpy()[:lead, :lead])
+        assert bits_eq(LU[:lead, :lead].cpu().numpy(), lu_o)
+        return
     lu_o, info_o = oracle.lu_factor(d["At"].T.numpy(), tau=(n * np.finfo(float).eps *
                                                             np.abs(d["At"].T.numpy()).sum(1).max()) if tau < 0 else 0.0)
     assert int(info) == info_o
