@@ -61,7 +61,7 @@ def test_spec_residual_examples(golden):
 
 
 # ---------------------------------------------------------------- exact rational
-@pytest.mark.parametrize("n,seed", [(2, 1), (3, 2), (5, 3), (8, 4), (16, 5), (33, 6)])
+@pytest.mark.parametrize("n,seed", [(2, 1), (3, 2), (5, 3), (8, 4), (16, 5), (33, 6), (64, 7)])
 def test_exact_rational_lu_and_solve(n, seed):
     """The unique no-pivot LU of the exact input, computed with Crout formulas
     in rationals; the fp64 oracle must agree normwise to ~1e-14, and the exact
