@@ -215,6 +215,160 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   }
 }
 
+// Persistent form: grid = resident CTAs, each walks tiles blockIdx.x,
+// blockIdx.x + gridDim.x, ... (same grouped raster).  The TMA ring runs on
+// one global slice counter across the CTA's tiles, so the producer prefetches
+// the next tile's first slices while the current tile finishes, and each tile
+// prefetches the next tile's C block into L2 — the tile epilogue / prologue
+// no longer drains the DMMA pipe.  Per entry the same fma chain (bitwise).
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, C::MINB)
+    gemm_tma_persistent_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                               int64_t M, int64_t N, int64_t K, double* __restrict__ Cm, int64_t ldc, int tilesM,
+                               int tilesN) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  double* sA = reinterpret_cast<double*>(base);
+  double* sB = sA + C::STAGES * C::A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_STAGE);
+  uint64_t* empty = full + C::STAGES;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nk = (int)((K + C::KC - 1) / C::KC);
+  const int ntiles = tilesM * tilesN;
+  const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const long long total = (long long)my_tiles * nk;
+  auto coords = [&](int ti, int& m0, int& n0) {
+    const int G = 8;
+    const int bid = blockIdx.x + ti * gridDim.x;
+    const int group = bid / (G * tilesN);
+    const int first_m = group * G;
+    const int gsz = min(tilesM - first_m, G);
+    m0 = (first_m + (bid % (G * tilesN)) % gsz) * C::BM;
+    n0 = ((bid % (G * tilesN)) / gsz) * C::BN;
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < C::STAGES; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  // producer cursor (warp 0): slot ps, its empty-barrier phase pph, tile pt, slice pk
+  int ps = 0, pt = 0, pk = 0, pm0 = 0, pn0 = 0;
+  uint32_t pph = 0;
+  long long pj = 0;
+  if (my_tiles > 0) coords(0, pm0, pn0);
+  auto produce = [&]() {
+    if (pj >= C::STAGES) mbar_wait(&empty[ps], pph ^ 1u);
+    if (lane == 0) {
+      const int m0 = pm0, n0 = pn0, kt = pk;
+      mbar_expect_tx(&full[ps], C::STAGE_BYTES);
+      tma_load_2d(sA + ps * C::A_STAGE, &tmA, m0, kt * C::KC, &full[ps]);
+      tma_load_2d(sB + ps * C::B_STAGE, &tmB, kt * C::KC, n0, &full[ps]);
+    }
+    __syncwarp();
+    ++pj;
+    if (++ps == C::STAGES) { ps = 0; pph ^= 1u; }
+    if (++pk == nk) { pk = 0; if (++pt < my_tiles) coords(pt, pm0, pn0); }
+  };
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    while (pj < C::STAGES - 1 && pj < total) produce();
+  }
+
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp % C::WM, wn = warp / C::WM;
+  int cs = 0;
+  uint32_t cph = 0;
+  for (int ti = 0; ti < my_tiles; ti++) {
+    int m0, n0;
+    coords(ti, m0, n0);
+    const int64_t mb = (int64_t)m0 + wm * (C::MT * 8) + 2 * t;
+    const int64_t nb = (int64_t)n0 + wn * (C::NT * 8) + g;
+    const bool vec_c = ((ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(Cm) & 15) == 0) && (m0 + C::BM <= M) &&
+                       (n0 + C::BN <= N);
+    double acc[C::MT][C::NT][2];
+    if (vec_c) {
+#pragma unroll
+      for (int mt = 0; mt < C::MT; mt++)
+#pragma unroll
+        for (int nt = 0; nt < C::NT; nt++) {
+          const double2 v = *reinterpret_cast<const double2*>(Cm + (mb + mt * 8) + (nb + nt * 8) * ldc);
+          acc[mt][nt][0] = v.x;
+          acc[mt][nt][1] = v.y;
+        }
+    } else {
+#pragma unroll
+      for (int mt = 0; mt < C::MT; mt++)
+#pragma unroll
+        for (int nt = 0; nt < C::NT; nt++)
+#pragma unroll
+          for (int q = 0; q < 2; q++) {
+            const int64_t m = mb + mt * 8 + q, n = nb + nt * 8;
+            acc[mt][nt][q] = (m < M && n < N) ? Cm[m + n * ldc] : 0.0;
+          }
+    }
+    if (ti + 1 < my_tiles) {   // the next tile's C block into L2 (one 128-byte line per thread and column slice)
+      int pm0, pn0;
+      coords(ti + 1, pm0, pn0);
+      for (int idx = tid; idx < C::BN * (C::BM / 16); idx += C::THREADS) {
+        const int64_t col = pn0 + idx / (C::BM / 16), row = pm0 + (idx % (C::BM / 16)) * 16;
+        if (col < N && row < M)
+          asm volatile("prefetch.global.L2 [%0];\n" ::"l"(Cm + row + col * ldc));
+      }
+    }
+    for (int kt = 0; kt < nk; kt++) {
+      const int s = cs;
+      if (warp == 0 && pj < total) produce();
+      mbar_wait(&full[s], cph);
+      __syncwarp();
+      const double* a = sA + s * C::A_STAGE + wm * (C::MT * 8) + g;
+      const double* b = sB + s * C::B_STAGE + (wn * (C::NT * 8) + g) * C::BSTR + t;
+#pragma unroll
+      for (int ks = 0; ks < C::KC / 4; ks++) {
+        double af[C::MT], bf[C::NT];
+#pragma unroll
+        for (int mt = 0; mt < C::MT; mt++) af[mt] = a[(ks * 4 + t) * C::AST + mt * 8];
+#pragma unroll
+        for (int nt = 0; nt < C::NT; nt++) bf[nt] = -b[nt * 8 * C::BSTR + ks * 4];
+#pragma unroll
+        for (int mt = 0; mt < C::MT; mt++)
+#pragma unroll
+          for (int nt = 0; nt < C::NT; nt++) dmma(acc[mt][nt][0], acc[mt][nt][1], bf[nt], af[mt]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++cs == C::STAGES) { cs = 0; cph ^= 1u; }
+    }
+    if (vec_c) {
+#pragma unroll
+      for (int mt = 0; mt < C::MT; mt++)
+#pragma unroll
+        for (int nt = 0; nt < C::NT; nt++)
+          *reinterpret_cast<double2*>(Cm + (mb + mt * 8) + (nb + nt * 8) * ldc) =
+              make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+    } else {
+#pragma unroll
+      for (int mt = 0; mt < C::MT; mt++)
+#pragma unroll
+        for (int nt = 0; nt < C::NT; nt++)
+#pragma unroll
+          for (int q = 0; q < 2; q++) {
+            const int64_t m = mb + mt * 8 + q, n = nb + nt * 8;
+            if (m < M && n < N) Cm[m + n * ldc] = acc[mt][nt][q];
+          }
+    }
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -258,6 +412,32 @@ cudaError_t run_tma(int64_t M, int64_t N, int64_t K, const double* A, int64_t ld
   return cudaGetLastError();
 }
 
+template <class C>
+cudaError_t run_tma_persistent(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                               int64_t ldb, double* Cm, int64_t ldc, cudaStream_t s) {
+  static bool attr_done = false;
+  static int slots = 0;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tma_persistent_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gemm_tma_persistent_kernel<C>, C::THREADS, C::SMEM);
+    slots = sms * (per > 0 ? per : 1);
+    attr_done = true;
+  }
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, M, K, lda, C::AST, C::KC) || !make_map(&mb, B, K, N, ldb, C::BSTR, C::BN))
+    return cudaErrorNotSupported;
+  const int64_t tm = (M + C::BM - 1) / C::BM, tn = (N + C::BN - 1) / C::BN;
+  const int64_t grid = tm * tn < slots ? tm * tn : slots;
+  gemm_tma_persistent_kernel<C><<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(ma, mb, M, N, K, Cm, ldc, (int)tm,
+                                                                           (int)tn);
+  return cudaGetLastError();
+}
+
 //                     BM   BN  WM WN KC ST MINB
 using TMid = TCfg<128, 64, 4, 2, 16, 4, 2>;     // 8 warps (32x32 warp tiles), 2 CTAs/SM
 using TBig = TCfg<128, 128, 4, 4, 16, 4, 1>;    // 16 warps (32x32), 1 CTA/SM
@@ -283,6 +463,8 @@ cudaError_t launch_gemm_sub_tma(int64_t M, int64_t N, int64_t K, const double* A
     case 3: return run_tma<TWide>(M, N, K, A, lda, B, ldb, Cm, ldc, s);
     case 4: return run_tma<TBig6>(M, N, K, A, lda, B, ldb, Cm, ldc, s);
     case 5: return run_tma<TMid3>(M, N, K, A, lda, B, ldb, Cm, ldc, s);
+    case 6: return run_tma_persistent<TMid3>(M, N, K, A, lda, B, ldb, Cm, ldc, s);
+    case 7: return run_tma_persistent<TMid>(M, N, K, A, lda, B, ldb, Cm, ldc, s);
     default: return run_tma<TMid>(M, N, K, A, lda, B, ldb, Cm, ldc, s);
   }
 }
