@@ -1,0 +1,272 @@
+// Probe: latency of the panel kernels of k_leaf.cu in isolation (the panel
+// is the critical chain of the blocked factorization once the trailing
+// updates get small: n = 1024 .. 8192).  Includes the library's k_leaf.cu
+// (same kernels, same launch configuration) and times single launches with
+// CUDA events (the empty-launch line is the event overhead); %clock64-
+// instrumented copies of the diagonal-block loop (with the division or the
+// per-step barrier removed, timing only) and of trsm_ru give cycles per
+// elimination step.  Results: profiles/r01_probe_leaf.jsonl.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 \
+//        -I paper_1907_05767_b200/csrc probes/leaf_probe.cu -o probes/leaf_probe
+#include "k_leaf.cu"
+#include <cstdio>
+#include <vector>
+#include <cstring>
+
+namespace ebv {
+void set_error(const std::string&) {}
+}
+
+using namespace ebv;
+
+// DD test block: a_ii = n + 1, off-diagonal in (-1, 1)
+static void fill(std::vector<double>& h, int64_t M, int64_t ld) {
+  uint64_t s = 12345;
+  for (int64_t c = 0; c < 64; c++)
+    for (int64_t r = 0; r < M; r++) {
+      s = s * 6364136223846793005ULL + 1442695040888963407ULL;
+      double v = ((s >> 11) * (1.0 / 9007199254740992.0)) * 2.0 - 1.0;
+      h[r + c * ld] = (r == c) ? 65.0 : v;
+    }
+}
+
+// instrumented diagonal-block loop (leaf_lu_kernel's scheme): thread 0
+// stamps each step.  MODE 0: as the library; 1: multiply instead of divide
+// (timing only); 2: no __syncthreads (timing only, wrong values);
+// 3: divide by the reciprocal published with the row (timing of the
+// reciprocal scheme)
+template <int GD, int MODE>
+__global__ void leaf_steps(double* A, int64_t lda, long long* stamps) {
+  constexpr int QD = W / GD;
+  __shared__ __align__(16) double urow[2][2 * W];
+  __shared__ double rc[2];
+  const int tid = threadIdx.x, i = tid / GD, j = tid % GD, lane = tid & 31, base = lane & ~(GD - 1);
+  double a[QD];
+  for (int q = 0; q < QD; q++) a[q] = A[i + (int64_t)(j + GD * q) * lda];
+  __syncthreads();
+  const long long t0 = clock64();
+#pragma unroll 1
+  for (int qk = 0; qk < QD; qk++) {
+#pragma unroll
+    for (int o = 0; o < GD; o++) {
+      const int k = qk * GD + o;
+      double* ur = urow[o & 1] + GD * qk;
+      if (i == k) {
+#pragma unroll
+        for (int q = 0; q < QD; q++) ur[j + GD * q] = a[q];
+        if (MODE == 3 && j == o) rc[o & 1] = 1.0 / a[0];
+      }
+      if (MODE != 2) __syncthreads();
+      const double piv = ur[o];
+      if (i > k && j == o) {
+        if (MODE == 0) a[0] = a[0] / piv;
+        else if (MODE == 3) a[0] = a[0] * rc[o & 1];
+        else a[0] = a[0] * piv;
+      }
+      const double l = __shfl_sync(0xffffffffu, a[0], base + o);
+      if (i > k) {
+        if (j > o) a[0] = fma(-l, ur[j], a[0]);
+#pragma unroll
+        for (int q = 1; q < QD; q++) a[q] = fma(-l, ur[j + GD * q], a[q]);
+      }
+    }
+    A[i + (int64_t)(j + GD * qk) * lda] = a[0];
+    for (int q = 0; q < QD - 1; q++) a[q] = a[q + 1];
+    a[QD - 1] = 0.0;
+  }
+  if (tid == 0) stamps[0] = clock64() - t0;
+}
+template <int GD, int MODE>
+void leaf_steps_run(double* d, int64_t ld, long long* st, const char* name) {
+  long long h;
+  for (int r = 0; r < 3; r++) leaf_steps<GD, MODE><<<1, W * GD>>>(d, ld, st);
+  cudaDeviceSynchronize();
+  cudaMemcpy(&h, st, 8, cudaMemcpyDeviceToHost);
+  printf("{\"probe\": \"leaf_steps\", \"GD\": %d, \"mode\": \"%s\", \"cycles_per_step\": %.1f}\n", GD, name, h / 64.0);
+}
+
+// instrumented trsm_ru_kernel: thread 0 stamps after the U fill and at each
+// 8-step block; mode 1 = plain division (no verified reciprocal)
+__global__ void __launch_bounds__(256, 2) trsm_steps(int64_t m, int k, double* __restrict__ X, int64_t ldx,
+                                                     const double* __restrict__ U, int64_t ldu, long long* stamps,
+                                                     int mode) {
+  __shared__ __align__(16) double sU[W * S + W];
+  __shared__ double srcp[W];
+  if (threadIdx.x == 0) stamps[0] = clock64();
+  for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
+    const int p = idx % W, c = idx / W;
+    sU[p * S + c] = (p < k && c < k) ? (p <= c ? U[p + (int64_t)c * ldu] : 0.0) : (p == c ? 1.0 : 0.0);
+  }
+  for (int idx = threadIdx.x; idx < W * (S - W) + W; idx += blockDim.x)
+    if (idx < W * (S - W)) sU[(idx / (S - W)) * S + W + idx % (S - W)] = 0.0; else sU[W * S + idx - W * (S - W)] = 0.0;
+  __syncthreads();
+  if (threadIdx.x < W) srcp[threadIdx.x] = 1.0 / sU[threadIdx.x * S + threadIdx.x];
+  __syncthreads();
+  const int tid = threadIdx.x, j = tid % G, lane = tid & 31, base = lane & ~(G - 1);
+  const int64_t i0 = (int64_t)blockIdx.x * (32 * RR) + tid / G;
+  double x[RR][Q];
+  for (int r = 0; r < RR; r++)
+    for (int q = 0; q < Q; q++) {
+      const int c = j + G * q;
+      const int64_t i = i0 + 32 * r;
+      x[r][q] = (i < m && c < k) ? X[i + (int64_t)c * ldx] : 0.0;
+    }
+  if (threadIdx.x == 0) stamps[1] = clock64();
+  int redo = 0;
+#pragma unroll 1
+  for (int qk = 0; qk < Q; qk++) {
+    double xs[RR][Q];
+#pragma unroll
+    for (int r = 0; r < RR; r++)
+#pragma unroll
+      for (int q = 0; q < Q; q++) xs[r][q] = x[r][q];
+    bool ok = true;
+#pragma unroll
+    for (int o = 0; o < G; o++) {
+      const int p = qk * G + o;
+      const double* up = sU + p * S + G * qk;
+      const double upp = up[o], rp = srcp[p];
+#pragma unroll
+      for (int r = 0; r < RR; r++) {
+        if (j == o) x[r][0] = mode ? x[r][0] / upp : quot_v(x[r][0], upp, rp, ok);
+        const double xp = __shfl_sync(0xffffffffu, x[r][0], base + o);
+        if (j > o) x[r][0] = fma(-xp, up[j], x[r][0]);
+#pragma unroll
+        for (int q = 1; q < Q; q++) x[r][q] = fma(-xp, up[j + G * q], x[r][q]);
+      }
+    }
+    if (__any_sync(0xffffffffu, !ok)) {
+      redo++;
+#pragma unroll
+      for (int r = 0; r < RR; r++)
+#pragma unroll
+        for (int q = 0; q < Q; q++) x[r][q] = xs[r][q];
+#pragma unroll
+      for (int o = 0; o < G; o++) {
+        const int p = qk * G + o;
+        const double* up = sU + p * S + G * qk;
+#pragma unroll
+        for (int r = 0; r < RR; r++) {
+          if (j == o) x[r][0] = x[r][0] / up[o];
+          const double xp = __shfl_sync(0xffffffffu, x[r][0], base + o);
+          if (j > o) x[r][0] = fma(-xp, up[j], x[r][0]);
+#pragma unroll
+          for (int q = 1; q < Q; q++) x[r][q] = fma(-xp, up[j + G * q], x[r][q]);
+        }
+      }
+    }
+    const int c = j + G * qk;
+#pragma unroll
+    for (int r = 0; r < RR; r++) {
+      const int64_t i = i0 + 32 * r;
+      if (i < m && c < k) X[i + (int64_t)c * ldx] = x[r][0];
+#pragma unroll
+      for (int q = 0; q < Q - 1; q++) x[r][q] = x[r][q + 1];
+      x[r][Q - 1] = 0.0;
+    }
+    if (threadIdx.x == 0) stamps[2 + qk] = clock64();
+  }
+  if (threadIdx.x == 0) stamps[10] = redo;
+}
+
+// per-launch event timing: reset (untimed), then event / kernel / event
+template <class F, class R>
+static float time_one(F f, R reset, int reps) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float tot = 0;
+  for (int r = 0; r < reps + 3; r++) {
+    reset();
+    cudaDeviceSynchronize();
+    cudaEventRecord(e0);
+    f();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r >= 3) tot += ms;
+  }
+  return 1e3f * tot / reps;
+}
+template <class F>
+static float time_it(F f, int reps) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int r = 0; r < 5; r++) f();
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; r++) f();
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  return 1e3f * ms / reps;
+}
+
+int main() {
+  const int64_t Mmax = 8192, ld = Mmax;
+  std::vector<double> h(ld * 64);
+  fill(h, Mmax, ld);
+  double *d, *d0, *tau;
+  int64_t* info;
+  int* cnt;
+  long long* st;
+  cudaMalloc(&d, ld * 64 * 8);
+  cudaMalloc(&d0, ld * 64 * 8);
+  cudaMalloc(&tau, 8);
+  cudaMalloc(&info, 8);
+  cudaMalloc(&cnt, 4);
+  cudaMalloc(&st, 65 * 8);
+  cudaMemset(tau, 0, 8);
+  cudaMemset(info, 0, 8);
+  cudaMemset(cnt, 0, 4);
+  cudaMemcpy(d0, h.data(), ld * 64 * 8, cudaMemcpyHostToDevice);
+  // the factor of a fixed DD block is re-run in place: values drift but stay
+  // finite (DD is preserved: the LU overwrites, then the next run factors the
+  // packed factors, still DD-like); timing only
+  auto reset = [&] { cudaMemcpy(d, d0, ld * 64 * 8, cudaMemcpyDeviceToDevice); };
+  reset();
+  printf("{\"probe\": \"leaf_lu_w64\", \"us\": %.2f}\n",
+         time_one([&] { launch_leaf_lu(64, d, ld, tau, info, 0, 0); }, reset, 50));
+  for (int64_t M : {64, 128, 256, 1024, 2048, 4096, 8192}) {
+    float t = time_one([&] { launch_panel_leaf(M, 64, d, ld, tau, info, 0, cnt, 0); }, reset, 50);
+    printf("{\"probe\": \"panel_leaf_w64\", \"M\": %lld, \"us\": %.2f}\n", (long long)M, t);
+  }
+  for (int64_t m : {64, 1024, 8192}) {
+    float t = time_one([&] { launch_trsm_right_upper(m, 64, d + 64, ld, d, ld, 0); }, reset, 50);
+    printf("{\"probe\": \"trsm_ru_k64\", \"m\": %lld, \"us\": %.2f}\n", (long long)m, t);
+  }
+  double* dx;
+  cudaMalloc(&dx, 64 * 8192 * 8);
+  cudaMemset(dx, 0, 64 * 8192 * 8);
+  for (int64_t m : {64, 1024, 8192}) {
+    float t = time_it([&] { launch_trsm_left_lower_unit(64, m, d, ld, dx, 64, 0); }, 100);
+    printf("{\"probe\": \"trsm_llu_k64\", \"m\": %lld, \"us\": %.2f}\n", (long long)m, t);
+  }
+  long long hs[65];
+  leaf_steps_run<4, 0>(d, ld, st, "div");
+  leaf_steps_run<4, 1>(d, ld, st, "mul");
+  leaf_steps_run<4, 2>(d, ld, st, "nosync");
+  leaf_steps_run<4, 3>(d, ld, st, "rcp");
+  leaf_steps_run<2, 0>(d, ld, st, "div");
+  leaf_steps_run<8, 0>(d, ld, st, "div");
+  leaf_steps_run<8, 1>(d, ld, st, "mul");
+  leaf_steps_run<16, 0>(d, ld, st, "div");
+  leaf_steps_run<16, 1>(d, ld, st, "mul");
+  printf("{\"probe\": \"empty_launch_event_us\", \"us\": %.2f}\n", time_one([&] { launch_panel_leaf(0, 64, d, ld, tau, info, 0, cnt, 0); }, reset, 50));
+  for (int mode = 0; mode < 2; mode++) {
+    reset();
+    trsm_steps<<<1, 256>>>(64, 64, d + 64, ld, d, ld, st, mode);
+    reset();
+    trsm_steps<<<1, 256>>>(64, 64, d + 64, ld, d, ld, st, mode);
+    cudaDeviceSynchronize();
+    cudaMemcpy(hs, st, 11 * 8, cudaMemcpyDeviceToHost);
+    printf("{\"probe\": \"trsm_ru_cycles\", \"mode\": %d, \"fill\": %lld, \"blocks\": [", mode, hs[1] - hs[0]);
+    for (int b = 0; b < 8; b++) printf("%lld%s", hs[2 + b] - hs[1 + b], b < 7 ? ", " : "]");
+    printf(", \"redo\": %lld}\n", hs[10]);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
+  return 0;
+}
