@@ -102,9 +102,14 @@ __global__ void __launch_bounds__(W * GD) leaf_lu_kernel(int w, double* __restri
 // unverified quotient redoes its rows with true division, so every entry is
 // RN(x/u) — bitwise the oracle — and the chain per step is three dependent
 // fp64 operations instead of a division.
-__device__ __forceinline__ double quot_v(double y, double u, double r, bool& ok) {
+__device__ __forceinline__ double quot_m(double y, double u, double r) {   // Markstein: q0 + r (y - u q0)
   const double q0 = y * r;
-  const double q = fma(r, fma(-u, q0, y), q0);
+  return fma(r, fma(-u, q0, y), q0);
+}
+// exact test that q == RN(y / u): the remainder y - u q (exact by fma) is
+// below half an ulp of q times |u| (halved below a power of two on the side
+// of the smaller ulp); +0 dividends (the identity padding) are exact
+__device__ __forceinline__ bool quot_ok(double y, double u, double q) {
   const double rr = fma(-u, q, y);
   const long long qb = __double_as_longlong(q);
   const long long e = qb & 0x7ff0000000000000LL;
@@ -116,8 +121,7 @@ __device__ __forceinline__ double quot_v(double y, double u, double r, bool& ok)
   // y = +0 (the identity padding): the sequence returns +0 / -0 for u > 0 /
   // u < 0, which is RN(y/u) exactly
   const bool pzero = __double_as_longlong(y) == 0;
-  ok = ok && (pzero || (normal && fabs(rr) < lim));
-  return q;
+  return pzero || (normal && fabs(rr) < lim);
 }
 
 // RR rows per lane group (independent chains interleaved): a CTA of 256
@@ -163,7 +167,9 @@ __global__ void __launch_bounds__(256, 2) trsm_ru_kernel(int64_t m, int k, doubl
     for (int r = 0; r < RR; r++)
 #pragma unroll
       for (int q = 0; q < Q; q++) xs[r][q] = x[r][q];
-    bool ok = true;
+    // the quotients of the block are verified after it (off the step chain):
+    // lane j owns step qk*G + j and keeps its dividend and quotient
+    double ychk[RR], qchk[RR];
 #pragma unroll
     for (int o = 0; o < G; o++) {
       const int p = qk * G + o;
@@ -171,12 +177,22 @@ __global__ void __launch_bounds__(256, 2) trsm_ru_kernel(int64_t m, int k, doubl
       const double upp = up[o], rp = srcp[p];
 #pragma unroll
       for (int r = 0; r < RR; r++) {
-        if (j == o) x[r][0] = quot_v(x[r][0], upp, rp, ok);
+        if (j == o) {
+          ychk[r] = x[r][0];
+          x[r][0] = quot_m(x[r][0], upp, rp);
+          qchk[r] = x[r][0];
+        }
         const double xp = __shfl_sync(0xffffffffu, x[r][0], base + o);
         if (j > o) x[r][0] = fma(-xp, up[j], x[r][0]);
 #pragma unroll
         for (int q = 1; q < Q; q++) x[r][q] = fma(-xp, up[j + G * q], x[r][q]);
       }
+    }
+    bool ok = true;
+    {
+      const double uown = sU[(qk * G + j) * S + qk * G + j];
+#pragma unroll
+      for (int r = 0; r < RR; r++) ok = ok && quot_ok(ychk[r], uown, qchk[r]);
     }
     if (__any_sync(0xffffffffu, !ok)) {            // redo the block with true division
 #pragma unroll
@@ -305,16 +321,22 @@ __global__ void __launch_bounds__(W * GD) panel_leaf_kernel(int64_t M, int w, do
     for (int q = 0; q < QD; q++) x[q] = x0[q];
 #pragma unroll 1
     for (int qk = 0; qk < QD; qk++) {
+      double ychk = 0.0, qchk = 0.0;                  // lane j's step of the block, verified after it
 #pragma unroll
       for (int o = 0; o < GD; o++) {
         const int p = qk * GD + o;
         const double* up = sUp + p * US + GD * qk;
-        if (j == o) x[0] = exact ? x[0] / up[o] : quot_v(x[0], up[o], srcp[p], ok);
+        if (j == o) {
+          ychk = x[0];
+          x[0] = exact ? x[0] / up[o] : quot_m(x[0], up[o], srcp[p]);
+          qchk = x[0];
+        }
         const double xp = __shfl_sync(0xffffffffu, x[0], base + o);
         if (j > o) x[0] = fma(-xp, up[j], x[0]);
 #pragma unroll
         for (int q = 1; q < QD; q++) x[q] = fma(-xp, up[j + GD * q], x[q]);
       }
+      if (!exact) ok = ok && quot_ok(ychk, sUp[(qk * GD + j) * US + qk * GD + j], qchk);
       const int c = j + GD * qk;
       if (rv && c < w) P[r + (int64_t)c * lda] = x[0];
 #pragma unroll

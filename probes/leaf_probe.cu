@@ -18,6 +18,11 @@ void set_error(const std::string&) {}
 }
 
 using namespace ebv;
+__device__ __forceinline__ double quot_v(double y, double u, double r, bool& ok) {
+  const double q = quot_m(y, u, r);
+  ok = ok && quot_ok(y, u, q);
+  return q;
+}
 
 // DD test block: a_ii = n + 1, off-diagonal in (-1, 1)
 static void fill(std::vector<double>& h, int64_t M, int64_t ld) {
@@ -232,6 +237,23 @@ int main() {
   for (int64_t M : {64, 128, 256, 1024, 2048, 4096, 8192}) {
     float t = time_one([&] { launch_panel_leaf(M, 64, d, ld, tau, info, 0, cnt, 0); }, reset, 50);
     printf("{\"probe\": \"panel_leaf_w64\", \"M\": %lld, \"us\": %.2f}\n", (long long)M, t);
+  }
+  {
+    std::vector<double> ha(ld * 64), hb(ld * 64);
+    for (int64_t m : {1, 64, 100, 1024, 8128}) {
+      for (int kv : {64, 37, 8}) {
+        auto old_k = [&] {   // reference: the same scheme with true division every step
+          trsm_steps<<<(unsigned)((m + 32 * RR - 1) / (32 * RR)), 256>>>(m, kv, d + 64, ld, d, ld, st, 1);
+        };
+        auto new_k = [&] { launch_trsm_right_upper(m, kv, d + 64, ld, d, ld, 0); };
+        reset(); old_k(); cudaMemcpy(ha.data(), d, ld * 64 * 8, cudaMemcpyDeviceToHost);
+        reset(); new_k(); cudaMemcpy(hb.data(), d, ld * 64 * 8, cudaMemcpyDeviceToHost);
+        long long diff = 0;
+        for (size_t q = 0; q < ha.size(); q++) diff += memcmp(&ha[q], &hb[q], 8) != 0;
+        printf("{\"probe\": \"trsm_ru_vs_ref\", \"m\": %lld, \"k\": %d, \"us\": %.2f, \"div_ref_us\": %.2f, \"mismatch\": %lld}\n",
+               (long long)m, kv, time_one(new_k, reset, 30), time_one(old_k, reset, 30), diff);
+      }
+    }
   }
   for (int64_t m : {64, 1024, 8192}) {
     float t = time_one([&] { launch_trsm_right_upper(m, 64, d + 64, ld, d, ld, 0); }, reset, 50);
