@@ -48,8 +48,8 @@ constexpr int Q = W / G;      // entries per lane
 template <int GD>
 __global__ void __launch_bounds__(W * GD) leaf_lu_kernel(int w, double* __restrict__ A, int64_t lda,
                                                         const double* __restrict__ tau, int64_t* info, int64_t koff) {
-  constexpr int QD = W / GD;
-  __shared__ __align__(16) double urow[2][2 * W];
+  constexpr int QD = W / GD, PS = QD + 2;
+  __shared__ __align__(16) double urow[2][GD * PS];   // lane-slot layout: urow[.][j*PS + q] = lane j's a[q]
   __shared__ int smin;
   const int tid = threadIdx.x, i = tid / GD, j = tid % GD, lane = tid & 31, base = lane & ~(GD - 1);
   double a[QD];
@@ -65,20 +65,24 @@ __global__ void __launch_bounds__(W * GD) leaf_lu_kernel(int w, double* __restri
 #pragma unroll
     for (int o = 0; o < GD; o++) {
       const int k = qk * GD + o;
-      double* ur = urow[o & 1] + GD * qk;           // ur[j + GD*q] = u(k, j + GD*(q + qk))
+      double* ur = urow[o & 1];                    // ur[j*PS + q] = u(k, j + GD*(q + qk))
       if (i == k) {
 #pragma unroll
-        for (int q = 0; q < QD; q++) ur[j + GD * q] = a[q];
+        for (int q = 0; q < QD; q += 2) *reinterpret_cast<double2*>(ur + j * PS + q) = make_double2(a[q], a[q + 1]);
       }
       __syncthreads();
-      const double piv = ur[o];
+      const double piv = ur[o * PS];
       if (tid == 0 && k < w && fabs(piv) <= tv) atomicMin(&smin, k + 1);
       if (i > k && j == o) a[0] = a[0] / piv;                       // Eq 6-a
       const double l = __shfl_sync(0xffffffffu, a[0], base + o);
-      if (i > k) {
-        if (j > o) a[0] = fma(-l, ur[j], a[0]);                      // Eq 6-c
+      if (i > k) {                                                   // Eq 6-c
+        const double* uj = ur + j * PS;
 #pragma unroll
-        for (int q = 1; q < QD; q++) a[q] = fma(-l, ur[j + GD * q], a[q]);
+        for (int q = 0; q < QD; q += 2) {
+          const double2 u2 = *reinterpret_cast<const double2*>(uj + q);
+          if (q > 0 || j > o) a[q] = fma(-l, u2.x, a[q]);
+          a[q + 1] = fma(-l, u2.y, a[q + 1]);
+        }
       }
     }
     const int c = j + GD * qk;                        // final: store, rotate
@@ -236,18 +240,20 @@ __global__ void __launch_bounds__(256, 2) trsm_ru_kernel(int64_t m, int k, doubl
 // and reports info,
 // publishing each final U row into a full shared copy of U11, then solves
 // its 64 rows below with the trsm_ru scheme (verified reciprocal quotients).
-constexpr int US = 2 * W;     // shared U row stride (covers the rotation overrun)
+// Shared U rows in the lane-slot layout of leaf_lu_kernel: row k occupies
+// GD slots of PS doubles, slot j holding lane j's entries in local
+// (rotated) order, so each lane reads its entries with 16-byte loads.
 
 template <int GD>
 __global__ void __launch_bounds__(W * GD) panel_leaf_kernel(int64_t M, int w, double* __restrict__ P, int64_t lda,
                                                            const double* __restrict__ tau, int64_t* info,
                                                            int64_t koff, int* count) {
-  constexpr int QD = W / GD;
-  extern __shared__ __align__(16) double sUp[];    // [W][US]: sUp[k*US + c] = u(k, c)
+  constexpr int QD = W / GD, PS = QD + 2, RS = GD * PS;
+  extern __shared__ __align__(16) double sUp[];    // [W][RS]: sUp[k*RS + j*PS + q] = u(k, j + GD*(q + k/GD))
   __shared__ double srcp[W];
   __shared__ int smin, slast;
   const int tid = threadIdx.x, i = tid / GD, j = tid % GD, lane = tid & 31, base = lane & ~(GD - 1);
-  for (int idx = tid; idx < W * US; idx += W * GD) sUp[idx] = 0.0;
+  for (int idx = tid; idx < W * RS; idx += W * GD) sUp[idx] = 0.0;
   double a[QD];
 #pragma unroll
   for (int q = 0; q < QD; q++) {
@@ -274,20 +280,24 @@ __global__ void __launch_bounds__(W * GD) panel_leaf_kernel(int64_t M, int w, do
 #pragma unroll
     for (int o = 0; o < GD; o++) {
       const int k = qk * GD + o;
-      double* ur = sUp + k * US + GD * qk;           // ur[j + GD*q] = u(k, j + GD*(q + qk))
+      double* ur = sUp + k * RS;                     // ur[j*PS + q] = u(k, j + GD*(q + qk))
       if (i == k) {
 #pragma unroll
-        for (int q = 0; q < QD; q++) ur[j + GD * q] = a[q];
+        for (int q = 0; q < QD; q += 2) *reinterpret_cast<double2*>(ur + j * PS + q) = make_double2(a[q], a[q + 1]);
       }
       __syncthreads();
-      const double piv = ur[o];
+      const double piv = ur[o * PS];
       if (store && tid == 0 && k < w && fabs(piv) <= tv) atomicMin(&smin, k + 1);
       if (i > k && j == o) a[0] = a[0] / piv;                       // Eq 6-a
       const double l = __shfl_sync(0xffffffffu, a[0], base + o);
-      if (i > k) {
-        if (j > o) a[0] = fma(-l, ur[j], a[0]);                      // Eq 6-c
+      if (i > k) {                                                   // Eq 6-c
+        const double* uj = ur + j * PS;
 #pragma unroll
-        for (int q = 1; q < QD; q++) a[q] = fma(-l, ur[j + GD * q], a[q]);
+        for (int q = 0; q < QD; q += 2) {
+          const double2 u2 = *reinterpret_cast<const double2*>(uj + q);
+          if (q > 0 || j > o) a[q] = fma(-l, u2.x, a[q]);
+          a[q + 1] = fma(-l, u2.y, a[q + 1]);
+        }
       }
     }
     const int c = j + GD * qk;
@@ -302,7 +312,7 @@ __global__ void __launch_bounds__(W * GD) panel_leaf_kernel(int64_t M, int w, do
     if (*vi == 0) *vi = koff + smin;
   }
   if (M <= w) return;
-  if (tid < W) srcp[tid] = 1.0 / sUp[tid * US + tid];
+  if (tid < W) srcp[tid] = 1.0 / sUp[tid * RS + (tid % GD) * PS];
   __syncthreads();
   // ---- rows below (trsm_ru): this CTA's 64 rows, a group of 8 lanes each
   const int64_t r = (int64_t)w + (int64_t)blockIdx.x * W + i;
@@ -325,18 +335,22 @@ __global__ void __launch_bounds__(W * GD) panel_leaf_kernel(int64_t M, int w, do
 #pragma unroll
       for (int o = 0; o < GD; o++) {
         const int p = qk * GD + o;
-        const double* up = sUp + p * US + GD * qk;
+        const double* up = sUp + p * RS;
         if (j == o) {
           ychk = x[0];
-          x[0] = exact ? x[0] / up[o] : quot_m(x[0], up[o], srcp[p]);
+          x[0] = exact ? x[0] / up[o * PS] : quot_m(x[0], up[o * PS], srcp[p]);
           qchk = x[0];
         }
         const double xp = __shfl_sync(0xffffffffu, x[0], base + o);
-        if (j > o) x[0] = fma(-xp, up[j], x[0]);
+        const double* uj = up + j * PS;
 #pragma unroll
-        for (int q = 1; q < QD; q++) x[q] = fma(-xp, up[j + GD * q], x[q]);
+        for (int q = 0; q < QD; q += 2) {
+          const double2 u2 = *reinterpret_cast<const double2*>(uj + q);
+          if (q > 0 || j > o) x[q] = fma(-xp, u2.x, x[q]);
+          x[q + 1] = fma(-xp, u2.y, x[q + 1]);
+        }
       }
-      if (!exact) ok = ok && quot_ok(ychk, sUp[(qk * GD + j) * US + qk * GD + j], qchk);
+      if (!exact) ok = ok && quot_ok(ychk, sUp[(qk * GD + j) * RS + j * PS], qchk);
       const int c = j + GD * qk;
       if (rv && c < w) P[r + (int64_t)c * lda] = x[0];
 #pragma unroll
@@ -439,7 +453,7 @@ cudaError_t launch_panel_leaf(int64_t M, int64_t w, double* P, int64_t lda, cons
                               int64_t koff, int* count, cudaStream_t s) {
   if (w <= 0 || M <= 0) return cudaSuccess;
   if (w > W || M < w) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)W * US * sizeof(double);
+  const size_t smem = (size_t)W * kLeafG * (W / kLeafG + 2) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaError_t e =
