@@ -163,6 +163,15 @@ static int64_t kU12SplitRows = [] {
 // streamed host factor plan: PCIe copy rate and DMMA update rate (B200)
 static const double kHostCopyBps = 55e9, kUpdateFlops = 33e12;
 
+// U12 lookahead (EBV_U12_LA: -1 auto = n >= 16384, 0 off, 1 on): step K
+// updates block row K+1 first, and the side stream computes U12 of step K+1
+// (after panel K+1) while the main stream updates the rows below; see
+// lu_blocked.
+static int kU12La = [] {
+  const char* e = getenv("EBV_U12_LA");
+  return e ? atoi(e) : -1;
+}();
+
 static int64_t kTailRows = [] {
   const char* e = getenv("EBV_TAIL_ROWS");
   return e ? (int64_t)atoll(e) : (int64_t)0;
@@ -253,6 +262,8 @@ cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_
     if (e != cudaSuccess) return e;
   }
   auto clip = [](int64_t a, int64_t b) { return a < b ? a : b; };
+  const bool u12la = la && (kU12La >= 0 ? kU12La != 0 : n >= 16384);
+  bool u12_done = false;   // U12 of the current step was solved on the side stream
   {
     const int64_t w0 = step_w(0);
     e = panel_rec(c, clip(n, w0 + kl), w0, A, lda, 0, info, s);
@@ -275,20 +286,47 @@ cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_
       // lookahead: the update of panel K+1's columns first, then factor it on
       // the side stream while the rest of the trailing matrix is updated.
       // For large n U12 is split too, so panel K+1 need not wait for all of
-      // U12 (columns are independent: same bits).
+      // U12 (columns are independent: same bits).  With the U12 lookahead,
+      // U12 of this step was already computed on the side stream, and this
+      // step updates block row K+1 (the rows U12 of step K+1 is solved
+      // from) before the rows below, so the side stream solves U12 of step
+      // K+1 while the main stream updates the rest: the U12 solves leave the
+      // main stream's critical path.  Every entry still receives the same
+      // updates in the same order (row / column splits of one update do not
+      // change any entry's fma chain): bitwise the same factors.
       const bool split = kU12SplitRows >= 0 ? rest < kU12SplitRows : n >= 16384;
-      e = trsm_l(c, w, split ? w1 : Nbw, P, lda, P + w * lda, lda, s);
+      if (!u12_done) e = trsm_l(c, w, split ? w1 : Nbw, P, lda, P + w * lda, lda, s);
       if (e == cudaSuccess) e = gemm(c, Mb, w1, w, P + w, lda, P + w * lda, lda, P1, lda, false, s, KC_UPDATE);
       if (e == cudaSuccess) e = cudaEventRecord(c->ev_a, s);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_a, 0);
       if (e == cudaSuccess) e = panel_rec(c, Mp1, w1, P1, lda, c0 + w, info, c->side);
-      if (e == cudaSuccess) e = cudaEventRecord(c->ev_p, c->side);
-      if (e == cudaSuccess && split) e = trsm_l(c, w, Nbw - w1, P, lda, P + (w + w1) * lda, lda, s);
-      if (e == cudaSuccess)
-        e = gemm(c, Mb, Nbw - w1, w, P + w, lda, P + (w + w1) * lda, lda, P1 + w1 * lda, lda, false, s, KC_UPDATE);
+      if (e == cudaSuccess && split && !u12_done) e = trsm_l(c, w, Nbw - w1, P, lda, P + (w + w1) * lda, lda, s);
+      // the next step: its panel width, U12 columns and whether it takes this branch
+      const int64_t rest1 = rest - w1;
+      const int64_t w2 = rest1 > 0 ? step_w(c0 + w + w1) : 0;
+      const int64_t Nbw1 = clip(rest1, ku);
+      const bool next_la = rest1 > 0 && Nbw1 > w2;
+      if (e == cudaSuccess && u12la && next_la && Mb > w1) {
+        const int64_t w1r = w1;                       // block row K+1 (Mb > w1 rows exist)
+        e = gemm(c, w1r, Nbw - w1, w, P + w, lda, P + (w + w1) * lda, lda, P1 + w1 * lda, lda, false, s, KC_UPDATE);
+        if (e == cudaSuccess) e = cudaEventRecord(c->ev_b, s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_b, 0);
+        if (e == cudaSuccess) e = trsm_l(c, w1, Nbw1, P1, lda, P1 + w1 * lda, lda, c->side);   // U12 of step K+1
+        if (e == cudaSuccess) e = cudaEventRecord(c->ev_p, c->side);
+        if (e == cudaSuccess)
+          e = gemm(c, Mb - w1r, Nbw - w1, w, P + w + w1r, lda, P + (w + w1) * lda, lda, P1 + w1r + w1 * lda, lda,
+                   false, s, KC_UPDATE);
+        u12_done = true;
+      } else {
+        if (e == cudaSuccess) e = cudaEventRecord(c->ev_p, c->side);
+        if (e == cudaSuccess)
+          e = gemm(c, Mb, Nbw - w1, w, P + w, lda, P + (w + w1) * lda, lda, P1 + w1 * lda, lda, false, s, KC_UPDATE);
+        u12_done = false;
+      }
       if (e != cudaSuccess) return e;
     } else {
-      e = trsm_l(c, w, Nbw, P, lda, P + w * lda, lda, s);
+      if (!u12_done) e = trsm_l(c, w, Nbw, P, lda, P + w * lda, lda, s);
+      u12_done = false;
       if (e != cudaSuccess) return e;
       e = gemm(c, Mb, Nbw, w, P + w, lda, P + w * lda, lda, P1, lda, false, s, KC_UPDATE);
       if (e != cudaSuccess) return e;
@@ -576,6 +614,7 @@ ebv_status_t ebv_create(ebv_context_t* ctx, int device) {
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_p, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming);
   if (e != cudaSuccess) { cudaFree(base); delete c; *ctx = nullptr; return cuda_fail(e, "stream/event create"); }
   *ctx = c;
   return EBV_SUCCESS;
@@ -599,6 +638,7 @@ ebv_status_t ebv_destroy(ebv_context_t c) {
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_p) cudaEventDestroy(c->ev_p);
+  if (c->ev_b) cudaEventDestroy(c->ev_b);
   delete c;
   return EBV_SUCCESS;
 }

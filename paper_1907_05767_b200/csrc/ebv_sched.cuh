@@ -31,7 +31,7 @@ struct ebv_context {
   int vector_ctas = 0;      // 0 = auto; < 0 = cyclic map with |value| CTAs (for comparison)
   bool lookahead = true;    // factor panel K+1 on a side stream under the update of step K
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_start = nullptr, ev_a = nullptr, ev_p = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_a = nullptr, ev_p = nullptr, ev_b = nullptr;
   cudaStream_t copy = nullptr;            // host -> device column blocks (ebv_lu_factor_host)
   std::vector<cudaEvent_t> copy_ev;       // one per column block
   bool stats = false;

@@ -1,0 +1,36 @@
+"""Median time of ebv_lu_factor (default schedule, CUDA-graph replay) at the
+given orders: python scripts/factor_time.py 8192 16384 [--reps 5]"""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import argparse
+import json
+import torch
+import ebv_inputs
+import paper_1907_05767_b200 as ebv
+
+ap = argparse.ArgumentParser()
+ap.add_argument("n", type=int, nargs="+")
+ap.add_argument("--reps", type=int, default=5)
+a = ap.parse_args()
+dev = torch.device("cuda:0")
+ctx = ebv.Context(0)
+s = torch.cuda.Stream(dev)
+for n in a.n:
+    A0 = ebv_inputs.generate(n, seed=1, device=dev, with_b=False)["At"]
+    A = A0.clone()
+    info = torch.zeros((), dtype=torch.int64, device=dev)
+    ts = []
+    with torch.cuda.stream(s):
+        for r in range(a.reps + 3):
+            A.copy_(A0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            ebv.ebv_lu_factor(ctx.handle, n, A.data_ptr(), n, 0.0, info.data_ptr(), s.cuda_stream)
+            e1.record(s)
+            torch.cuda.synchronize()
+            if r >= 3:
+                ts.append(e0.elapsed_time(e1))
+    ts.sort()
+    print(json.dumps({"n": n, "ms_median": ts[len(ts) // 2], "ms_min": ts[0], "u12la": os.environ.get("EBV_U12_LA", "auto"),
+                      "tflops": 2 / 3 * n ** 3 / (ts[len(ts) // 2] * 1e-3) / 1e12}), flush=True)
+    del A, A0
