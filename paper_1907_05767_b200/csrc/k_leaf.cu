@@ -14,6 +14,7 @@
 // with an identity: padded multipliers are exactly 0 and fma(-0, u, a) == a,
 // so the real entries see exactly the same operation sequence.
 #include "ebv_internal.cuh"
+#include <cstdlib>
 
 namespace ebv {
 namespace {
@@ -364,6 +365,10 @@ __global__ void __launch_bounds__(W * GD) panel_leaf_kernel(int64_t M, int w, do
 // ---------------------------------------------------------------- U12 = L11^-1 A12
 // Group per column: step p, x_p is final (owner lane), broadcast; every lane
 // applies x_r = fma(-l_rp, x_p, x_r) to its rows r > p (unit diagonal).
+// CC columns per lane group (independent chains interleaved, the shared L
+// values loaded once for all of them): a CTA of 256 threads covers 32*CC
+// columns, so the kernel holds fewer SM slots beside the DMMA update.
+template <int CC>
 __global__ void __launch_bounds__(256) trsm_llu_kernel(int k, int64_t m, const double* __restrict__ L, int64_t ldl,
                                                        double* __restrict__ X, int64_t ldx) {
   __shared__ __align__(16) double sL[W * S];   // sL[p*S + r] = l(r, p), r > p
@@ -373,29 +378,44 @@ __global__ void __launch_bounds__(256) trsm_llu_kernel(int k, int64_t m, const d
   }
   __syncthreads();
   const int tid = threadIdx.x, j = tid % G, lane = tid & 31, base = lane & ~(G - 1);
-  const int64_t cidx = (int64_t)blockIdx.x * (256 / G) + tid / G;
-  const bool cv = cidx < m;
-  double* col = X + (cv ? cidx : 0) * ldx;
-  double x[Q];
+  const int64_t c0 = (int64_t)blockIdx.x * (256 / G) * CC + tid / G;   // columns c0 + 32 cc
+  double x[CC][Q];
+  bool cv[CC];
 #pragma unroll
-  for (int q = 0; q < Q; q++) {
-    const int r = j + G * q;
-    x[q] = (cv && r < k) ? col[r] : 0.0;
+  for (int cc = 0; cc < CC; cc++) {
+    const int64_t cidx = c0 + 32 * cc;
+    cv[cc] = cidx < m;
+    const double* col = X + (cv[cc] ? cidx : 0) * ldx;
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+      const int r = j + G * q;
+      x[cc][q] = (cv[cc] && r < k) ? col[r] : 0.0;
+    }
   }
 #pragma unroll
   for (int p = 0; p < W; p++) {
     const int o = p % G, qp = p / G;
     const double* lp = sL + p * S;
-    const double xp = __shfl_sync(0xffffffffu, x[qp], base + o);
+    double xp[CC];
+#pragma unroll
+    for (int cc = 0; cc < CC; cc++) xp[cc] = __shfl_sync(0xffffffffu, x[cc][qp], base + o);
 #pragma unroll
     for (int q = qp; q < Q; q++)
-      if (q > qp || j > o) x[q] = fma(-lp[j + G * q], xp, x[q]);
-  }
-  if (cv) {
+      if (q > qp || j > o) {
+        const double l = lp[j + G * q];
 #pragma unroll
-    for (int q = 0; q < Q; q++) {
-      const int r = j + G * q;
-      if (r < k) col[r] = x[q];
+        for (int cc = 0; cc < CC; cc++) x[cc][q] = fma(-l, xp[cc], x[cc][q]);
+      }
+  }
+#pragma unroll
+  for (int cc = 0; cc < CC; cc++) {
+    if (cv[cc]) {
+      double* col = X + (c0 + 32 * cc) * ldx;
+#pragma unroll
+      for (int q = 0; q < Q; q++) {
+        const int r = j + G * q;
+        if (r < k) col[r] = x[cc][q];
+      }
     }
   }
 }
@@ -478,7 +498,15 @@ cudaError_t launch_trsm_left_lower_unit(int64_t k, int64_t m, const double* L, i
                                         int64_t ldx, cudaStream_t s) {
   if (m <= 0 || k <= 0) return cudaSuccess;
   if (k > W) return cudaErrorInvalidValue;
-  trsm_llu_kernel<<<(unsigned)((m + 31) / 32), 256, 0, s>>>((int)k, m, L, ldl, X, ldx);
+  static const int cc = [] {
+    const char* e = getenv("EBV_TRSM_LLU_CC");
+    return e ? atoi(e) : 2;
+  }();
+  if (cc == 2) {
+    trsm_llu_kernel<2><<<(unsigned)((m + 63) / 64), 256, 0, s>>>((int)k, m, L, ldl, X, ldx);
+    return cudaGetLastError();
+  }
+  trsm_llu_kernel<1><<<(unsigned)((m + 31) / 32), 256, 0, s>>>((int)k, m, L, ldl, X, ldx);
   return cudaGetLastError();
 }
 
