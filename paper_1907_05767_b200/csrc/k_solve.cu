@@ -80,21 +80,23 @@ __device__ __forceinline__ unsigned long long gtime() {
 // ties and non-normal q count as unverified.  The caller redoes the block
 // with true division if any step is unverified, so the result is always
 // RN(y/u), bitwise the oracle's division.
-__device__ __forceinline__ double quot(double y, double u, double r, bool own, bool& ok) {
+__device__ __forceinline__ double quot_nc(double y, double u, double r) {
   const double q0 = y * r;
-  const double q = fma(r, fma(-u, q0, y), q0);
-  if (own) {
-    const double rr = fma(-u, q, y);                               // exact remainder y - q u
-    const long long qb = __double_as_longlong(q);
-    const long long e = qb & 0x7ff0000000000000LL;
-    const bool normal = e > (54LL << 52) && e < (0x7feLL << 52);
-    double lim = fabs(u) * __longlong_as_double(e - (53LL << 52));   // |u| ulp(q) / 2, exact
-    const bool below = (rr < 0.0) != (u < 0.0);                      // true quotient < |q| side
-    const bool pow2 = (qb & 0x000fffffffffffffLL) == 0;
-    if (pow2 && below == (q > 0.0)) lim *= 0.5;                      // toward zero from 2^e
-    ok = ok && normal && fabs(rr) < lim;
-  }
-  return q;
+  return fma(r, fma(-u, q0, y), q0);
+}
+// the exact test, applied after the block's sweep (off the step chain: the
+// owner lane keeps its step's dividend and quotient)
+__device__ __forceinline__ bool quot_chk(double y, double u, double q) {
+  const double rr = fma(-u, q, y);                                 // exact remainder y - q u
+  const long long qb = __double_as_longlong(q);
+  const long long e = qb & 0x7ff0000000000000LL;
+  const bool normal = e > (54LL << 52) && e < (0x7feLL << 52);
+  double lim = fabs(u) * __longlong_as_double(e - (53LL << 52));     // |u| ulp(q) / 2, exact
+  const bool below = (rr < 0.0) != (u < 0.0);                        // true quotient < |q| side
+  const bool pow2 = (qb & 0x000fffffffffffffLL) == 0;
+  if (pow2 && below == (q > 0.0)) lim *= 0.5;                        // toward zero from 2^e
+  const bool pzero = __double_as_longlong(y) == 0;                   // +0 / u: exact (skipped steps)
+  return pzero || (normal && fabs(rr) < lim);
 }
 
 // Window form (the multi-GPU ring solve, ebv_dist.cu): only the column
@@ -262,7 +264,9 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
         double w0[HR], w1[HR];
 #pragma unroll
         for (int q = 0; q < HR; q++) { w0[q] = v0[q]; w1[q] = v1[q]; }
-        bool ok = true;
+        double yo0[HR], qo0[HR], yo1[HR], qo1[HR];   // the owned steps' dividends / quotients
+#pragma unroll
+        for (int q = 0; q < HR; q++) { yo0[q] = 0.0; qo0[q] = 0.0; yo1[q] = 0.0; qo1[q] = 0.0; }
         for (int k = BR - 1; k >= 32; k--) {
           if (k >= nv) continue;
           const double ukk = st[k * TSTR + k];
@@ -272,7 +276,9 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
 #pragma unroll
           for (int q = 0; q < HR; q++) {
             if (NR == 1 && q > 0) break;
-            const double xk = __shfl_sync(0xffffffffu, quot(v1[q], ukk, rk, own && q < myr, ok), k - 32);
+            const double qv = quot_nc(v1[q], ukk, rk);
+            if (own) { yo1[q] = v1[q]; qo1[q] = qv; }
+            const double xk = __shfl_sync(0xffffffffu, qv, k - 32);
             v1[q] = own ? xk : (b1 ? fma(-u1, xk, v1[q]) : v1[q]);
             v0[q] = fma(-u0, xk, v0[q]);
           }
@@ -286,8 +292,19 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
 #pragma unroll
           for (int q = 0; q < HR; q++) {
             if (NR == 1 && q > 0) break;
-            const double xk = __shfl_sync(0xffffffffu, quot(v0[q], ukk, rk, own && q < myr, ok), k);
+            const double qv = quot_nc(v0[q], ukk, rk);
+            if (own) { yo0[q] = v0[q]; qo0[q] = qv; }
+            const double xk = __shfl_sync(0xffffffffu, qv, k);
             v0[q] = own ? xk : (b0 ? fma(-u0, xk, v0[q]) : v0[q]);
+          }
+        }
+        bool ok = true;
+        {
+          const double d0 = st[lane * TSTR + lane], d1 = st[(lane + 32) * TSTR + lane + 32];
+#pragma unroll
+          for (int q = 0; q < HR; q++) {
+            if (NR == 1 && q > 0) break;
+            if (q < myr) ok = ok && quot_chk(yo0[q], d0, qo0[q]) && quot_chk(yo1[q], d1, qo1[q]);
           }
         }
         // any unverified quotient (checked by its owner lane) -> redo the
