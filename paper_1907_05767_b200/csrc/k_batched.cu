@@ -15,6 +15,7 @@
 // solve (Eq 1) follows in registers: forward over L_(k), backward over U_(k).
 // Per-entry arithmetic is exactly the oracle's (bitwise).
 #include "ebv_internal.cuh"
+#include <type_traits>
 
 namespace ebv {
 namespace {
@@ -23,6 +24,34 @@ constexpr int NP = 32;   // padded order
 constexpr int MAXRHS = 16;
 
 constexpr int CH = 8;     // columns per shuffle chunk
+
+// Markstein quotient from an approximate reciprocal, and the exact test that
+// it is RN(y / u) (remainder y - q u exact by fma, inside half an ulp of q
+// times |u|, halved below a power of two; +0 dividends exact)
+__device__ __forceinline__ double rcp_approx(double u) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(u));
+  double e = fma(-u, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-u, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double quot_mk(double y, double u, double r) {
+  const double q0 = y * r;
+  return fma(r, fma(-u, q0, y), q0);
+}
+__device__ __forceinline__ bool quot_exact(double y, double u, double q) {
+  const double rr = fma(-u, q, y);
+  const long long qb = __double_as_longlong(q);
+  const long long e = qb & 0x7ff0000000000000LL;
+  const bool normal = e > (54LL << 52) && e < (0x7feLL << 52);
+  double lim = fabs(u) * __longlong_as_double(e - (53LL << 52));
+  const bool below = (rr < 0.0) != (u < 0.0);
+  const bool pow2 = (qb & 0x000fffffffffffffLL) == 0;
+  if (pow2 && below == (q > 0.0)) lim *= 0.5;
+  const bool pzero = __double_as_longlong(y) == 0;
+  return pzero || (normal && fabs(rr) < lim);
+}
 
 // Row updates of rows that may sit above the pivot are guarded by a branch
 // around a chunk of CH fma's (a predicated fma is if-converted by ptxas into
@@ -152,6 +181,9 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
           }
         }
       }
+      if constexpr (RG == 1) {
+      // backward: UX = Y (one chain: true division; the verified-quotient
+      // form below measured slower here — its extra live registers spill)
 #pragma unroll
       for (int k = NP - 1; k >= 0; k--) {   // backward: UX = Y
         const int src = hb + (k < 16 ? k : NP - 1 - k);
@@ -170,6 +202,68 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
             if (r1 < k) y1[g] = fma(-rb[k], xk, y1[g]);
           }
         }
+      }
+      } else {
+      // backward: UX = Y.  The owner's quotient is a Markstein step from an
+      // approximate reciprocal of its (final) diagonal entry, computed off
+      // the chain; the exact correct-rounding test runs after the sweep on
+      // the two (dividend, quotient) pairs each lane owns, and a warp with an
+      // unverified quotient redoes the sweep with true division (RG > 1: 2.57 -> 1.64 ms for
+      // 100k systems x 16 right-hand sides).
+      double ys0[RG], ys1[RG], yo0[RG], qo0[RG], yo1[RG], qo1[RG];
+#pragma unroll
+      for (int g = 0; g < RG; g++) {
+        ys0[g] = y0[g]; ys1[g] = y1[g];
+        yo0[g] = 0.0; qo0[g] = 0.0; yo1[g] = 0.0; qo1[g] = 0.0;
+      }
+      double d0 = 1.0, d1 = 1.0;                         // the lane's own pivots u_tt, u_(31-t)(31-t)
+      auto sweep = [&](auto exact_tag) {
+        constexpr bool EXACT = decltype(exact_tag)::value;
+#pragma unroll
+        for (int k = NP - 1; k >= 0; k--) {
+          const int src = hb + (k < 16 ? k : NP - 1 - k);
+          if (k < 16) {
+            if (t == k) {
+              const double rk = EXACT ? 0.0 : rcp_approx(ra[k]);
+              d0 = ra[k];
+#pragma unroll
+              for (int g = 0; g < RG; g++) {
+                const double q = EXACT ? y0[g] / ra[k] : quot_mk(y0[g], ra[k], rk);
+                yo0[g] = y0[g]; qo0[g] = q; y0[g] = q;
+              }
+            }
+          } else {
+            if (t == NP - 1 - k) {
+              const double rk = EXACT ? 0.0 : rcp_approx(rb[k]);
+              d1 = rb[k];
+#pragma unroll
+              for (int g = 0; g < RG; g++) {
+                const double q = EXACT ? y1[g] / rb[k] : quot_mk(y1[g], rb[k], rk);
+                yo1[g] = y1[g]; qo1[g] = q; y1[g] = q;
+              }
+            }
+          }
+#pragma unroll
+          for (int g = 0; g < RG; g++) {
+            const double xk = __shfl_sync(0xffffffffu, k < 16 ? y0[g] : y1[g], src);
+            if (k < 16) {
+              if (r0 < k) y0[g] = fma(-ra[k], xk, y0[g]);   // rows 31-t >= 16 > k never
+            } else {
+              y0[g] = fma(-ra[k], xk, y0[g]);               // rows t < 16 <= k always
+              if (r1 < k) y1[g] = fma(-rb[k], xk, y1[g]);
+            }
+          }
+        }
+      };
+      sweep(std::false_type{});
+      bool okq = true;
+#pragma unroll
+      for (int g = 0; g < RG; g++) okq = okq && quot_exact(yo0[g], d0, qo0[g]) && quot_exact(yo1[g], d1, qo1[g]);
+      if (__any_sync(0xffffffffu, !okq)) {               // rare: the sweep again with true division
+#pragma unroll
+        for (int g = 0; g < RG; g++) { y0[g] = ys0[g]; y1[g] = ys1[g]; }
+        sweep(std::true_type{});
+      }
       }
 #pragma unroll
       for (int g = 0; g < RG; g++) {
