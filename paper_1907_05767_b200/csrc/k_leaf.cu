@@ -378,7 +378,11 @@ __global__ void __launch_bounds__(256) trsm_llu_kernel(int k, int64_t m, const d
   }
   __syncthreads();
   const int tid = threadIdx.x, j = tid % G, lane = tid & 31, base = lane & ~(G - 1);
-  const int64_t c0 = (int64_t)blockIdx.x * (256 / G) * CC + tid / G;   // columns c0 + 32 cc
+  // grid-stride over chunks of 32*CC columns (the grid may be capped so the
+  // solve holds fewer SM slots beside the update; L11 is staged once per CTA)
+  const int64_t nchunks = (m + 32 * CC - 1) / (32 * CC);
+  for (int64_t chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
+  const int64_t c0 = chunk * (256 / G) * CC + tid / G;   // columns c0 + 32 cc
   double x[CC][Q];
   bool cv[CC];
 #pragma unroll
@@ -417,6 +421,7 @@ __global__ void __launch_bounds__(256) trsm_llu_kernel(int k, int64_t m, const d
         if (r < k) col[r] = x[cc][q];
       }
     }
+  }
   }
 }
 
@@ -503,7 +508,13 @@ cudaError_t launch_trsm_left_lower_unit(int64_t k, int64_t m, const double* L, i
     return e ? atoi(e) : 2;
   }();
   if (cc == 2) {
-    trsm_llu_kernel<2><<<(unsigned)((m + 63) / 64), 256, 0, s>>>((int)k, m, L, ldl, X, ldx);
+    static const int64_t gcap = [] {
+      const char* e = getenv("EBV_TRSM_LLU_GRID");
+      return e ? (int64_t)atoll(e) : (int64_t)0;
+    }();
+    int64_t grid = (m + 63) / 64;
+    if (gcap > 0 && grid > gcap) grid = gcap;
+    trsm_llu_kernel<2><<<(unsigned)grid, 256, 0, s>>>((int)k, m, L, ldl, X, ldx);
     return cudaGetLastError();
   }
   trsm_llu_kernel<1><<<(unsigned)((m + 31) / 32), 256, 0, s>>>((int)k, m, L, ldl, X, ldx);
