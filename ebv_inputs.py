@@ -210,3 +210,34 @@ def generate_leading(n: int, m: int, seed: int = 1, nrhs: int = 1, device="cpu",
     At = K.to(torch.float64) * SCALE
     At[jj, jj] = dunits.to(torch.float64) * SCALE
     return {"At": At, "X": X_u.to(torch.float64), "B": B_u.to(torch.float64) * SCALE, "n": m}
+
+
+def generate_band(n: int, kl: int, ku: int, pad: int, ldab: int, seed: int = 1, nrhs: int = 1, device="cpu",
+                  system: int = 0):
+    """The banded matrix of ``generate(n, seed, kl=kl, ku=ku)`` (the same
+    entries bit for bit) written directly in compact band storage, so orders
+    whose dense storage would not fit can be generated: returns dict(AB=(n,
+    ldab) float64 whose row j is column j of the ldab x n column-major band
+    storage, a_ij at AB[j, pad + ku + i - j] — the layout of include/ebv.h —
+    X, B as generate).  Layout only; no arithmetic of the method."""
+    dev = torch.device(device)
+    base = system_base(seed, system)
+    j = torch.arange(n, dtype=torch.int64, device=dev)
+    rr = torch.arange(nrhs, dtype=torch.int64, device=dev)
+    X_u = xtrue_units(base, j[:, None], rr[None, :], n)                 # (n, nrhs)
+    AB = torch.zeros(n, ldab, dtype=torch.float64, device=dev)
+    rowsum = torch.zeros(n, dtype=torch.int64, device=dev)
+    rowdot = torch.zeros(n, nrhs, dtype=torch.int64, device=dev)
+    for d in range(-ku, kl + 1):                                         # diagonal d = i - j
+        if d == 0:
+            continue
+        jj = j[(j + d >= 0) & (j + d < n)]
+        ii = jj + d
+        K = offdiag_units(base, ii, jj)
+        AB[jj, pad + ku + d] = K.to(torch.float64) * SCALE
+        rowsum.index_add_(0, ii, K.abs())
+        rowdot.index_add_(0, ii, K[:, None] * X_u[jj])
+    dunits = rowsum + ONE_UNITS
+    AB[j, pad + ku] = dunits.to(torch.float64) * SCALE
+    B_u = rowdot + dunits[:, None] * X_u
+    return {"AB": AB, "X": X_u.to(torch.float64), "B": B_u.to(torch.float64) * SCALE, "n": n, "seed": seed}

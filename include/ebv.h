@@ -222,6 +222,28 @@ ebv_status_t ebv_lu_factor_banded(ebv_context_t ctx, int64_t n, int64_t kl, int6
 ebv_status_t ebv_lu_solve_banded(ebv_context_t ctx, int64_t n, int64_t kl, int64_t ku, const double* LU,
                                  int64_t lda, double* B, int64_t ldb, int64_t nrhs, void* stream);
 
+/* Banded systems in compact band storage (memory
+ * ~ n*(kl+ku) instead of n^2, so orders far beyond the dense limit fit).
+ * AB is ldab x n column-major (device, caller-owned); entry a_ij of the band
+ * (max(0, j-ku) <= i <= min(n-1, j+kl)) lives at
+ *     AB[(EBV_BAND_PAD + ku + i - j) + j*ldab],
+ * i.e. LAPACK's band layout with EBV_BAND_PAD extra rows above and below:
+ * the blocked schedule works on 64-column steps whose panels, U12 blocks and
+ * solve tiles reach up to EBV_BAND_PAD entries past the band (exact zeros).
+ * Requires ldab >= kl + ku + 2*EBV_BAND_PAD + 1 and every entry of AB outside
+ * the band zero on entry.  The factor overwrites the band with L\U in the
+ * same layout (padding entries may become +-0); the factors in the band are
+ * bitwise ebv_lu_factor_banded's on the same matrix in dense storage.  The
+ * pivot threshold must be explicit (tau >= 0: the tau < 0 norm rule needs
+ * the dense layout).  The solve (Eq 1) overwrites B (n x nrhs, ldb) with X.
+ * Errors: INVALID_VALUE (negative sizes, ldab too small, tau < 0, NULL
+ * pointers), plus the conditions of ebv_lu_factor / ebv_lu_solve. */
+#define EBV_BAND_PAD 128
+ebv_status_t ebv_lu_factor_band(ebv_context_t ctx, int64_t n, int64_t kl, int64_t ku, double* AB,
+                                int64_t ldab, double tau, int64_t* d_info, void* stream);
+ebv_status_t ebv_lu_solve_band(ebv_context_t ctx, int64_t n, int64_t kl, int64_t ku, const double* AB,
+                               int64_t ldab, double* B, int64_t ldb, int64_t nrhs, void* stream);
+
 /* Solve only, for batched systems factored earlier by ebv_lu_factor_batched
  * (factor once, solve many — SURVEY §8f f1): for each system s,
  * B_s <- U_s^-1 (L_s^-1 B_s) with the packed LU_s = LU + s*strideA (read

@@ -28,6 +28,7 @@ LIB_PATH = os.path.join(_HERE, "libebv.so")
 EBV_SUCCESS = 0
 EBV_PATH_AUTO, EBV_PATH_VECTOR, EBV_PATH_BLOCKED, EBV_PATH_LEFT = 0, 1, 2, 3
 EBV_LAYOUT_CYCLIC, EBV_LAYOUT_EBVPAIR, EBV_LAYOUT_SNAKE = 0, 1, 2
+EBV_BAND_PAD = 128   # include/ebv.h: padding rows above and below the band in compact band storage
 KCLASSES = ["gemm_dmma", "leaf_lu", "trsm", "solve", "batched", "vector", "other", "update"]
 
 # every exported symbol of include/ebv.h with its ctypes signature
@@ -44,6 +45,8 @@ SIGNATURES = {
     "ebv_block_width": (_i64, [_vp, _i64]),
     "ebv_lu_factor_banded": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _d, _vp, _vp]),
     "ebv_lu_solve_banded": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _vp]),
+    "ebv_lu_factor_band": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _d, _vp, _vp]),
+    "ebv_lu_solve_band": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _vp]),
     "ebv_batched_shard": (_int, [_i64, _int, _int, _vp, _vp]),
     "ebv_lu_factor_host": (_int, [_vp, _i64, _vp, _i64, _vp, _i64, _d, _vp, _vp]),
     "ebv_stats_timeline": (_i64, [_vp, _vp, _i64]),
@@ -206,6 +209,70 @@ def lu_solve_banded(LU: torch.Tensor, B: torch.Tensor, kl: int, ku: int, ctx: Co
     X = B.reshape(n, -1).mT.contiguous().mT.clone()
     _check(ebv_lu_solve_banded(ctx.handle, n, kl, ku, LU.data_ptr(), max(_colmajor_ld(LU), 1), X.data_ptr(),
                                max(n, 1), X.shape[1], _stream_handle(LU.device)), "ebv_lu_solve_banded")
+    return X[:, 0] if vec else X
+
+
+def ebv_lu_factor_band(ctx, n, kl, ku, AB, ldab, tau, d_info, stream):
+    return lib().ebv_lu_factor_band(ctx, n, kl, ku, AB, ldab, tau, d_info, stream)
+
+
+def ebv_lu_solve_band(ctx, n, kl, ku, AB, ldab, B, ldb, nrhs, stream):
+    return lib().ebv_lu_solve_band(ctx, n, kl, ku, AB, ldab, B, ldb, nrhs, stream)
+
+
+def band_ld(kl: int, ku: int) -> int:
+    """Smallest leading dimension of compact band storage (odd, so the dense
+    view's leading dimension ldab - 1 is even and TMA-eligible)."""
+    ld = kl + ku + 2 * EBV_BAND_PAD + 1
+    return ld if ld % 2 == 1 else ld + 1
+
+
+def band_pack(A: torch.Tensor, kl: int, ku: int, ldab: int | None = None) -> torch.Tensor:
+    """Compact band storage of a dense (n, n) A (layout of include/ebv.h:
+    a_ij at AB[PAD + ku + i - j, j]); returns AB as a (n, ldab) tensor whose
+    row j is column j of the (ldab x n) column-major storage.  Layout only."""
+    n = A.shape[0]
+    ldab = ldab or band_ld(kl, ku)
+    AB = torch.zeros(n, ldab, dtype=A.dtype, device=A.device)
+    j = torch.arange(n, device=A.device)
+    for d in range(-ku, kl + 1):   # diagonal d = i - j
+        jj = j[(j + d >= 0) & (j + d < n)]
+        AB[jj, EBV_BAND_PAD + ku + d] = A[jj + d, jj]
+    return AB
+
+
+def band_unpack(AB: torch.Tensor, n: int, kl: int, ku: int) -> torch.Tensor:
+    """Dense (n, n) matrix holding the band of AB (zeros elsewhere).  Layout only."""
+    A = torch.zeros(n, n, dtype=AB.dtype, device=AB.device)
+    j = torch.arange(n, device=AB.device)
+    for d in range(-ku, kl + 1):
+        jj = j[(j + d >= 0) & (j + d < n)]
+        A[jj + d, jj] = AB[jj, EBV_BAND_PAD + ku + d]
+    return A
+
+
+def lu_factor_band(AB: torch.Tensor, n: int, kl: int, ku: int, tau: float = 0.0, ctx: Context | None = None):
+    """In-place LU of a band-stored matrix (AB from band_pack: (n, ldab),
+    contiguous); returns (AB, info)."""
+    _require(AB, "AB")
+    if not AB.is_contiguous() or AB.shape[0] != n:
+        raise EbvError("AB must be a contiguous (n, ldab) tensor (band_pack layout)")
+    ctx = ctx or default_context(AB.device.index or 0)
+    info = torch.zeros((), dtype=torch.int64, device=AB.device)
+    _check(ebv_lu_factor_band(ctx.handle, n, kl, ku, AB.data_ptr(), AB.shape[1], float(tau), info.data_ptr(),
+                              _stream_handle(AB.device)), "ebv_lu_factor_band")
+    return AB, info
+
+
+def lu_solve_band(AB: torch.Tensor, B: torch.Tensor, kl: int, ku: int, ctx: Context | None = None):
+    """X from band-stored factors (AB as returned by lu_factor_band); B (n,) or (n, nrhs)."""
+    _require(AB, "AB")
+    n = AB.shape[0]
+    ctx = ctx or default_context(AB.device.index or 0)
+    vec = B.dim() == 1
+    X = B.reshape(n, -1).mT.contiguous().mT.clone()
+    _check(ebv_lu_solve_band(ctx.handle, n, kl, ku, AB.data_ptr(), AB.shape[1], X.data_ptr(), max(n, 1),
+                             X.shape[1], _stream_handle(AB.device)), "ebv_lu_solve_band")
     return X[:, 0] if vec else X
 
 

@@ -245,12 +245,14 @@ static int64_t step_width(const ebv_context* c, int64_t n, int64_t c0) {
 // (fma(-0, u, +0) == +0), so the factors inside the band are bitwise the
 // dense ones.  kl = ku = n - 1 is the dense schedule.
 cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s,
-                       int64_t kl, int64_t ku) {
+                       int64_t kl, int64_t ku, bool band_storage) {
   if (kl < 0 || kl > n) kl = n;
   if (ku < 0 || ku > n) ku = n;
   // narrow bands: 64-wide panels (the per-step windows are ~band-sized;
-  // measured n = 65536, kl = ku = 256: 61.8 ms at nb = 64, 98.9 at 512)
-  const bool narrow = c->nb <= 0 && kl + ku < n / 4;
+  // measured n = 65536, kl = ku = 256: 61.8 ms at nb = 64, 98.9 at 512).
+  // Compact band storage always takes 64-wide steps: its padding
+  // (EBV_BAND_PAD) covers how far a 64-column step reaches past the band.
+  const bool narrow = band_storage || (c->nb <= 0 && kl + ku < n / 4);
   const int64_t nb = narrow ? ((64 + c->leaf - 1) / c->leaf) * c->leaf : block_width(c, n);
   auto step_w = [&](int64_t c0) { return narrow ? ((n - c0) < nb ? (n - c0) : nb) : step_width(c, n, c0); };
   const bool la = c->lookahead && n > 2 * nb;
@@ -874,13 +876,49 @@ ebv_status_t ebv_lu_factor_banded(ebv_context_t c, int64_t n, int64_t kl, int64_
   return EBV_SUCCESS;
 }
 
-ebv_status_t ebv_lu_solve_banded(ebv_context_t c, int64_t n, int64_t kl, int64_t ku, const double* LU, int64_t lda,
-                                 double* B, int64_t ldb, int64_t nrhs, void* stream) {
-  if (!c) return invalid("ebv_lu_solve_banded: NULL ctx");
-  if (n < 0 || nrhs < 0 || kl < 0 || ku < 0) return invalid("ebv_lu_solve_banded: negative size");
-  if (lda < (n > 1 ? n : 1) || ldb < (n > 1 ? n : 1)) return invalid("ebv_lu_solve_banded: leading dimension");
+static ebv_status_t solve_banded_impl(ebv_context_t c, int64_t n, int64_t kl, int64_t ku, const double* LU,
+                                      int64_t lda, double* B, int64_t ldb, int64_t nrhs, void* stream);
+
+// Compact band storage: AB[(PAD + ku + i - j) + j*ldab] = a_ij is the dense
+// column-major view A = AB + PAD + ku with leading dimension ldab - 1 (entry
+// (i, j) at A[i + j*(ldab - 1)]); every entry the 64-column banded schedule
+// and the tile-skipping solve touch has |offset from the band| <= PAD, so it
+// maps into its own column's slot (no aliasing) and holds an exact zero.
+ebv_status_t ebv_lu_factor_band(ebv_context_t c, int64_t n, int64_t kl, int64_t ku, double* AB, int64_t ldab,
+                                double tau, int64_t* d_info, void* stream) {
+  if (!c) return invalid("ebv_lu_factor_band: NULL ctx");
+  if (n < 0 || kl < 0 || ku < 0) return invalid("ebv_lu_factor_band: negative size");
+  if (ldab < kl + ku + 2 * EBV_BAND_PAD + 1) return invalid("ebv_lu_factor_band: ldab < kl + ku + 2*EBV_BAND_PAD + 1");
+  if (!(tau >= 0)) return invalid("ebv_lu_factor_band: tau must be >= 0 (explicit threshold)");
+  if (!d_info) return invalid("ebv_lu_factor_band: d_info is NULL");
+  if (n > 0 && !AB) return invalid("ebv_lu_factor_band: AB is NULL");
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = timed(c, KC_OTHER, 0, 0, s, 1, [&] { return launch_set_info0(d_info, s); });
+  if (e != cudaSuccess) return cuda_fail(e, "info init");
+  if (n == 0) return EBV_SUCCESS;
+  double* A = AB + EBV_BAND_PAD + ku;
+  const int64_t lda = ldab - 1;
+  e = timed(c, KC_OTHER, 0, 0, s, 1, [&] { return launch_tau(n, A, lda, tau, c->d_tau, c->d_norm, s); });
+  if (e != cudaSuccess) return cuda_fail(e, "tau");
+  e = lu_blocked(c, n, A, lda, d_info, s, kl, ku, true);
+  if (e != cudaSuccess) return cuda_fail(e, "band factor");
+  return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_lu_solve_band(ebv_context_t c, int64_t n, int64_t kl, int64_t ku, const double* AB, int64_t ldab,
+                               double* B, int64_t ldb, int64_t nrhs, void* stream) {
+  if (!c) return invalid("ebv_lu_solve_band: NULL ctx");
+  if (n < 0 || nrhs < 0 || kl < 0 || ku < 0) return invalid("ebv_lu_solve_band: negative size");
+  if (ldab < kl + ku + 2 * EBV_BAND_PAD + 1) return invalid("ebv_lu_solve_band: ldab < kl + ku + 2*EBV_BAND_PAD + 1");
+  if (ldb < (n > 1 ? n : 1)) return invalid("ebv_lu_solve_band: ldb < max(1, n)");
   if (n == 0 || nrhs == 0) return EBV_SUCCESS;
-  if (!LU || !B) return invalid("ebv_lu_solve_banded: NULL pointer");
+  if (!AB || !B) return invalid("ebv_lu_solve_band: NULL pointer");
+  return solve_banded_impl(c, n, kl, ku, AB + EBV_BAND_PAD + ku, ldab - 1, B, ldb, nrhs, stream);
+}
+
+static ebv_status_t solve_banded_impl(ebv_context_t c, int64_t n, int64_t kl, int64_t ku, const double* LU,
+                                      int64_t lda, double* B, int64_t ldb, int64_t nrhs, void* stream) {
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t NB = (n + solve_block_rows() - 1) / solve_block_rows();
@@ -894,6 +932,16 @@ ebv_status_t ebv_lu_solve_banded(ebv_context_t c, int64_t n, int64_t kl, int64_t
   });
   if (e != cudaSuccess) return cuda_fail(e, "banded solve");
   return EBV_SUCCESS;
+}
+
+ebv_status_t ebv_lu_solve_banded(ebv_context_t c, int64_t n, int64_t kl, int64_t ku, const double* LU, int64_t lda,
+                                 double* B, int64_t ldb, int64_t nrhs, void* stream) {
+  if (!c) return invalid("ebv_lu_solve_banded: NULL ctx");
+  if (n < 0 || nrhs < 0 || kl < 0 || ku < 0) return invalid("ebv_lu_solve_banded: negative size");
+  if (lda < (n > 1 ? n : 1) || ldb < (n > 1 ? n : 1)) return invalid("ebv_lu_solve_banded: leading dimension");
+  if (n == 0 || nrhs == 0) return EBV_SUCCESS;
+  if (!LU || !B) return invalid("ebv_lu_solve_banded: NULL pointer");
+  return solve_banded_impl(c, n, kl, ku, LU, lda, B, ldb, nrhs, stream);
 }
 
 ebv_status_t ebv_lu_factor_batched(ebv_context_t c, int64_t n, double* A, int64_t lda, int64_t strideA,

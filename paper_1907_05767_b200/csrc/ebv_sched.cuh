@@ -110,7 +110,7 @@ cudaError_t lu_rec(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t ko
 cudaError_t panel_rec(ebv_context* c, int64_t M, int64_t w, double* P, int64_t lda, int64_t koff, int64_t* info,
                       cudaStream_t s);
 cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s,
-                       int64_t kl, int64_t ku);
+                       int64_t kl, int64_t ku, bool band_storage = false);
 cudaError_t lu_left(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s,
                     const double* hA, int64_t ldh);
 cudaError_t lu_blocked_stream(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s,

@@ -181,3 +181,26 @@ for m in (128, 256):
     emit(config="f4-stencil", n=n, m=m, what="banded solve (zero-skip)", ms=med2, ms_min=lo2, ms_max=hi2,
          max_err=(Bw.T - X).abs().max().item())
     del A0, Aw, Bs, Bw, X
+
+# ---------------- f4: compact band storage (ebv_lu_factor_band): memory ~ n (kl + ku)
+for n, kl, ku in ((65536, 256, 256), (262144, 128, 128), (1048576, 64, 64)):
+    ld = ebv.band_ld(kl, ku)
+    g = ebv_inputs.generate_band(n, kl, ku, ebv.EBV_BAND_PAD, ld, seed=1, device=dev)
+    AB0 = g["AB"]
+    ABw = torch.empty_like(AB0)
+    Bs = g["B"].T.contiguous()
+    Bw = torch.empty_like(Bs)
+    X = g["X"]
+    del g
+    med, lo, hi = timeit(lambda: ABw.copy_(AB0),
+                         lambda: ebv.ebv_lu_factor_band(ctx.handle, n, kl, ku, ABw.data_ptr(), ld, 0.0,
+                                                        info.data_ptr(), sh))
+    emit(config="f4-band-storage", n=n, kl=kl, ku=ku, ldab=ld, storage_gb=8.0 * n * ld / 1e9,
+         dense_storage_gb=8.0 * n * n / 1e9, what="band factor (compact storage)", ms=med, ms_min=lo, ms_max=hi,
+         gflops_band=2.0 * n * kl * ku / med / 1e6, info_ok=int(info) == 0)
+    med2, lo2, hi2 = timeit(lambda: Bw.copy_(Bs),
+                            lambda: ebv.ebv_lu_solve_band(ctx.handle, n, kl, ku, ABw.data_ptr(), ld, Bw.data_ptr(),
+                                                          n, 1, sh))
+    emit(config="f4-band-storage", n=n, kl=kl, ku=ku, what="band solve (compact storage)", ms=med2, ms_min=lo2,
+         ms_max=hi2, max_err=(Bw.T - X).abs().max().item())
+    del AB0, ABw, Bs, Bw, X
