@@ -43,6 +43,13 @@ for n, nb in ((700, 64), (1100, 128), (1300, 256)):
     torch.cuda.synchronize()
     lu_o, _ = oracle.lu_factor(A.cpu().numpy())
     assert bits(LU.cpu().numpy(), lu_o), (n, nb)
+for n, kl, ku in ((600, 20, 33), (1000, 87, 5), (500, 3, 120)):
+    d = ebv_inputs.generate(n, seed=n + kl, device=dev, kl=kl, ku=ku)
+    A = d["At"].T
+    LU, info = ebv.lu_factor_banded(A, kl, ku, ctx=ctx)
+    torch.cuda.synchronize()
+    lu_o, _ = oracle.lu_factor(A.cpu().numpy())
+    assert bits(LU.cpu().numpy(), lu_o), ("banded", n, kl, ku)
 print("OK")
 """
 
