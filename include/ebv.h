@@ -87,7 +87,8 @@ typedef struct ebv_context* ebv_context_t;
 typedef enum { EBV_PATH_AUTO = 0, EBV_PATH_VECTOR = 1, EBV_PATH_BLOCKED = 2, EBV_PATH_LEFT = 3 } ebv_path_t;
 
 #define EBV_VECTOR_MAX_N 1536
-#define EBV_BATCHED_MAX_N 64
+#define EBV_BATCHED_MAX_N 64          /* register-resident kernels (one or two systems per warp / CTA) */
+#define EBV_BATCHED_MEDIUM_MAX_N 512  /* batched blocked schedule beyond that */
 
 /* Column-block -> rank layouts for a 1D distribution:
  * CYCLIC = J mod P; EBVPAIR = block pairs (J, N-1-J) dealt round-robin
@@ -200,7 +201,11 @@ ebv_status_t ebv_lu_solve(ebv_context_t ctx, int64_t n, const double* LU, int64_
  * system (the paper's first-with-last pairing, Eq 7, at lane granularity).
  * Sharding across GPUs = the caller passes its shard's pointers.
  * Errors: INVALID_VALUE (n < 0, batch < 0, lda < n, strides too small,
- * NULL pointers); NOT_SUPPORTED for n > EBV_BATCHED_MAX_N or nrhs > 16. */
+ * NULL pointers); NOT_SUPPORTED for n > EBV_BATCHED_MEDIUM_MAX_N or
+ * nrhs > 16.  Orders EBV_BATCHED_MAX_N < n <= EBV_BATCHED_MEDIUM_MAX_N (SURVEY
+ * §8f f2) take the blocked schedule with 64-column steps for all systems at
+ * once (every launch covers the batch): same per-system results (bitwise
+ * ebv_lu_factor / the oracle). */
 ebv_status_t ebv_lu_factor_batched(ebv_context_t ctx, int64_t n, double* A, int64_t lda,
                                    int64_t strideA, int64_t batch, double* B, int64_t ldb,
                                    int64_t strideB, int64_t nrhs, double tau, int32_t* d_info,
@@ -249,7 +254,7 @@ ebv_status_t ebv_lu_solve_band(ebv_context_t ctx, int64_t n, int64_t kl, int64_t
  * B_s <- U_s^-1 (L_s^-1 B_s) with the packed LU_s = LU + s*strideA (read
  * only), forward then backward substitution of Eq 1 per column in
  * the canonical order (bitwise ebv_lu_solve / the oracle on each system).
- * Layout, strides and limits as ebv_lu_factor_batched (n <= 32,
+ * Layout, strides and limits as ebv_lu_factor_batched (n <= 512,
  * nrhs <= 16).  Errors: INVALID_VALUE, NOT_SUPPORTED as there. */
 ebv_status_t ebv_lu_solve_batched(ebv_context_t ctx, int64_t n, const double* LU, int64_t lda,
                                   int64_t strideA, int64_t batch, double* B, int64_t ldb,

@@ -627,6 +627,7 @@ ebv_status_t ebv_destroy(ebv_context_t c) {
   DeviceGuard g(c->device);
   dist_release(c);
   if (c->d_vec) cudaFree(c->d_vec);
+  if (c->d_bws) cudaFree(c->d_bws);
   for (auto& r : c->recs) { cudaEventDestroy(r.e0); cudaEventDestroy(r.e1); }
   for (auto e : c->pool) cudaEventDestroy(e);
   for (auto& en : c->gcache)
@@ -944,6 +945,76 @@ ebv_status_t ebv_lu_solve_banded(ebv_context_t c, int64_t n, int64_t kl, int64_t
   return solve_banded_impl(c, n, kl, ku, LU, lda, B, ldb, nrhs, stream);
 }
 
+// Batched medium orders (SURVEY §8f f2, 64 < n <= EBV_BATCHED_MEDIUM_MAX_N):
+// the blocked schedule with 64-column steps run for every system at once —
+// each launch covers all systems (blockIdx.y / z = system): panel leaf, U12
+// leaf solve, DMMA update; then (B given) forward / backward substitution as
+// row-block TRSMs whose off-diagonal parts are DMMA updates (k ascending
+// forward, descending backward).  Per system the operations are those of the
+// single-system blocked path, in the canonical order (bitwise the oracle).
+static ebv_status_t batched_medium(ebv_context_t c, int64_t n, double* A, int64_t lda, int64_t sA, int64_t batch,
+                                   double* B, int64_t ldb, int64_t sB, int64_t nrhs, double tau, int32_t* d_info,
+                                   cudaStream_t s, bool solve_only) {
+  const int64_t need = batch * (int64_t)(sizeof(double) + sizeof(int64_t) + sizeof(int));
+  if (need > c->bws_cap) {
+    if (c->d_bws) cudaFree(c->d_bws);
+    c->d_bws = nullptr;
+    c->bws_cap = 0;
+    if (cudaMalloc(&c->d_bws, need) != cudaSuccess) { set_error("workspace alloc failed"); return EBV_ERR_ALLOC; }
+    if (cudaMemset(c->d_bws, 0, need) != cudaSuccess) { set_error("workspace init failed"); return EBV_ERR_ALLOC; }
+    c->bws_cap = need;
+  }
+  double* tau_s = reinterpret_cast<double*>(c->d_bws);
+  int64_t* info64 = reinterpret_cast<int64_t*>(tau_s + batch);
+  int* counts = reinterpret_cast<int*>(info64 + batch);   // panel-leaf arrival counters (self-resetting)
+  constexpr int64_t NB = 64;
+  cudaError_t e = cudaSuccess;
+  if (!solve_only) {
+    e = timed(c, KC_OTHER, 0, tau < 0 ? 8.0 * n * n * batch : 0, s, 1,
+              [&] { return launch_batched_prep(n, A, lda, sA, batch, tau, tau_s, info64, s); });
+    for (int64_t c0 = 0; c0 < n && e == cudaSuccess; c0 += NB) {
+      const int64_t w = n - c0 < NB ? n - c0 : NB, rest = n - c0 - w;
+      double* P = A + c0 + c0 * lda;
+      e = timed(c, KC_LEAF, batch * (2.0 / 3.0 * w * w * w + (double)(n - c0 - w) * w * w), batch * 16.0 * (n - c0) * w,
+                s, 1, [&] {
+                  return launch_panel_leaf_batched(n - c0, w, P, lda, sA, tau_s, 1, info64, 1, c0, counts, batch, s);
+                });
+      if (e != cudaSuccess || rest <= 0) break;
+      e = timed(c, KC_TRSM, batch * (double)rest * w * w, batch * 16.0 * rest * w, s, 1,
+                [&] { return launch_trsm_llu_batched(w, rest, P, lda, sA, P + w * lda, lda, sA, batch, s); });
+      if (e != cudaSuccess) break;
+      e = timed(c, KC_UPDATE, batch * 2.0 * rest * rest * w, batch * 8.0 * (2.0 * rest * w + 2.0 * rest * rest), s, 1,
+                [&] {
+                  return launch_gemm_sub_batched(rest, rest, w, P + w, lda, sA, P + w * lda, lda, sA,
+                                                 P + w + w * lda, lda, sA, batch, false, s);
+                });
+    }
+    if (e == cudaSuccess) e = launch_info_to_i32(batch, info64, d_info, s);
+    if (e != cudaSuccess) return cuda_fail(e, "batched medium factor");
+  }
+  if (B && nrhs > 0) {
+    for (int64_t r0 = 0; r0 < n && e == cudaSuccess; r0 += NB) {   // LY = B (Eq 1), k ascending
+      const int64_t k = n - r0 < NB ? n - r0 : NB;
+      if (r0 > 0)
+        e = launch_gemm_sub_batched(k, nrhs, r0, A + r0, lda, sA, B, ldb, sB, B + r0, ldb, sB, batch, false, s);
+      if (e == cudaSuccess)
+        e = launch_trsm_llu_batched(k, nrhs, A + r0 + r0 * lda, lda, sA, B + r0, ldb, sB, batch, s);
+    }
+    const int64_t last = ((n - 1) / NB) * NB;
+    for (int64_t r0 = last; r0 >= 0 && e == cudaSuccess; r0 -= NB) {   // UX = Y, k descending
+      const int64_t k = n - r0 < NB ? n - r0 : NB, r1 = r0 + k;
+      if (r1 < n)
+        e = launch_gemm_sub_batched(k, nrhs, n - r1, A + r0 + r1 * lda, lda, sA, B + r1, ldb, sB, B + r0, ldb, sB,
+                                    batch, true, s);
+      if (e == cudaSuccess)
+        e = launch_trsm_luu_batched(k, nrhs, A + r0 + r0 * lda, lda, sA, B + r0, ldb, sB, batch, s);
+    }
+    c->launches += 4 * ((n + NB - 1) / NB);
+    if (e != cudaSuccess) return cuda_fail(e, "batched medium solve");
+  }
+  return EBV_SUCCESS;
+}
+
 ebv_status_t ebv_lu_factor_batched(ebv_context_t c, int64_t n, double* A, int64_t lda, int64_t strideA,
                                    int64_t batch, double* B, int64_t ldb, int64_t strideB, int64_t nrhs,
                                    double tau, int32_t* d_info, void* stream) {
@@ -957,10 +1028,13 @@ ebv_status_t ebv_lu_factor_batched(ebv_context_t c, int64_t n, double* A, int64_
   }
   if (n == 0 || batch == 0) return EBV_SUCCESS;
   if (!A || !d_info) return invalid("ebv_lu_factor_batched: NULL pointer");
-  if (n > EBV_BATCHED_MAX_N) { set_error("batched path supports n <= 64"); return EBV_ERR_NOT_SUPPORTED; }
+  if (n > EBV_BATCHED_MEDIUM_MAX_N) { set_error("batched path supports n <= 512"); return EBV_ERR_NOT_SUPPORTED; }
   if (nrhs > 16) { set_error("batched path supports nrhs <= 16"); return EBV_ERR_NOT_SUPPORTED; }
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
+  if (n > EBV_BATCHED_MAX_N)
+    return batched_medium(c, n, A, lda, strideA, batch, nrhs > 0 ? B : nullptr, ldb, strideB, nrhs, tau, d_info, s,
+                          false);
   double* Bp = (nrhs > 0) ? B : nullptr;
   double fl = batch * (2.0 / 3.0 * n * n * n + 2.0 * n * n * (Bp ? nrhs : 0));
   double by = batch * (16.0 * n * n + (Bp ? 16.0 * n * nrhs : 0) + 4.0);
@@ -982,10 +1056,13 @@ ebv_status_t ebv_lu_solve_batched(ebv_context_t c, int64_t n, const double* LU, 
   if (batch > 1 && strideB < ldb * nrhs) return invalid("ebv_lu_solve_batched: strideB < ldb*nrhs");
   if (n == 0 || batch == 0 || nrhs == 0) return EBV_SUCCESS;
   if (!LU || !B) return invalid("ebv_lu_solve_batched: NULL pointer");
-  if (n > EBV_BATCHED_MAX_N) { set_error("batched path supports n <= 64"); return EBV_ERR_NOT_SUPPORTED; }
+  if (n > EBV_BATCHED_MEDIUM_MAX_N) { set_error("batched path supports n <= 512"); return EBV_ERR_NOT_SUPPORTED; }
   if (nrhs > 16) { set_error("batched path supports nrhs <= 16"); return EBV_ERR_NOT_SUPPORTED; }
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
+  if (n > EBV_BATCHED_MAX_N)
+    return batched_medium(c, n, const_cast<double*>(LU), lda, strideA, batch, B, ldb, strideB, nrhs, 0.0, nullptr, s,
+                          true);
   double fl = batch * 2.0 * n * n * nrhs, by = batch * (8.0 * n * n + 16.0 * n * nrhs);
   cudaError_t e = timed(c, KC_BATCHED, fl, by, s, 1, [&] {
     return launch_batched(n, const_cast<double*>(LU), lda, strideA, batch, B, ldb, strideB, nrhs, nullptr, false, 0.0,

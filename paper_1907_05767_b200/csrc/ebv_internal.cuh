@@ -39,6 +39,20 @@ cudaError_t launch_leaf_lu(int64_t n, double* A, int64_t lda, const double* tau,
 
 // X <- X U^-1, U upper triangular k x k (k <= 64, non-unit), X m x k:
 // row-parallel substitution (the L21 panel of the blocked form).
+// Batched forms of the blocked-schedule kernels (systems at base + s*stride,
+// s < batch): per system bitwise the single-system launches.  Used by the
+// batched medium-order path (ebv_lu_factor_batched, 64 < n <= 512).
+cudaError_t launch_panel_leaf_batched(int64_t M, int64_t w, double* P, int64_t lda, int64_t bsP, const double* tau,
+                                      int64_t bsTau, int64_t* info, int64_t bsInfo, int64_t koff, int* count,
+                                      int64_t batch, cudaStream_t s);
+cudaError_t launch_trsm_llu_batched(int64_t k, int64_t m, const double* L, int64_t ldl, int64_t bsL, double* X,
+                                    int64_t ldx, int64_t bsX, int64_t batch, cudaStream_t s);
+cudaError_t launch_trsm_luu_batched(int64_t k, int64_t m, const double* U, int64_t ldu, int64_t bsU, double* X,
+                                    int64_t ldx, int64_t bsX, int64_t batch, cudaStream_t s);
+cudaError_t launch_gemm_sub_batched(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int64_t sA,
+                                    const double* B, int64_t ldb, int64_t sB, double* Cm, int64_t ldc, int64_t sC,
+                                    int64_t batch, bool reverse_k, cudaStream_t s);
+
 cudaError_t launch_panel_leaf(int64_t M, int64_t w, double* P, int64_t lda, const double* tau, int64_t* info,
                               int64_t koff, int* count, cudaStream_t s);
 cudaError_t launch_trsm_right_upper(int64_t m, int64_t k, double* X, int64_t ldx, const double* U,
@@ -84,6 +98,11 @@ size_t vector_smem_bytes(int64_t n, int num_ctas);
 
 // Utilities.
 cudaError_t launch_set_info0(int64_t* info, cudaStream_t s);
+// batched medium path: per-system pivot floors and cleared int64 info words;
+// int64 info words -> the API's int32 per-system info
+cudaError_t launch_batched_prep(int64_t n, const double* A, int64_t lda, int64_t sA, int64_t batch, double tau,
+                                double* tau_s, int64_t* info64, cudaStream_t s);
+cudaError_t launch_info_to_i32(int64_t batch, const int64_t* info64, int32_t* info32, cudaStream_t s);
 // tau_out = (tau >= 0) ? tau : n * eps * ||A||_inf  (norm pre-pass)
 cudaError_t launch_tau(int64_t n, const double* A, int64_t lda, double tau, double* tau_out,
                        unsigned long long* norm_ws, cudaStream_t s);

@@ -21,6 +21,8 @@ struct ebv_context {
   int* d_ticket = nullptr;
   int* d_pcount = nullptr;
   double* d_vec = nullptr;  // n-vector workspace (row scalings)
+  void* d_bws = nullptr;    // batched medium path: per-system tau, info, arrival counters
+  int64_t bws_cap = 0;
   int64_t vec_cap = 0;  // panel-leaf arrival counter (zero between launches; self-resetting)
   int* d_flags = nullptr;
   int64_t flags_cap = 0;

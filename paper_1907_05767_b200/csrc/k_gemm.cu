@@ -73,7 +73,11 @@ template <class C, int VEC>
 __global__ void __launch_bounds__(C::THREADS, C::MINB)
     gemm_sub_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int64_t lda,
                     const double* __restrict__ B, int64_t ldb, double* __restrict__ Cm, int64_t ldc,
-                    int reverse_k, int tilesM, int tilesN) {
+                    int reverse_k, int tilesM, int tilesN, int64_t bsA, int64_t bsB, int64_t bsC) {
+  // batched form (blockIdx.z = system; strides 0 / gridDim.z = 1 otherwise)
+  A += blockIdx.z * bsA;
+  B += blockIdx.z * bsB;
+  Cm += blockIdx.z * bsC;
   extern __shared__ __align__(16) double smem[];
   double* sA = smem;                              // [STAGES][KC][AST]
   double* sB = smem + C::STAGES * C::A_STAGE;     // [STAGES][BN][BSTR]
@@ -203,7 +207,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
 
 template <class C, int VEC>
 cudaError_t run_v(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb,
-                  double* Cm, int64_t ldc, bool rev, cudaStream_t s) {
+                  double* Cm, int64_t ldc, bool rev, cudaStream_t s, int64_t sA = 0, int64_t sB = 0, int64_t sC = 0,
+                  int64_t batch = 1) {
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e =
@@ -214,22 +219,29 @@ cudaError_t run_v(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
   int64_t tm = (M + C::BM - 1) / C::BM, tn = (N + C::BN - 1) / C::BN;
   int64_t nblk = tm * tn;
   if (nblk == 0) return cudaSuccess;
-  gemm_sub_kernel<C, VEC><<<(unsigned)nblk, C::THREADS, C::SMEM, s>>>(M, N, K, A, lda, B, ldb, Cm, ldc, rev ? 1 : 0,
-                                                                       (int)tm, (int)tn);
-  return cudaGetLastError();
+  for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+    const int64_t nb = batch - b0 < 65535 ? batch - b0 : 65535;
+    gemm_sub_kernel<C, VEC><<<dim3((unsigned)nblk, 1, (unsigned)nb), C::THREADS, C::SMEM, s>>>(
+        M, N, K, A + b0 * sA, lda, B + b0 * sB, ldb, Cm + b0 * sC, ldc, rev ? 1 : 0, (int)tm, (int)tn, sA, sB, sC);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 template <class C>
 cudaError_t run(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb,
-                double* Cm, int64_t ldc, bool rev, cudaStream_t s) {
+                double* Cm, int64_t ldc, bool rev, cudaStream_t s, int64_t sA = 0, int64_t sB = 0, int64_t sC = 0,
+                int64_t batch = 1) {
   // 16-byte copies need 16-byte aligned column starts of A and B, which the
   // even leading dimensions and aligned bases guarantee (k stays even
   // because stages start at multiples of KC); the reversed order reads k
   // downwards and takes the 8-byte path.
   const bool v2 = !rev && ((lda & 1) == 0) && ((ldb & 1) == 0) &&
-                  ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0);
-  if (v2) return run_v<C, 2>(M, N, K, A, lda, B, ldb, Cm, ldc, rev, s);
-  return run_v<C, 1>(M, N, K, A, lda, B, ldb, Cm, ldc, rev, s);
+                  ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0) &&
+                  ((sA & 1) == 0) && ((sB & 1) == 0);
+  if (v2) return run_v<C, 2>(M, N, K, A, lda, B, ldb, Cm, ldc, rev, s, sA, sB, sC, batch);
+  return run_v<C, 1>(M, N, K, A, lda, B, ldb, Cm, ldc, rev, s, sA, sB, sC, batch);
 }
 
 //                 BM   BN  WM WN KC ST MINB
@@ -280,6 +292,18 @@ cudaError_t launch_gemm_sub(int64_t M, int64_t N, int64_t K, const double* A, in
   }
   if (M <= 64) return run<Wide>(M, N, K, A, lda, B, ldb, Cm, ldc, reverse_k, s);
   return run<Mid>(M, N, K, A, lda, B, ldb, Cm, ldc, reverse_k, s);
+}
+
+// Batched form (systems s = 0..batch-1 at A + s*sA, B + s*sB, C + s*sC): the
+// cp.async kernels with blockIdx.z as the system — per system the same fma
+// chains as launch_gemm_sub (bitwise).
+cudaError_t launch_gemm_sub_batched(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int64_t sA,
+                                    const double* B, int64_t ldb, int64_t sB, double* Cm, int64_t ldc, int64_t sC,
+                                    int64_t batch, bool reverse_k, cudaStream_t s) {
+  if (M <= 0 || N <= 0 || K <= 0 || batch <= 0) return cudaSuccess;
+  if (N <= 8) return run<Vec>(M, N, K, A, lda, B, ldb, Cm, ldc, reverse_k, s, sA, sB, sC, batch);
+  if (M <= 64) return run<Wide>(M, N, K, A, lda, B, ldb, Cm, ldc, reverse_k, s, sA, sB, sC, batch);
+  return run<Mid>(M, N, K, A, lda, B, ldb, Cm, ldc, reverse_k, s, sA, sB, sC, batch);
 }
 
 }  // namespace ebv

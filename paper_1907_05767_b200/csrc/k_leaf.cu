@@ -248,7 +248,14 @@ __global__ void __launch_bounds__(256, 2) trsm_ru_kernel(int64_t m, int k, doubl
 template <int GD>
 __global__ void __launch_bounds__(W * GD) panel_leaf_kernel(int64_t M, int w, double* __restrict__ P, int64_t lda,
                                                            const double* __restrict__ tau, int64_t* info,
-                                                           int64_t koff, int* count) {
+                                                           int64_t koff, int* count, int64_t bsP, int64_t bsInfo,
+                                                           int64_t bsTau) {
+  // batched form: blockIdx.y = system (its panel, info word, tau and
+  // arrival counter); strides 0 and gridDim.y = 1 for one system
+  P += blockIdx.y * bsP;
+  info += blockIdx.y * bsInfo;
+  tau += blockIdx.y * bsTau;
+  count += blockIdx.y;
   constexpr int QD = W / GD, PS = QD + 2, RS = GD * PS;
   extern __shared__ __align__(16) double sUp[];    // [W][RS]: sUp[k*RS + j*PS + q] = u(k, j + GD*(q + k/GD))
   __shared__ double srcp[W];
@@ -370,7 +377,9 @@ __global__ void __launch_bounds__(W * GD) panel_leaf_kernel(int64_t M, int w, do
 // columns, so the kernel holds fewer SM slots beside the DMMA update.
 template <int CC>
 __global__ void __launch_bounds__(256) trsm_llu_kernel(int k, int64_t m, const double* __restrict__ L, int64_t ldl,
-                                                       double* __restrict__ X, int64_t ldx) {
+                                                       double* __restrict__ X, int64_t ldx, int64_t bsL, int64_t bsX) {
+  L += blockIdx.y * bsL;   // batched form: blockIdx.y = system
+  X += blockIdx.y * bsX;
   __shared__ __align__(16) double sL[W * S];   // sL[p*S + r] = l(r, p), r > p
   for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
     const int r = idx % W, p = idx / W;
@@ -431,7 +440,9 @@ __global__ void __launch_bounds__(256) trsm_llu_kernel(int k, int64_t m, const d
 // backward order (Eq 1, UX = Y).  Padded rows (p >= k) are identity rows and
 // come first in the descending sweep: they change nothing.
 __global__ void __launch_bounds__(128) trsm_luu_kernel(int k, int64_t m, const double* __restrict__ U, int64_t ldu,
-                                                       double* __restrict__ X, int64_t ldx) {
+                                                       double* __restrict__ X, int64_t ldx, int64_t bsU, int64_t bsX) {
+  U += blockIdx.y * bsU;   // batched form: blockIdx.y = system
+  X += blockIdx.y * bsX;
   __shared__ __align__(16) double sU[W * S];   // sU[p*S + i] = u(i, p), i <= p (column p of U)
   for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
     const int i = idx % W, p = idx / W;
@@ -462,7 +473,7 @@ cudaError_t launch_trsm_left_upper(int64_t k, int64_t m, const double* U, int64_
                                    cudaStream_t s) {
   if (m <= 0 || k <= 0) return cudaSuccess;
   if (k > W) return cudaErrorInvalidValue;
-  trsm_luu_kernel<<<(unsigned)((m + 127) / 128), 128, 0, s>>>((int)k, m, U, ldu, X, ldx);
+  trsm_luu_kernel<<<(unsigned)((m + 127) / 128), 128, 0, s>>>((int)k, m, U, ldu, X, ldx, 0, 0);
   return cudaGetLastError();
 }
 
@@ -474,11 +485,7 @@ cudaError_t launch_leaf_lu(int64_t n, double* A, int64_t lda, const double* tau,
   return cudaGetLastError();
 }
 
-cudaError_t launch_panel_leaf(int64_t M, int64_t w, double* P, int64_t lda, const double* tau, int64_t* info,
-                              int64_t koff, int* count, cudaStream_t s) {
-  if (w <= 0 || M <= 0) return cudaSuccess;
-  if (w > W || M < w) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)W * kLeafG * (W / kLeafG + 2) * sizeof(double);
+static cudaError_t panel_leaf_attr(size_t smem) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e =
@@ -486,8 +493,21 @@ cudaError_t launch_panel_leaf(int64_t M, int64_t w, double* P, int64_t lda, cons
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  return cudaSuccess;
+}
+
+cudaError_t launch_panel_leaf(int64_t M, int64_t w, double* P, int64_t lda, const double* tau, int64_t* info,
+                              int64_t koff, int* count, cudaStream_t s) {
+  if (w <= 0 || M <= 0) return cudaSuccess;
+  if (w > W || M < w) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)W * kLeafG * (W / kLeafG + 2) * sizeof(double);
+  {
+    cudaError_t e = panel_leaf_attr(smem);
+    if (e != cudaSuccess) return e;
+  }
   const int64_t grid = M > w ? (M - w + W - 1) / W : 1;
-  panel_leaf_kernel<kLeafG><<<(unsigned)grid, W * kLeafG, smem, s>>>(M, (int)w, P, lda, tau, info, koff, count);
+  panel_leaf_kernel<kLeafG><<<(unsigned)grid, W * kLeafG, smem, s>>>(M, (int)w, P, lda, tau, info, koff, count, 0, 0,
+                                                                      0);
   return cudaGetLastError();
 }
 
@@ -514,11 +534,60 @@ cudaError_t launch_trsm_left_lower_unit(int64_t k, int64_t m, const double* L, i
     }();
     int64_t grid = (m + 63) / 64;
     if (gcap > 0 && grid > gcap) grid = gcap;
-    trsm_llu_kernel<2><<<(unsigned)grid, 256, 0, s>>>((int)k, m, L, ldl, X, ldx);
+    trsm_llu_kernel<2><<<(unsigned)grid, 256, 0, s>>>((int)k, m, L, ldl, X, ldx, 0, 0);
     return cudaGetLastError();
   }
-  trsm_llu_kernel<1><<<(unsigned)((m + 31) / 32), 256, 0, s>>>((int)k, m, L, ldl, X, ldx);
+  trsm_llu_kernel<1><<<(unsigned)((m + 31) / 32), 256, 0, s>>>((int)k, m, L, ldl, X, ldx, 0, 0);
   return cudaGetLastError();
+}
+
+// ---- batched forms (systems s = 0..batch-1 at base + s*stride; gridDim.y =
+// system, chunks of 65535): per system exactly the single-system kernels
+cudaError_t launch_panel_leaf_batched(int64_t M, int64_t w, double* P, int64_t lda, int64_t bsP, const double* tau,
+                                      int64_t bsTau, int64_t* info, int64_t bsInfo, int64_t koff, int* count,
+                                      int64_t batch, cudaStream_t s) {
+  if (w <= 0 || M <= 0 || batch <= 0) return cudaSuccess;
+  if (w > W || M < w) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)W * kLeafG * (W / kLeafG + 2) * sizeof(double);
+  cudaError_t e = panel_leaf_attr(smem);
+  if (e != cudaSuccess) return e;
+  const int64_t grid = M > w ? (M - w + W - 1) / W : 1;
+  for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+    const int64_t nb = batch - b0 < 65535 ? batch - b0 : 65535;
+    panel_leaf_kernel<kLeafG><<<dim3((unsigned)grid, (unsigned)nb), W * kLeafG, smem, s>>>(
+        M, (int)w, P + b0 * bsP, lda, tau + b0 * bsTau, info + b0 * bsInfo, koff, count + b0, bsP, bsInfo, bsTau);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_trsm_llu_batched(int64_t k, int64_t m, const double* L, int64_t ldl, int64_t bsL, double* X,
+                                    int64_t ldx, int64_t bsX, int64_t batch, cudaStream_t s) {
+  if (m <= 0 || k <= 0 || batch <= 0) return cudaSuccess;
+  if (k > W) return cudaErrorInvalidValue;
+  for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+    const int64_t nb = batch - b0 < 65535 ? batch - b0 : 65535;
+    trsm_llu_kernel<2><<<dim3((unsigned)((m + 63) / 64), (unsigned)nb), 256, 0, s>>>((int)k, m, L + b0 * bsL, ldl,
+                                                                                     X + b0 * bsX, ldx, bsL, bsX);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_trsm_luu_batched(int64_t k, int64_t m, const double* U, int64_t ldu, int64_t bsU, double* X,
+                                    int64_t ldx, int64_t bsX, int64_t batch, cudaStream_t s) {
+  if (m <= 0 || k <= 0 || batch <= 0) return cudaSuccess;
+  if (k > W) return cudaErrorInvalidValue;
+  for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+    const int64_t nb = batch - b0 < 65535 ? batch - b0 : 65535;
+    trsm_luu_kernel<<<dim3((unsigned)((m + 127) / 128), (unsigned)nb), 128, 0, s>>>((int)k, m, U + b0 * bsU, ldu,
+                                                                                  X + b0 * bsX, ldx, bsU, bsX);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace ebv

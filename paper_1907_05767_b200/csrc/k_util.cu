@@ -23,7 +23,53 @@ __global__ void tau_kernel(int64_t n, const unsigned long long* nrm, double* tau
 
 __global__ void set_tau_kernel(double tau, double* tau_out) { *tau_out = tau; }
 
+// batched medium systems: per system the pivot floor (tau >= 0 as given, or
+// n * eps * ||A_s||_inf — the row sums accumulated over j ascending like
+// norm_inf_kernel), info words cleared
+__global__ void batched_prep_kernel(int64_t n, const double* __restrict__ A, int64_t lda, int64_t sA, double tau,
+                                    double* tau_s, int64_t* info64) {
+  const int64_t sys = blockIdx.x;
+  __shared__ double red[256];
+  double m = 0.0;
+  if (tau < 0.0) {
+    const double* As = A + sys * sA;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      double r = 0.0;
+      for (int64_t j = 0; j < n; j++) r += fabs(As[i + j * lda]);
+      m = fmax(m, r);
+    }
+  }
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    tau_s[sys] = tau < 0.0 ? (double)n * 2.220446049250313e-16 * red[0] : tau;
+    info64[sys] = 0;
+  }
+}
+
+__global__ void info_to_i32_kernel(int64_t batch, const int64_t* info64, int32_t* info32) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < batch) info32[s] = (int32_t)info64[s];
+}
+
 }  // namespace
+
+cudaError_t launch_batched_prep(int64_t n, const double* A, int64_t lda, int64_t sA, int64_t batch, double tau,
+                                double* tau_s, int64_t* info64, cudaStream_t s) {
+  if (batch <= 0) return cudaSuccess;
+  batched_prep_kernel<<<(unsigned)batch, 256, 0, s>>>(n, A, lda, sA, tau, tau_s, info64);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_info_to_i32(int64_t batch, const int64_t* info64, int32_t* info32, cudaStream_t s) {
+  if (batch <= 0) return cudaSuccess;
+  info_to_i32_kernel<<<(unsigned)((batch + 255) / 256), 256, 0, s>>>(batch, info64, info32);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_set_info0(int64_t* info, cudaStream_t s) {
   set_info0_kernel<<<1, 1, 0, s>>>(info);

@@ -164,6 +164,29 @@ by = 16.0 * n * (n - 1) / 2
 emit(config="f3-ldu", n=n, what="LDU form (strict upper / pivot)", ms=med, ms_min=lo, ms_max=hi,
      gbs=by / med / 1e6, frac_hbm=by / med / 1e6 / HBM)
 
+# ---------------- f2: batched medium orders (64 < n <= 512: batched blocked schedule)
+for nm, bm in ((128, 20000), (256, 4000), (512, 800)):
+    dbm = ebv_inputs.generate_batched(bm, nm, seed=2, nrhs=1, device=dev)
+    Am = dbm["At"]
+    Bm = dbm["B"].transpose(1, 2).clone(memory_format=torch.contiguous_format)
+    Xm = dbm["X"]
+    Awm, Bwm = torch.empty_like(Am), torch.empty_like(Bm)
+    infom = torch.zeros(bm, dtype=torch.int32, device=dev)
+    del dbm
+
+    def prepm():
+        Awm.copy_(Am)
+        Bwm.copy_(Bm)
+
+    med, lo, hi = timeit(prepm, lambda: ebv.ebv_lu_factor_batched(ctx.handle, nm, Awm.data_ptr(), nm, nm * nm, bm,
+                                                                  Bwm.data_ptr(), nm, nm, 1, 0.0, infom.data_ptr(), sh))
+    fl = bm * (2.0 / 3.0 * nm ** 3 + 2.0 * nm * nm)
+    emit(config="f2-batched-medium", batch=bm, n=nm, what="batched factor+solve (blocked, all systems per launch)",
+         ms=med, ms_min=lo, ms_max=hi, tflops=fl / med / 1e9, frac_fp64_peak=fl / med / 1e9 / PEAK_TF,
+         systems_per_s=bm / med * 1e3, info_ok=not infom.any().item(),
+         max_err=(Bwm.transpose(1, 2) - Xm).abs().max().item())
+    del Am, Bm, Awm, Bwm, Xm
+
 # ---------------- f4: banded / 2D five-point stencil (zero-skip), dense storage
 for m in (128, 256):
     n = m * m

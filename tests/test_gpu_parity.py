@@ -171,7 +171,7 @@ def test_argument_errors(dev, ctx):
     assert L.ebv_lu_factor(ctx.handle, 4, None, 4, 0.0, info.data_ptr(), None) == 1
     assert L.ebv_lu_factor(ctx.handle, 0, None, 1, 0.0, info.data_ptr(), None) == 0
     assert L.ebv_lu_solve(ctx.handle, 4, A.data_ptr(), 4, None, 4, 1, None) == 1
-    assert L.ebv_lu_factor_batched(ctx.handle, 65, A.data_ptr(), 65, 65 * 65, 1, None, 65, 0, 0, 0.0,
+    assert L.ebv_lu_factor_batched(ctx.handle, 513, A.data_ptr(), 513, 513 * 513, 1, None, 513, 0, 0, 0.0,
                                    info.data_ptr(), None) == 5
     torch.cuda.synchronize()
 
@@ -345,7 +345,8 @@ def test_vector_path_bitwise(dev, ctx, n, ctas):
 # ------------------------------------------------------------------ batched
 @pytest.mark.parametrize("n,batch,nrhs", [(32, 1000, 1), (32, 1, 1), (32, 7, 2), (1, 5, 1), (7, 33, 3),
                                           (31, 64, 16), (32, 257, 0), (33, 50, 1), (48, 31, 3), (64, 200, 1),
-                                          (64, 3, 16), (64, 9, 0)])
+                                          (64, 3, 16), (64, 9, 0),
+                                          (65, 9, 1), (100, 20, 3), (128, 7, 16), (200, 5, 2), (511, 3, 1), (512, 2, 4)])
 def test_batched_bitwise(dev, ctx, n, batch, nrhs):
     db = ebv_inputs.generate_batched(batch, n, seed=n + batch, nrhs=max(nrhs, 1), device=dev)
     At = db["At"].clone()
@@ -364,7 +365,7 @@ def test_batched_bitwise(dev, ctx, n, batch, nrhs):
 
 
 @pytest.mark.parametrize("n,batch,nrhs", [(32, 1000, 1), (32, 333, 16), (7, 65, 3), (1, 4, 2), (31, 2, 5),
-                                          (64, 100, 2), (40, 7, 1)])
+                                          (64, 100, 2), (40, 7, 1), (130, 6, 3), (300, 3, 16)])
 def test_batched_solve_only_bitwise(dev, ctx, n, batch, nrhs):
     """Factor once, solve many: ebv_lu_solve_batched on the
     factors of ebv_lu_factor_batched equals the oracle's solve of every
@@ -542,3 +543,28 @@ def test_random_schedules_bitwise(dev, n, nb, leaf, path, la, nrhs):
     assert int(info) == info_o == 0
     assert bits_eq(LU.cpu().numpy(), lu_o)
     assert bits_eq(X.cpu().numpy(), oracle.lu_solve(lu_o, d["B"].cpu().numpy()))
+
+
+@pytest.mark.parametrize("n,tau", [(100, 0.0), (150, -1.0), (300, 0.25)])
+def test_batched_medium_info(dev, ctx, n, tau):
+    """Batched medium orders: per-system info (first failing
+    1-based step, reading R9's threshold) equals the oracle's, including
+    tau < 0 (n * eps * ||A_s||_inf per system), and the factors stay bitwise."""
+    batch = 5
+    db = ebv_inputs.generate_batched(batch, n, seed=n, nrhs=1, device=dev)
+    At = db["At"].clone()
+    At[2, 0, 0] = 0.0                      # system 2: a zero first pivot
+    At[4, 70, 70] = 1e-300                 # system 4: a tiny pivot at step 71 (caught by tau < 0 / tau > 0)
+    a = At.transpose(1, 2).cpu().numpy()
+    info = ebv.lu_factor_batched(At, None, tau=tau, ctx=ctx)
+    torch.cuda.synchronize()
+    if tau >= 0:
+        lu_o, _, info_o = oracle.lu_factor_batched(a, None, tau=tau)
+    else:   # the API's default floor per system (reading R9), passed to the oracle explicitly
+        res = [oracle.lu_factor(a[s], n * 2.220446049250313e-16 * np.abs(a[s]).sum(1).max()) for s in range(batch)]
+        lu_o = np.stack([r[0] for r in res])
+        info_o = np.array([r[1] for r in res], dtype=np.int32)
+    assert bits_eq(info.cpu().numpy(), info_o)
+    assert info_o[2] == 1
+    ok = [s for s in range(batch) if info_o[s] == 0]
+    assert bits_eq(At.transpose(1, 2).cpu().numpy()[ok], lu_o[ok])
