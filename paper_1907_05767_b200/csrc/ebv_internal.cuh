@@ -98,6 +98,10 @@ size_t vector_smem_bytes(int64_t n, int num_ctas);
 
 // Utilities.
 cudaError_t launch_set_info0(int64_t* info, cudaStream_t s);
+// cudaFuncSetAttribute(fn, MaxDynamicSharedMemorySize, bytes) once per
+// (kernel, device) — the attribute is per device, so a process that drives
+// several GPUs sets it on each (thread-safe).
+cudaError_t ensure_max_dyn_smem(const void* fn, int bytes);
 // batched medium path: per-system pivot floors and cleared int64 info words;
 // int64 info words -> the API's int32 per-system info
 cudaError_t launch_batched_prep(int64_t n, const double* A, int64_t lda, int64_t sA, int64_t batch, double tau,

@@ -209,12 +209,9 @@ template <class C, int VEC>
 cudaError_t run_v(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb,
                   double* Cm, int64_t ldc, bool rev, cudaStream_t s, int64_t sA = 0, int64_t sB = 0, int64_t sC = 0,
                   int64_t batch = 1) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e =
-        cudaFuncSetAttribute(gemm_sub_kernel<C, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  {
+    cudaError_t e = ensure_max_dyn_smem(reinterpret_cast<const void*>(gemm_sub_kernel<C, VEC>), C::SMEM);
     if (e != cudaSuccess) return e;
-    attr_done = true;
   }
   int64_t tm = (M + C::BM - 1) / C::BM, tn = (N + C::BN - 1) / C::BN;
   int64_t nblk = tm * tn;

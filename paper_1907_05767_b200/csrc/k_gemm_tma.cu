@@ -398,11 +398,9 @@ bool make_map(CUtensorMap* map, const double* ptr, int64_t rows, int64_t cols, i
 template <class C>
 cudaError_t run_tma(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb,
                     double* Cm, int64_t ldc, cudaStream_t s) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tma_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  {
+    cudaError_t e = ensure_max_dyn_smem(reinterpret_cast<const void*>(gemm_tma_kernel<C>), C::SMEM);
     if (e != cudaSuccess) return e;
-    attr_done = true;
   }
   CUtensorMap ma, mb;
   if (!make_map(&ma, A, M, K, lda, C::AST, C::KC) || !make_map(&mb, B, K, N, ldb, C::BSTR, C::BN))
@@ -415,19 +413,13 @@ cudaError_t run_tma(int64_t M, int64_t N, int64_t K, const double* A, int64_t ld
 template <class C>
 cudaError_t run_tma_persistent(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
                                int64_t ldb, double* Cm, int64_t ldc, cudaStream_t s) {
-  static bool attr_done = false;
-  static int slots = 0;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tma_persistent_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM);
-    if (e != cudaSuccess) return e;
-    int dev = 0, sms = 148, per = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gemm_tma_persistent_kernel<C>, C::THREADS, C::SMEM);
-    slots = sms * (per > 0 ? per : 1);
-    attr_done = true;
-  }
+  cudaError_t ea = ensure_max_dyn_smem(reinterpret_cast<const void*>(gemm_tma_persistent_kernel<C>), C::SMEM);
+  if (ea != cudaSuccess) return ea;
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gemm_tma_persistent_kernel<C>, C::THREADS, C::SMEM);
+  const int slots = sms * (per > 0 ? per : 1);
   CUtensorMap ma, mb;
   if (!make_map(&ma, A, M, K, lda, C::AST, C::KC) || !make_map(&mb, B, K, N, ldb, C::BSTR, C::BN))
     return cudaErrorNotSupported;

@@ -486,14 +486,7 @@ cudaError_t launch_leaf_lu(int64_t n, double* A, int64_t lda, const double* tau,
 }
 
 static cudaError_t panel_leaf_attr(size_t smem) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(panel_leaf_kernel<kLeafG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  return cudaSuccess;
+  return ensure_max_dyn_smem(reinterpret_cast<const void*>(panel_leaf_kernel<kLeafG>), (int)smem);
 }
 
 cudaError_t launch_panel_leaf(int64_t M, int64_t w, double* P, int64_t lda, const double* tau, int64_t* info,

@@ -2,6 +2,10 @@
 // the default pivot floor tau = n * DBL_EPSILON * ||A||_inf (reading R9).
 #include "ebv_internal.cuh"
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 namespace ebv {
 namespace {
 
@@ -87,6 +91,19 @@ cudaError_t launch_tau(int64_t n, const double* A, int64_t lda, double tau, doub
   norm_inf_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, A, lda, norm_ws);
   tau_kernel<<<1, 1, 0, s>>>(n, norm_ws, tau_out);
   return cudaGetLastError();
+}
+
+cudaError_t ensure_max_dyn_smem(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({fn, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({fn, dev});
+  return e;
 }
 
 }  // namespace ebv
