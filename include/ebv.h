@@ -30,6 +30,10 @@
  *   - Calls are asynchronous on the caller's `stream` (a cudaStream_t passed
  *     as void*; NULL = legacy default stream).  The library never
  *     synchronizes the caller's stream.
+ *   - A context's workspace (pivot floor, arrival counters, solve flags,
+ *     batched scratch) is shared by its calls: calls on one context must be
+ *     ordered (one stream, or streams ordered by events); use one context
+ *     per concurrent stream / host thread.
  *   - Host-detectable argument errors return EBV_ERR_INVALID_VALUE before
  *     anything is launched.  CUDA launch / runtime failures return
  *     EBV_ERR_CUDA; ebv_last_error() gives a one-line description.
