@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--nb", type=int, default=256, help="column block width of the multi-GPU layout")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-plain-first", action="store_true",
+                    help="e2e: copy the first step's inputs before it instead of streaming them in")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-GPU (1D block-cyclic + NCCL) schedule even on one rank")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -353,24 +355,45 @@ def run_ebv(args, rank, world, local):
         ev_in = [torch.cuda.Event(), torch.cuda.Event()]
         ev_done = [torch.cuda.Event(), torch.cuda.Event()]
 
-        def e2e_run(ksteps):
+        # One GPU: the first step has no earlier step to hide its upload
+        # under, so it goes through ebv_lu_factor_host, which streams the
+        # matrix in block by block under its own factorization; the next
+        # step's upload waits for that stream-in to land
+        # (ebv_stream_wait_host_copy) instead of sharing PCIe with it.
+        first_host = not use_dist and not args.e2e_plain_first
+
+        def next_copy(i, ksteps, after_host):
+            if i + 1 >= ksteps:
+                return
+            An, Bn = bufs[(i + 1) % 2]
             with torch.cuda.stream(cs):
-                bufs[0][0].copy_(hA, non_blocking=True)
-                bufs[0][1].copy_(hB, non_blocking=True)
-                ev_in[0].record(cs)
+                if i >= 1:
+                    cs.wait_event(ev_done[(i + 1) % 2])
+                if after_host:
+                    ebv.ebv_stream_wait_host_copy(ctx.handle, cs.cuda_stream)
+                An.copy_(hA, non_blocking=True)
+                Bn.copy_(hB, non_blocking=True)
+                ev_in[(i + 1) % 2].record(cs)
+
+        def e2e_run(ksteps):
+            if not first_host:
+                with torch.cuda.stream(cs):
+                    bufs[0][0].copy_(hA, non_blocking=True)
+                    bufs[0][1].copy_(hB, non_blocking=True)
+                    ev_in[0].record(cs)
             for i in range(ksteps):
                 Ab, Bb = bufs[i % 2]
-                if i + 1 < ksteps:
-                    An, Bn = bufs[(i + 1) % 2]
-                    with torch.cuda.stream(cs):
-                        if i >= 1:
-                            cs.wait_event(ev_done[(i + 1) % 2])
-                        An.copy_(hA, non_blocking=True)
-                        Bn.copy_(hB, non_blocking=True)
-                        ev_in[(i + 1) % 2].record(cs)
-                stream.wait_event(ev_in[i % 2])
-                s, solve = factor_solve(Ab, Bb)
-                s |= solve()
+                if i == 0 and first_host:
+                    Bb.copy_(hB, non_blocking=True)
+                    s = ebv.ebv_lu_factor_host(ctx.handle, n, hA.data_ptr(), n, Ab.data_ptr(), n, 0.0,
+                                               info.data_ptr(), sh)
+                    next_copy(i, ksteps, True)
+                    s |= ebv.ebv_lu_solve(ctx.handle, n, Ab.data_ptr(), n, Bb.data_ptr(), n, nrhs, sh)
+                else:
+                    next_copy(i, ksteps, False)
+                    stream.wait_event(ev_in[i % 2])
+                    s, solve = factor_solve(Ab, Bb)
+                    s |= solve()
                 hX.copy_(Bb, non_blocking=True)
                 ev_done[i % 2].record(stream)
                 if s:
@@ -397,7 +420,9 @@ def run_ebv(args, rank, world, local):
         e2e = {"value": fl * ksteps / (ems / 1e3) / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": int(hA.numel() * 8 + hB.numel() * 8), "d2h_bytes_per_step": int(hX.numel() * 8),
                "ms_per_step": ems / ksteps, "steps": ksteps, "correct": bool(e2e_ok),
-               "pipelined": "next step's H2D on a copy stream under the current step's factor"}
+               "pipelined": ("first step streamed in under its own factorization (ebv_lu_factor_host); each later "
+                             "step's H2D on a copy stream under the previous step, after the stream-in has landed")
+                            if first_host else "next step's H2D on a copy stream under the current step's factor"}
         if not use_dist:
             # one system from host memory through ebv_lu_factor_host (the
             # matrix streams in block by block under the factorization):

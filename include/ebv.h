@@ -170,15 +170,23 @@ ebv_status_t ebv_lu_factor(ebv_context_t ctx, int64_t n, double* A, int64_t lda,
 
 /* A = LU from a HOST-resident matrix: hA (host, column-major, ldh >= n;
  * page-locked memory for full copy speed) is copied to A (device, lda >= n)
- * on `stream` and factored there; A holds the packed LU (bitwise
- * ebv_lu_factor's).  With EBV_PATH_LEFT (and tau >= 0) the column blocks
- * stream in on an internal copy stream under the left-looking factorization
- * instead — every transfer but the first block's hidden, but that schedule
- * is slower on B200 (n = 32768: 1.21 s vs 0.88 s for copy + right-looking;
- * DESIGN.md), so the default copies first.  Errors as ebv_lu_factor, plus
+ * and factored there; A holds the packed LU (bitwise ebv_lu_factor's).
+ * Default (blocked path, tau >= 0, n >= 16384): the column blocks stream in
+ * on an internal copy stream and join the right-looking updates as they
+ * arrive (each late block first catches up on the steps it missed, in
+ * order), so most of the transfer hides under the factorization; smaller n
+ * copy first on `stream`.  With EBV_PATH_LEFT (and tau >= 0) the blocks
+ * stream in under the left-looking schedule.  Errors as ebv_lu_factor, plus
  * INVALID_VALUE for ldh < n or hA NULL. */
 ebv_status_t ebv_lu_factor_host(ebv_context_t ctx, int64_t n, const double* hA, int64_t ldh, double* A,
                                 int64_t lda, double tau, int64_t* d_info, void* stream);
+
+/* Make `stream` wait (asynchronously) until every host-to-device transfer
+ * issued by the latest ebv_lu_factor_host call on ctx has landed — e.g. to
+ * start the next system's upload only after this one's, instead of sharing
+ * the link with it.  No-op if no such call.  Errors: INVALID_VALUE (NULL
+ * ctx), CUDA. */
+ebv_status_t ebv_stream_wait_host_copy(ebv_context_t ctx, void* stream);
 
 /* X from LY = B then UX = Y (Eq 1; "UX = B" read as UX = Y, R6).
  *   LU     device, the packed output of ebv_lu_factor (column-major, lda)

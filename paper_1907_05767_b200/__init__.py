@@ -46,6 +46,7 @@ SIGNATURES = {
     "ebv_lu_factor_banded": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _d, _vp, _vp]),
     "ebv_lu_solve_banded": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _vp]),
     "ebv_lu_factor_band": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _d, _vp, _vp]),
+    "ebv_stream_wait_host_copy": (_int, [_vp, _vp]),
     "ebv_lu_solve_band": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _vp]),
     "ebv_batched_shard": (_int, [_i64, _int, _int, _vp, _vp]),
     "ebv_lu_factor_host": (_int, [_vp, _i64, _vp, _i64, _vp, _i64, _d, _vp, _vp]),
@@ -210,6 +211,10 @@ def lu_solve_banded(LU: torch.Tensor, B: torch.Tensor, kl: int, ku: int, ctx: Co
     _check(ebv_lu_solve_banded(ctx.handle, n, kl, ku, LU.data_ptr(), max(_colmajor_ld(LU), 1), X.data_ptr(),
                                max(n, 1), X.shape[1], _stream_handle(LU.device)), "ebv_lu_solve_banded")
     return X[:, 0] if vec else X
+
+
+def ebv_stream_wait_host_copy(ctx, stream):
+    return lib().ebv_stream_wait_host_copy(ctx, stream)
 
 
 def ebv_lu_factor_band(ctx, n, kl, ku, AB, ldab, tau, d_info, stream):

@@ -642,6 +642,7 @@ ebv_status_t ebv_destroy(ebv_context_t c) {
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_p) cudaEventDestroy(c->ev_p);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
+  if (c->hostcopy_ev) cudaEventDestroy(c->hostcopy_ev);
   delete c;
   return EBV_SUCCESS;
 }
@@ -803,11 +804,18 @@ ebv_status_t ebv_lu_factor_host(ebv_context_t c, int64_t n, const double* hA, in
   cudaError_t e = timed(c, KC_OTHER, 0, 0, s, 1, [&] { return launch_set_info0(d_info, s); });
   if (e != cudaSuccess) return cuda_fail(e, "info init");
   if (n == 0) return EBV_SUCCESS;
+  if (!c->hostcopy_ev) {
+    e = cudaEventCreateWithFlags(&c->hostcopy_ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e, "event create");
+  }
+  c->hostcopy_valid = false;
   if (c->path == EBV_PATH_LEFT && tau >= 0) {
     // left-looking: the column blocks stream in under the factorization
     e = timed(c, KC_OTHER, 0, 0, s, 1, [&] { return launch_tau(n, A, lda, tau, c->d_tau, c->d_norm, s); });
     if (e == cudaSuccess) e = lu_left(c, n, A, lda, d_info, s, hA, ldh);
+    if (e == cudaSuccess && c->copy) e = cudaEventRecord(c->hostcopy_ev, c->copy);
     if (e != cudaSuccess) return cuda_fail(e, "host factor (left-looking)");
+    c->hostcopy_valid = c->copy != nullptr;
     return EBV_SUCCESS;
   }
   if (tau >= 0 && c->nb != -1 && (c->path == EBV_PATH_AUTO || c->path == EBV_PATH_BLOCKED) &&
@@ -815,14 +823,27 @@ ebv_status_t ebv_lu_factor_host(ebv_context_t c, int64_t n, const double* hA, in
     // default: right-looking with the column blocks joining as they arrive
     e = timed(c, KC_OTHER, 0, 0, s, 1, [&] { return launch_tau(n, A, lda, tau, c->d_tau, c->d_norm, s); });
     if (e == cudaSuccess) e = lu_blocked_stream(c, n, A, lda, d_info, s, hA, ldh);
+    if (e == cudaSuccess) e = cudaEventRecord(c->hostcopy_ev, c->copy);
     if (e != cudaSuccess) return cuda_fail(e, "host factor (streamed)");
+    c->hostcopy_valid = true;
     return EBV_SUCCESS;
   }
   // otherwise: one copy, then the device schedule
   e = cudaMemcpy2DAsync(A, lda * sizeof(double), hA, ldh * sizeof(double), n * sizeof(double), n,
                         cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaEventRecord(c->hostcopy_ev, s);
   if (e != cudaSuccess) return cuda_fail(e, "host copy");
+  c->hostcopy_valid = true;
   return factor_body(c, n, A, lda, tau, d_info, s);
+}
+
+ebv_status_t ebv_stream_wait_host_copy(ebv_context_t c, void* stream) {
+  if (!c) return invalid("ebv_stream_wait_host_copy: NULL ctx");
+  if (!c->hostcopy_valid) return EBV_SUCCESS;
+  DeviceGuard g(c->device);
+  cudaError_t e = cudaStreamWaitEvent((cudaStream_t)stream, c->hostcopy_ev, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "stream wait (host copy)");
+  return EBV_SUCCESS;
 }
 
 ebv_status_t ebv_lu_solve(ebv_context_t c, int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb,

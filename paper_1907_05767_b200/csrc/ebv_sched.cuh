@@ -36,6 +36,8 @@ struct ebv_context {
   cudaEvent_t ev_start = nullptr, ev_a = nullptr, ev_p = nullptr, ev_b = nullptr;
   cudaStream_t copy = nullptr;            // host -> device column blocks (ebv_lu_factor_host)
   std::vector<cudaEvent_t> copy_ev;       // one per column block
+  cudaEvent_t hostcopy_ev = nullptr;      // after the last host copy of the last ebv_lu_factor_host
+  bool hostcopy_valid = false;
   bool stats = false;
   struct Rec {
     int cls;

@@ -93,6 +93,7 @@ def test_argument_validation_without_gpu():
     assert L.ebv_lu_factor_banded(None, 4, 1, 1, None, 4, 0.0, None, None) == 1
     assert L.ebv_lu_solve_banded(None, 4, 1, 1, None, 4, None, 4, 1, None) == 1
     assert L.ebv_lu_factor_band(None, 4, 1, 1, None, 300, 0.0, None, None) == 1
+    assert L.ebv_stream_wait_host_copy(None, None) == 1
     assert L.ebv_lu_solve_band(None, 4, 1, 1, None, 300, None, 4, 1, None) == 1
     assert ebv.batched_shard(10, 2, 3) == (7, 3) and ebv.batched_shard(0, 0, 4) == (0, 0)
     with pytest.raises(ebv.EbvError):
