@@ -568,3 +568,27 @@ def test_batched_medium_info(dev, ctx, n, tau):
     assert info_o[2] == 1
     ok = [s for s in range(batch) if info_o[s] == 0]
     assert bits_eq(At.transpose(1, 2).cpu().numpy()[ok], lu_o[ok])
+
+
+@pytest.mark.parametrize("n", [700, 16384])
+def test_stream_wait_host_copy(dev, ctx, n):
+    """ebv_stream_wait_host_copy orders another stream after the library's
+    host stream-in (copy-first path for n = 700, streamed right-looking path
+    for n = 16384); the factors stay bitwise those of the device path."""
+    d = ebv_inputs.generate(n, seed=5, device=dev, with_b=False)
+    hA = torch.empty(d["At"].shape, dtype=torch.float64, pin_memory=True)
+    hA.copy_(d["At"])
+    A = torch.empty_like(d["At"])
+    A2 = torch.empty_like(d["At"])
+    info = torch.zeros((), dtype=torch.int64, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    assert ebv.ebv_lu_factor_host(ctx.handle, n, hA.data_ptr(), n, A.data_ptr(), n, 0.0, info.data_ptr(),
+                                  s1.cuda_stream) == 0
+    assert ebv.ebv_stream_wait_host_copy(ctx.handle, s2.cuda_stream) == 0
+    with torch.cuda.stream(s2):
+        A2.copy_(hA, non_blocking=True)
+    torch.cuda.synchronize()
+    assert int(info) == 0
+    ref, _ = run_factor(ctx, d["At"].T.clone())
+    assert bits_eq(A.T.cpu().numpy(), ref)
+    assert torch.equal(A2, d["At"])
