@@ -147,6 +147,7 @@ struct ebv_dist_state {
   cudaEvent_t ev_ready[2] = {nullptr, nullptr};   // panel K broadcast complete (side)
   cudaEvent_t ev_free[2] = {nullptr, nullptr};    // step K done reading pbuf[K%2] (main)
   cudaEvent_t ev_next = nullptr;                  // block K+1 columns updated (main)
+  cudaEvent_t ev_brow = nullptr;                  // block row K+1 of the local columns updated (main)
   cudaEvent_t ev_side = nullptr;                  // join point of the side stream
   int* sws = nullptr;           // ring-solve workspace: per RHS group, the two sweeps' row-block
   int64_t sws_cap = 0;          // flags, then one launch ticket per (window, sweep, group)
@@ -162,6 +163,7 @@ ebv_status_t ensure_pbuf(ebv_context* c, ebv_dist_state* d, size_t elems) {
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_free[i], cudaEventDisableTiming);
     }
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_next, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_brow, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_side, cudaEventDisableTiming);
     if (e != cudaSuccess) return cuda_fail(e, "dist events");
   }
@@ -182,6 +184,7 @@ void release_events(ebv_dist_state* d) {
     if (d->ev_free[i]) cudaEventDestroy(d->ev_free[i]);
   }
   if (d->ev_next) cudaEventDestroy(d->ev_next);
+  if (d->ev_brow) cudaEventDestroy(d->ev_brow);
   if (d->ev_side) cudaEventDestroy(d->ev_side);
 }
 
@@ -228,6 +231,18 @@ ebv_status_t dist_factor(ebv_context* c, ebv_dist_state* d, std::vector<View>& v
     return cudaSuccess;
   };
 
+  // U12 lookahead (as in the single-GPU schedule, EBV_U12_LA): step K
+  // updates block row K+1 of every rank's columns before the rows below, and
+  // the side stream solves U12 of step K+1 (after panel K+1's broadcast)
+  // while the caller stream updates the rest; per entry the same operations
+  // in the same order (bitwise).
+  static const int kDistU12La = [] {
+    const char* ev = getenv("EBV_U12_LA");
+    return ev ? atoi(ev) : -1;
+  }();
+  const bool u12la = kDistU12La >= 0 ? kDistU12La != 0 : n >= 16384;
+  bool u12_done = false;   // U12 of the current step was solved on the side stream
+
   e = prepare_panel(0);
   if (e != cudaSuccess) return cuda_fail(e, "dist panel");
   for (int64_t K = 0; K < N; K++) {
@@ -243,12 +258,25 @@ ebv_status_t dist_factor(ebv_context* c, ebv_dist_state* d, std::vector<View>& v
       if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(panel)");
       c->launches += 1;
     }
+    if (u12_done) {   // U12 of this step for every local column after block K, on the side stream
+      e = cudaStreamWaitEvent(side, d->ev_brow, 0);
+      for (auto& v : views) {
+        if (e != cudaSuccess) break;
+        const int64_t lc0 = suffix_after(v.plan, K);
+        const int64_t ncols = v.plan.cols - lc0;
+        if (ncols > 0) e = trsm_l(c, w, ncols, pbuf(K), M, v.A + c0 + lc0 * v.lda, v.lda, side);
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "dist U12 (lookahead)");
+    }
     e = cudaEventRecord(d->ev_ready[K & 1], side);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, d->ev_ready[K & 1], 0);
     if (e != cudaSuccess) return cuda_fail(e, "dist order");
     // ---- updates of step K on the caller stream; block K+1 first
     const bool has_next = K + 1 < N;
     const int64_t owner1 = has_next ? p0.owner(K + 1) : -1;
+    const int64_t w1 = has_next ? p0.width(K + 1) : 0;
+    // the next step takes the lookahead if its block row has rows below it
+    const bool la_next = u12la && has_next && M - w > w1;
     for (auto& v : views) {
       const int64_t lc0 = suffix_after(v.plan, K);
       int64_t ncols = v.plan.cols - lc0;
@@ -256,8 +284,8 @@ ebv_status_t dist_factor(ebv_context* c, ebv_dist_state* d, std::vector<View>& v
       double* X = v.A + c0 + lc0 * v.lda;
       int64_t first = 0;
       if (has_next && v.plan.rank == owner1) {
-        const int64_t w1 = p0.width(K + 1);    // block K+1 is the first local block after K
-        e = trsm_l(c, w, w1, pbuf(K), M, X, v.lda, s);
+        // block K+1 is the first local block after K
+        if (!u12_done) e = trsm_l(c, w, w1, pbuf(K), M, X, v.lda, s);
         if (e == cudaSuccess) e = gemm(c, M - w, w1, w, pbuf(K) + w, M, X, v.lda, X + w, v.lda, false, s, KC_UPDATE);
         if (e == cudaSuccess) e = cudaEventRecord(d->ev_next, s);
         if (e != cudaSuccess) return cuda_fail(e, "dist update(next)");
@@ -265,12 +293,31 @@ ebv_status_t dist_factor(ebv_context* c, ebv_dist_state* d, std::vector<View>& v
       }
       if (ncols - first > 0) {
         double* X2 = X + first * v.lda;
-        e = trsm_l(c, w, ncols - first, pbuf(K), M, X2, v.lda, s);
-        if (e == cudaSuccess)
-          e = gemm(c, M - w, ncols - first, w, pbuf(K) + w, M, X2, v.lda, X2 + w, v.lda, false, s, KC_UPDATE);
+        if (!u12_done) e = trsm_l(c, w, ncols - first, pbuf(K), M, X2, v.lda, s);
+        if (e == cudaSuccess) {
+          const int64_t rows = la_next ? w1 : M - w;   // block row K+1 only, the rest below
+          e = gemm(c, rows, ncols - first, w, pbuf(K) + w, M, X2, v.lda, X2 + w, v.lda, false, s, KC_UPDATE);
+        }
         if (e != cudaSuccess) return cuda_fail(e, "dist update");
       }
     }
+    if (la_next) {
+      e = cudaEventRecord(d->ev_brow, s);
+      for (auto& v : views) {
+        if (e != cudaSuccess) break;
+        const int64_t lc0 = suffix_after(v.plan, K);
+        int64_t ncols = v.plan.cols - lc0;
+        if (ncols <= 0) continue;
+        double* X = v.A + c0 + lc0 * v.lda;
+        const int64_t first = (v.plan.rank == owner1) ? w1 : 0;
+        if (ncols - first <= 0) continue;
+        double* X2 = X + first * v.lda;
+        e = gemm(c, M - w - w1, ncols - first, w, pbuf(K) + w + w1, M, X2, v.lda, X2 + w + w1, v.lda, false, s,
+                 KC_UPDATE);
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "dist update (rows below)");
+    }
+    u12_done = la_next;
     e = cudaEventRecord(d->ev_free[K & 1], s);
     if (e != cudaSuccess) return cuda_fail(e, "dist order");
     // ---- lookahead: panel K+1 on the side stream once its columns are updated

@@ -45,3 +45,15 @@ def test_u12_lookahead_bitwise():
     env = dict(os.environ, EBV_U12_LA="1")
     out = subprocess.run([sys.executable, "-c", CHILD, ROOT], env=env, capture_output=True, text=True, timeout=900)
     assert out.returncode == 0 and "OK" in out.stdout, out.stdout[-2000:] + out.stderr[-4000:]
+
+
+@pytest.mark.gpu
+def test_u12_lookahead_distributed_emulated_bitwise():
+    """The distributed schedule's U12 lookahead (ebv_dist.cu), forced on for
+    the emulated P-rank tests of tests/test_gpu_dist.py (bitwise against the
+    oracle there)."""
+    env = dict(os.environ, EBV_U12_LA="1")
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                          os.path.join(ROOT, "tests", "test_gpu_dist.py"), "-k", "emulated"],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
