@@ -241,3 +241,53 @@ def generate_band(n: int, kl: int, ku: int, pad: int, ldab: int, seed: int = 1, 
     AB[j, pad + ku] = dunits.to(torch.float64) * SCALE
     B_u = rowdot + dunits[:, None] * X_u
     return {"AB": AB, "X": X_u.to(torch.float64), "B": B_u.to(torch.float64) * SCALE, "n": n, "seed": seed}
+
+
+# ---------------------------------------------------------------- edge-case flavours
+EDGE_FLAVOURS = ("neg", "rowsign", "colsign", "scaled", "rhs_tiny", "rhs_huge")
+
+
+def _signs(n: int, seed: int, salt: int, device) -> torch.Tensor:
+    rows = torch.arange(n, dtype=torch.int64, device=device)
+    return ((hash32(hash32(torch.full_like(rows, _h(seed) ^ salt)) ^ rows) & 1) * 2 - 1).to(torch.float64)
+
+
+def _pow2(n: int, seed: int, salt: int, emax: int, device) -> torch.Tensor:
+    rows = torch.arange(n, dtype=torch.int64, device=device)
+    e = (hash32(hash32(torch.full_like(rows, _h(seed) ^ salt)) ^ rows) % (2 * emax + 1)) - emax
+    return torch.ldexp(torch.ones(n, dtype=torch.float64, device=device), e)
+
+
+def edge_flavour(A: torch.Tensor, B: torch.Tensor, flavour: str, seed: int = 1, emax: int = 500):
+    """Sign / scale variants of a generated system (A logical (..., n, n), B
+    (..., n, nrhs)) that exercise the division edge cases: negative and
+    mixed-sign pivots, multipliers and quotients far outside [2^-54, 2^54]
+    (subnormal / tiny ones, which the kernels' verified-quotient tests send to
+    their true-division branches).  Every transform multiplies rows / columns
+    by signs and powers of two, so it is exact (no method arithmetic):
+      neg       A' = -A, B' = -B                       (x unchanged)
+      rowsign   A' = S1 A, B' = S1 B                   (row signs: mixed pivots)
+      colsign   A' = A S2                              (x' = S2 x; B unchanged)
+      scaled    A' = D1 S1 A S2 D2, B' = D1 S1 B       (D = 2^e, |e| <= emax)
+      rhs_tiny  A' = 2^530 A, B' = 2^-530 B            (x' = 2^-1060 x: subnormal quotients)
+      rhs_huge  A' = 2^-500 A, B' = 2^500 B            (x' = 2^1000 x)
+    Returns (A', B') as new tensors of A's / B's dtype and device."""
+    n = A.shape[-1]
+    dev = A.device
+    if flavour == "neg":
+        return -A, -B
+    if flavour == "rowsign":
+        s = _signs(n, seed, 0x1B873593, dev)
+        return A * s[:, None], B * s[:, None]
+    if flavour == "colsign":
+        s = _signs(n, seed, 0x2F7A1C3D, dev)
+        return A * s[None, :], B.clone()
+    if flavour == "scaled":
+        s1 = _signs(n, seed, 0x1B873593, dev) * _pow2(n, seed, 0x3C6EF372, emax, dev)
+        s2 = _signs(n, seed, 0x2F7A1C3D, dev) * _pow2(n, seed, 0x5BD1E995, emax, dev)
+        return A * s1[:, None] * s2[None, :], B * s1[:, None]
+    if flavour == "rhs_tiny":
+        return torch.ldexp(A, torch.tensor(530, device=dev)), torch.ldexp(B, torch.tensor(-530, device=dev))
+    if flavour == "rhs_huge":
+        return torch.ldexp(A, torch.tensor(-500, device=dev)), torch.ldexp(B, torch.tensor(500, device=dev))
+    raise ValueError(flavour)

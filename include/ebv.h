@@ -163,8 +163,9 @@ ebv_status_t ebv_set_vector_ctas(ebv_context_t ctx, int64_t ctas);
  *   d_info device int64: written with 0 or the first failing 1-based step
  *   stream cudaStream_t
  * Errors (synchronous, nothing launched): INVALID_VALUE for n < 0,
- * lda < max(1,n), A or d_info NULL (when n > 0), or PATH_VECTOR with
- * n > EBV_VECTOR_MAX_N. */
+ * lda < max(1,n), A or d_info NULL (when n > 0), PATH_VECTOR with
+ * n > EBV_VECTOR_MAX_N, or a distributed context (ebv_create_dist: use
+ * ebv_lu_factor_dist; ebv_lu_solve and ebv_lu_factor_host reject it too). */
 ebv_status_t ebv_lu_factor(ebv_context_t ctx, int64_t n, double* A, int64_t lda, double tau,
                            int64_t* d_info, void* stream);
 
@@ -342,8 +343,11 @@ ebv_status_t ebv_dist_local_blocks(int64_t n, int64_t nb, int rank, int nranks, 
 
 /* Distributed A = LU (Eq 6): A_local is this rank's slab (device, column-
  * major, lda >= n), factored in place; d_info (device int64) receives the
- * global first failing step on every rank.  tau must be >= 0 (the default
- * floor would need a global norm: NOT_SUPPORTED).  Collective. */
+ * global first failing step on every rank.  tau < 0 selects the default
+ * floor n*eps*||A||_inf from the global row sums (each rank's partial row
+ * sums added by an NCCL all-reduce: bitwise the single-GPU floor when the
+ * row sums are exact, else equal up to the summation order, reading R18).
+ * Collective. */
 ebv_status_t ebv_lu_factor_dist(ebv_context_t ctx, int64_t n, double* A_local, int64_t lda, double tau,
                                 int64_t* d_info, void* stream);
 
@@ -384,6 +388,24 @@ ebv_status_t ebv_plan_units(int64_t n, int64_t workers, int32_t* tri0, int32_t* 
 /* Owner rank of column block J of N blocks over nranks under `layout`
  * (-1 on invalid arguments). */
 int64_t ebv_block_owner(int64_t J, int64_t N, int64_t nranks, ebv_layout_t layout);
+
+/* ---- debug knobs (validation; process-wide per device) -------------------- */
+/* flags:
+ *   EBV_DEBUG_FORCE_EXACT  every verified-quotient test (the Markstein
+ *       quotient from a hoisted reciprocal used on the division chains of
+ *       the solve, leaf, vector and batched kernels) reports "unverified", so
+ *       every such step takes its redo-with-true-division branch.  Results
+ *       must not change (they are RN(y/u) either way); slower.
+ *   EBV_DEBUG_JITTER  pseudo-random sleeps (0..4 us) before cross-CTA flag
+ *       releases, to stress the flag protocols' ordering.
+ * spin_timeout_s: bound on any one cross-CTA flag wait; a wait that exceeds
+ * it traps (the launch fails with a CUDA error instead of hanging the GPU).
+ * 0 = unbounded; the default is 60 s.  Applies to kernels launched on
+ * `device` after the call.  Errors: INVALID_VALUE (unknown flag, bad device,
+ * timeout < 0), CUDA. */
+#define EBV_DEBUG_FORCE_EXACT 1u
+#define EBV_DEBUG_JITTER 2u
+ebv_status_t ebv_set_debug(int device, unsigned flags, double spin_timeout_s);
 
 /* ---- measurement --------------------------------------------------------- */
 

@@ -76,7 +76,9 @@ SIGNATURES = {
     "ebv_stats_get": (_int, [_vp, _int, ctypes.POINTER(_i64), ctypes.POINTER(_d), ctypes.POINTER(_d),
                              ctypes.POINTER(_d)]),
     "ebv_launch_count": (_i64, [_vp]),
+    "ebv_set_debug": (_int, [_int, ctypes.c_uint, _d]),
 }
+EBV_DEBUG_FORCE_EXACT, EBV_DEBUG_JITTER = 1, 2
 
 _lib = None
 
@@ -350,6 +352,17 @@ def ebv_block_owner(J, N, nranks, layout=EBV_LAYOUT_CYCLIC) -> int:
 
 def ebv_launch_count(ctx) -> int:
     return lib().ebv_launch_count(ctx)
+
+
+def ebv_set_debug(device: int, flags: int, spin_timeout_s: float = 60.0):
+    return lib().ebv_set_debug(device, flags, spin_timeout_s)
+
+
+def set_debug(flags: int = 0, spin_timeout_s: float = 60.0, device: int = 0):
+    """Debug knobs of include/ebv.h (EBV_DEBUG_FORCE_EXACT: every verified
+    quotient takes its true-division redo branch; EBV_DEBUG_JITTER: random
+    sleeps before cross-CTA flag releases; a bound on flag waits)."""
+    _check(ebv_set_debug(device, flags, spin_timeout_s), "ebv_set_debug")
 
 
 def load_nccl():

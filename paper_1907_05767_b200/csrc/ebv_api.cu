@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include "ebv_device.cuh"
 #include "ebv_sched.cuh"
 
 namespace ebv {
@@ -703,6 +704,7 @@ ebv_status_t ebv_lu_factor(ebv_context_t c, int64_t n, double* A, int64_t lda, d
   if (!d_info) return invalid("ebv_lu_factor: d_info is NULL");
   if (n > 0 && !A) return invalid("ebv_lu_factor: A is NULL");
   if (c->path == EBV_PATH_VECTOR && n > EBV_VECTOR_MAX_N) return invalid("ebv_lu_factor: n too large for PATH_VECTOR");
+  if (c->dist) return invalid("ebv_lu_factor: distributed context (A would be read as a full n x n matrix; use ebv_lu_factor_dist)");
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   // CUDA Graph replay of the blocked schedule: the second call with the same
@@ -776,8 +778,10 @@ static ebv_status_t factor_body(ebv_context_t c, int64_t n, double* A, int64_t l
       return EBV_ERR_NOT_SUPPORTED;
     }
     double fl = 2.0 / 3.0 * n * n * n, by = 16.0 * n * n;
+    const int ep = (int)(c->vector_epoch % 0x3FFFFFF0) + 1;   // this context's flags, its own epochs
+    c->vector_epoch++;
     e = timed(c, KC_VECTOR, fl, by, s, 2, [&] {
-      return launch_vector_lu(n, A, lda, c->d_tau, d_info, c->d_vflags, c->d_scratch, C, s);
+      return launch_vector_lu(n, A, lda, c->d_tau, d_info, c->d_vflags, c->d_scratch, C, ep, s);
     });
     if (e != cudaSuccess) return cuda_fail(e, "vector path");
     return EBV_SUCCESS;
@@ -799,6 +803,8 @@ ebv_status_t ebv_lu_factor_host(ebv_context_t c, int64_t n, const double* hA, in
   if (lda < (n > 1 ? n : 1) || ldh < (n > 1 ? n : 1)) return invalid("ebv_lu_factor_host: leading dimension < n");
   if (!d_info) return invalid("ebv_lu_factor_host: d_info is NULL");
   if (n > 0 && (!A || !hA)) return invalid("ebv_lu_factor_host: NULL matrix pointer");
+  if (c->path == EBV_PATH_VECTOR && n > EBV_VECTOR_MAX_N) return invalid("ebv_lu_factor_host: n too large for PATH_VECTOR");
+  if (c->dist) return invalid("ebv_lu_factor_host: distributed context (use ebv_lu_factor_dist)");
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = timed(c, KC_OTHER, 0, 0, s, 1, [&] { return launch_set_info0(d_info, s); });
@@ -853,6 +859,7 @@ ebv_status_t ebv_lu_solve(ebv_context_t c, int64_t n, const double* LU, int64_t 
   if (lda < (n > 1 ? n : 1) || ldb < (n > 1 ? n : 1)) return invalid("ebv_lu_solve: leading dimension too small");
   if (n == 0 || nrhs == 0) return EBV_SUCCESS;
   if (!LU || !B) return invalid("ebv_lu_solve: NULL pointer");
+  if (c->dist) return invalid("ebv_lu_solve: distributed context (use ebv_lu_solve_dist)");
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   if (solve_use_trsm(n, nrhs)) {
@@ -868,11 +875,11 @@ ebv_status_t ebv_lu_solve(ebv_context_t c, int64_t n, const double* LU, int64_t 
   const int64_t NB = (n + solve_block_rows() - 1) / solve_block_rows();
   ebv_status_t st = ensure_flags(c, 2 * NB * solve_max_interleave());   // interleaved columns per sweep
   if (st != EBV_SUCCESS) return st;
-  c->solve_epoch++;
-  const int64_t groups = (nrhs + 63) / 64;
+  const int64_t groups = (nrhs + 63) / 64, ep0 = c->solve_epoch;
+  c->solve_epoch += launch_solve_epochs(nrhs);
   double by = (8.0 * n * n + 4.0 * 8.0 * n * nrhs), fl = 2.0 * n * n * nrhs;
   cudaError_t e = timed(c, KC_SOLVE, fl, by, s, (int)(2 * groups), [&] {
-    return launch_solve(n, LU, lda, B, ldb, nrhs, c->d_ticket, c->d_flags, c->solve_epoch, s);
+    return launch_solve(n, LU, lda, B, ldb, nrhs, c->d_ticket, c->d_flags, ep0, s);
   });
   if (e != cudaSuccess) return cuda_fail(e, "solve");
   return EBV_SUCCESS;
@@ -946,11 +953,11 @@ static ebv_status_t solve_banded_impl(ebv_context_t c, int64_t n, int64_t kl, in
   const int64_t NB = (n + solve_block_rows() - 1) / solve_block_rows();
   ebv_status_t st = ensure_flags(c, 2 * NB * solve_max_interleave());
   if (st != EBV_SUCCESS) return st;
-  c->solve_epoch++;
-  const int64_t groups = (nrhs + 63) / 64;
+  const int64_t groups = (nrhs + 63) / 64, ep0 = c->solve_epoch;
+  c->solve_epoch += launch_solve_epochs(nrhs);
   const double bw = (double)(kl + ku + 1) < n ? (double)(kl + ku + 1) : (double)n;
   cudaError_t e = timed(c, KC_SOLVE, 2.0 * n * bw * nrhs, 8.0 * n * bw + 32.0 * n * nrhs, s, (int)(2 * groups), [&] {
-    return launch_solve(n, LU, lda, B, ldb, nrhs, c->d_ticket, c->d_flags, c->solve_epoch, s, kl, ku);
+    return launch_solve(n, LU, lda, B, ldb, nrhs, c->d_ticket, c->d_flags, ep0, s, kl, ku);
   });
   if (e != cudaSuccess) return cuda_fail(e, "banded solve");
   return EBV_SUCCESS;
@@ -991,6 +998,11 @@ static ebv_status_t batched_medium(ebv_context_t c, int64_t n, double* A, int64_
   constexpr int64_t NB = 64;
   cudaError_t e = cudaSuccess;
   if (!solve_only) {
+    // the counters' offset depends on this call's batch, so an earlier call
+    // with another batch may have left its tau / info words there: clear them
+    // (the leaves reset them to zero after every launch from then on)
+    e = cudaMemsetAsync(counts, 0, batch * sizeof(int), s);
+    if (e != cudaSuccess) return cuda_fail(e, "batched medium counters");
     e = timed(c, KC_OTHER, 0, tau < 0 ? 8.0 * n * n * batch : 0, s, 1,
               [&] { return launch_batched_prep(n, A, lda, sA, batch, tau, tau_s, info64, s); });
     for (int64_t c0 = 0; c0 < n && e == cudaSuccess; c0 += NB) {
@@ -1200,6 +1212,25 @@ int64_t ebv_block_owner(int64_t J, int64_t N, int64_t nranks, ebv_layout_t layou
     }
   }
   return -1;
+}
+
+// ---- debug knobs ------------------------------------------------------------------
+
+ebv_status_t ebv_set_debug(int device, unsigned flags, double spin_timeout_s) {
+  if (flags & ~(unsigned)(EBV_DEBUG_FORCE_EXACT | EBV_DEBUG_JITTER)) return invalid("ebv_set_debug: unknown flag");
+  if (!(spin_timeout_s >= 0.0) || spin_timeout_s > 1e6) return invalid("ebv_set_debug: spin timeout out of range");
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (device < 0 || device >= count) return invalid("ebv_set_debug: bad device");
+  DeviceGuard g(device);
+  DebugCfg cfg{flags, (unsigned long long)(spin_timeout_s * 1e9)};
+  e = set_debug_solve(cfg);
+  if (e == cudaSuccess) e = set_debug_vector(cfg);
+  if (e == cudaSuccess) e = set_debug_batched(cfg);
+  if (e == cudaSuccess) e = set_debug_leaf(cfg);
+  if (e != cudaSuccess) return cuda_fail(e, "ebv_set_debug");
+  return EBV_SUCCESS;
 }
 
 // ---- measurement ---------------------------------------------------------------

@@ -383,8 +383,9 @@ ebv_status_t dist_solve(ebv_context* c, ebv_dist_state* d, std::vector<View>& vi
   int* tick = d->sws + nflags;
   cudaError_t e = cudaMemsetAsync(tick, 0, ntick * sizeof(int), s);
   if (e != cudaSuccess) return cuda_fail(e, "ring-solve tickets");
-  c->solve_epoch++;
+  // one epoch for the whole ring solve (its flags are per (group, sweep))
   const int ep = (int)(c->solve_epoch % 0x3FFFFFF0) + 1;
+  c->solve_epoch++;
   ncclResult_t r = ncclSuccess;
   for (int pass = 0; pass < 2; pass++) {
     const bool fwd = pass == 0;
@@ -420,14 +421,49 @@ ebv_status_t dist_solve(ebv_context* c, ebv_dist_state* d, std::vector<View>& vi
   return EBV_SUCCESS;
 }
 
-ebv_status_t check_common(ebv_context* c, int64_t n, int64_t lda, double tau, int P) {
+ebv_status_t check_common(ebv_context* c, int64_t n, int64_t lda, int P) {
   if (!c) return invalid("dist: NULL ctx");
   if (n < 0 || P < 1) return invalid("dist: bad size");
   if (lda < (n > 1 ? n : 1)) return invalid("dist: lda < n");
-  if (tau < 0) {
-    set_error("dist: the default pivot floor (tau < 0) needs a global norm; pass tau >= 0");
-    return EBV_ERR_NOT_SUPPORTED;
+  return EBV_SUCCESS;
+}
+
+// The pivot floor of a distributed factorization (before any update): tau
+// as given, or (tau < 0) the default n * eps * ||A||_inf (reading R9) from
+// the global row absolute sums — each rank sums its local columns (j
+// ascending), the partial sums are added over the ranks (ncclAllReduce sum;
+// emulation: rank order), and the maximum row sum gives the floor.  For
+// inputs whose row sums are exact (the generator's 2^-30 grid) this is
+// bitwise the single-GPU floor; otherwise it can differ in the last bits
+// (reading R18: the norm's summation order is unspecified).
+ebv_status_t dist_tau(ebv_context* c, ebv_dist_state* d, std::vector<View>& views, int64_t n, double tau,
+                      cudaStream_t s) {
+  cudaError_t e = launch_tau(n, nullptr, n > 0 ? n : 1, tau >= 0 ? tau : 0.0, c->d_tau, c->d_norm, s);
+  c->launches += 1;
+  if (e != cudaSuccess) return cuda_fail(e, "dist tau");
+  if (tau >= 0 || n == 0) return EBV_SUCCESS;
+  if (n > c->vec_cap) {
+    if (c->d_vec) cudaFree(c->d_vec);
+    c->d_vec = nullptr;
+    c->vec_cap = 0;
+    if (cudaMalloc(&c->d_vec, n * sizeof(double)) != cudaSuccess) { set_error("workspace alloc failed"); return EBV_ERR_ALLOC; }
+    c->vec_cap = n;
   }
+  bool first = true;
+  for (auto& v : views) {
+    e = launch_rowabs(n, v.A, v.lda, v.plan.cols, c->d_vec, first, s);
+    if (e != cudaSuccess) return cuda_fail(e, "dist row sums");
+    c->launches += 1;
+    first = false;
+  }
+  if (d->comm && d->nranks > 1) {
+    ncclResult_t r = nccl().AllReduce(c->d_vec, c->d_vec, (size_t)n, ncclFloat64, ncclSum, d->comm, s);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce(row sums)");
+    c->launches += 1;
+  }
+  e = launch_tau_from_rows(n, c->d_vec, c->d_tau, s);
+  c->launches += 1;
+  if (e != cudaSuccess) return cuda_fail(e, "dist tau");
   return EBV_SUCCESS;
 }
 
@@ -503,18 +539,18 @@ ebv_status_t ebv_lu_factor_dist(ebv_context_t c, int64_t n, double* A_local, int
                                 void* stream) {
   if (!c || !c->dist) return invalid("ebv_lu_factor_dist: not a distributed context");
   ebv_dist_state* d = c->dist;
-  ebv_status_t st = check_common(c, n, lda, tau, d->nranks);
+  ebv_status_t st = check_common(c, n, lda, d->nranks);
   if (st != EBV_SUCCESS) return st;
   if (!d_info) return invalid("ebv_lu_factor_dist: d_info NULL");
+  std::vector<View> views{View{make_plan(n, d->nb, d->rank, d->nranks, d->layout), A_local, lda}};
+  if (views[0].plan.cols > 0 && !A_local) return invalid("ebv_lu_factor_dist: A_local NULL");
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = launch_set_info0(d_info, s);
-  if (e == cudaSuccess) e = launch_tau(n, nullptr, lda, tau, c->d_tau, c->d_norm, s);
   if (e != cudaSuccess) return cuda_fail(e, "dist init");
-  c->launches += 2;
-  if (n == 0) return EBV_SUCCESS;
-  std::vector<View> views{View{make_plan(n, d->nb, d->rank, d->nranks, d->layout), A_local, lda}};
-  if (views[0].plan.cols > 0 && !A_local) return invalid("ebv_lu_factor_dist: A_local NULL");
+  c->launches += 1;
+  st = dist_tau(c, d, views, n, tau, s);
+  if (st != EBV_SUCCESS || n == 0) return st;
   return dist_factor(c, d, views, n, d_info, s);
 }
 
@@ -522,7 +558,7 @@ ebv_status_t ebv_lu_solve_dist(ebv_context_t c, int64_t n, const double* LU_loca
                                int64_t nrhs, void* stream) {
   if (!c || !c->dist) return invalid("ebv_lu_solve_dist: not a distributed context");
   ebv_dist_state* d = c->dist;
-  ebv_status_t st = check_common(c, n, lda, 0.0, d->nranks);
+  ebv_status_t st = check_common(c, n, lda, d->nranks);
   if (st != EBV_SUCCESS) return st;
   if (nrhs < 0 || ldb < (n > 1 ? n : 1)) return invalid("ebv_lu_solve_dist: bad B");
   if (n == 0 || nrhs == 0) return EBV_SUCCESS;
@@ -534,20 +570,20 @@ ebv_status_t ebv_lu_solve_dist(ebv_context_t c, int64_t n, const double* LU_loca
 
 ebv_status_t ebv_lu_factor_dist_emulated(ebv_context_t c, int64_t n, int nranks, int64_t nb, ebv_layout_t layout,
                                          double* const* slabs, int64_t lda, double tau, int64_t* d_info, void* stream) {
-  ebv_status_t st = check_common(c, n, lda, tau, nranks);
+  ebv_status_t st = check_common(c, n, lda, nranks);
   if (st != EBV_SUCCESS) return st;
   if (nb <= 0 || nb % 64) return invalid("emulated: nb must be a positive multiple of 64");
   if (!d_info || (n > 0 && !slabs)) return invalid("emulated: NULL pointer");
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = launch_set_info0(d_info, s);
-  if (e == cudaSuccess) e = launch_tau(n, nullptr, lda, tau, c->d_tau, c->d_norm, s);
   if (e != cudaSuccess) return cuda_fail(e, "emulated init");
-  if (n == 0) return EBV_SUCCESS;
   ebv_dist_state tmp;
   tmp.nranks = nranks; tmp.nb = nb; tmp.layout = layout;
   std::vector<View> views;
   for (int r = 0; r < nranks; r++) views.push_back(View{make_plan(n, nb, r, nranks, layout), slabs[r], lda});
+  st = dist_tau(c, &tmp, views, n, tau, s);
+  if (st != EBV_SUCCESS || n == 0) return st;
   st = dist_factor(c, &tmp, views, n, d_info, s);
   cudaStreamSynchronize(s);   // the temporary panel buffers / events die with tmp
   if (tmp.pbuf) cudaFree(tmp.pbuf);
@@ -558,7 +594,7 @@ ebv_status_t ebv_lu_factor_dist_emulated(ebv_context_t c, int64_t n, int nranks,
 ebv_status_t ebv_lu_solve_dist_emulated(ebv_context_t c, int64_t n, int nranks, int64_t nb, ebv_layout_t layout,
                                         double* const* slabs, int64_t lda, double* B, int64_t ldb, int64_t nrhs,
                                         void* stream) {
-  ebv_status_t st = check_common(c, n, lda, 0.0, nranks);
+  ebv_status_t st = check_common(c, n, lda, nranks);
   if (st != EBV_SUCCESS) return st;
   if (nb <= 0 || nb % 64) return invalid("emulated: nb must be a positive multiple of 64");
   if (nrhs < 0 || ldb < (n > 1 ? n : 1)) return invalid("emulated: bad B");
@@ -569,7 +605,11 @@ ebv_status_t ebv_lu_solve_dist_emulated(ebv_context_t c, int64_t n, int nranks, 
   tmp.nranks = nranks; tmp.nb = nb; tmp.layout = layout;
   std::vector<View> views;
   for (int r = 0; r < nranks; r++) views.push_back(View{make_plan(n, nb, r, nranks, layout), slabs[r], lda});
-  return dist_solve(c, &tmp, views, n, B, ldb, nrhs, (cudaStream_t)stream);
+  st = dist_solve(c, &tmp, views, n, B, ldb, nrhs, (cudaStream_t)stream);
+  // the temporary solve workspace dies with tmp (after the launches using it)
+  cudaStreamSynchronize((cudaStream_t)stream);
+  if (tmp.sws) cudaFree(tmp.sws);
+  return st;
 }
 
 }  // extern "C"

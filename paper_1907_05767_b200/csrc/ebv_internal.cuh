@@ -83,6 +83,8 @@ cudaError_t launch_solve(int64_t n, const double* LU, int64_t lda, double* B, in
                          int* ticket_ws, int* flags_ws, int64_t epoch, cudaStream_t s,
                          int64_t kl = -1, int64_t ku = -1);
 int64_t solve_block_rows();
+// flag epochs one launch_solve call consumes (base + 1 .. base + this)
+int64_t launch_solve_epochs(int64_t nrhs);
 
 // Batched n <= 32 fused factor + solve.
 cudaError_t launch_batched(int64_t n, double* A, int64_t lda, int64_t strideA, int64_t batch, double* B,
@@ -92,9 +94,17 @@ cudaError_t launch_batched(int64_t n, double* A, int64_t lda, int64_t strideA, i
 
 // Vector-level EbV path (persistent cooperative kernel).
 cudaError_t launch_vector_lu(int64_t n, double* A, int64_t lda, const double* tau, int64_t* info,
-                             int* flags_ws, double* lbuf_ws, int num_ctas, cudaStream_t s);
+                             int* flags_ws, double* lbuf_ws, int num_ctas, int epoch, cudaStream_t s);
 int vector_max_ctas(int device, int64_t n);
 size_t vector_smem_bytes(int64_t n, int num_ctas);
+
+// Debug knobs (ebv_set_debug): each kernel translation unit's setter of its
+// __constant__ copy (ebv_device.cuh, EBV_DEBUG_SETTER).
+struct DebugCfg;
+cudaError_t set_debug_solve(const DebugCfg& cfg);
+cudaError_t set_debug_vector(const DebugCfg& cfg);
+cudaError_t set_debug_batched(const DebugCfg& cfg);
+cudaError_t set_debug_leaf(const DebugCfg& cfg);
 
 // Utilities.
 cudaError_t launch_set_info0(int64_t* info, cudaStream_t s);
@@ -107,6 +117,12 @@ cudaError_t ensure_max_dyn_smem(const void* fn, int bytes);
 cudaError_t launch_batched_prep(int64_t n, const double* A, int64_t lda, int64_t sA, int64_t batch, double tau,
                                 double* tau_s, int64_t* info64, cudaStream_t s);
 cudaError_t launch_info_to_i32(int64_t batch, const int64_t* info64, int32_t* info32, cudaStream_t s);
+// distributed default floor: rs[i] (+)= sum_j |A[i + j*lda]| over cols
+// local columns (j ascending; first: rs overwritten), then
+// tau_out = n * eps * max_i rs[i]
+cudaError_t launch_rowabs(int64_t n, const double* A, int64_t lda, int64_t cols, double* rs, bool first,
+                          cudaStream_t s);
+cudaError_t launch_tau_from_rows(int64_t n, const double* rs, double* tau_out, cudaStream_t s);
 // tau_out = (tau >= 0) ? tau : n * eps * ||A||_inf  (norm pre-pass)
 cudaError_t launch_tau(int64_t n, const double* A, int64_t lda, double tau, double* tau_out,
                        unsigned long long* norm_ws, cudaStream_t s);

@@ -28,7 +28,8 @@ struct ebv_context {
   int64_t flags_cap = 0;
   int* d_vflags = nullptr;
   int64_t vflags_cap = 0;
-  int64_t solve_epoch = 0;
+  int64_t solve_epoch = 0;  // flag epochs consumed by the wavefront solves (d_flags)
+  int64_t vector_epoch = 0; // flag epochs consumed by the vector path (d_vflags)
   int64_t launches = 0;
   int vector_ctas = 0;      // 0 = auto; < 0 = cyclic map with |value| CTAs (for comparison)
   bool lookahead = true;    // factor panel K+1 on a side stream under the update of step K

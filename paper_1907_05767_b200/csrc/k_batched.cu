@@ -15,6 +15,7 @@
 // solve (Eq 1) follows in registers: forward over L_(k), backward over U_(k).
 // Per-entry arithmetic is exactly the oracle's (bitwise).
 #include "ebv_internal.cuh"
+#include "ebv_device.cuh"
 #include <type_traits>
 
 namespace ebv {
@@ -36,22 +37,8 @@ __device__ __forceinline__ double rcp_approx(double u) {
   e = fma(-u, r, 1.0);
   return fma(r, e, r);
 }
-__device__ __forceinline__ double quot_mk(double y, double u, double r) {
-  const double q0 = y * r;
-  return fma(r, fma(-u, q0, y), q0);
-}
-__device__ __forceinline__ bool quot_exact(double y, double u, double q) {
-  const double rr = fma(-u, q, y);
-  const long long qb = __double_as_longlong(q);
-  const long long e = qb & 0x7ff0000000000000LL;
-  const bool normal = e > (54LL << 52) && e < (0x7feLL << 52);
-  double lim = fabs(u) * __longlong_as_double(e - (53LL << 52));
-  const bool below = (rr < 0.0) != (u < 0.0);
-  const bool pow2 = (qb & 0x000fffffffffffffLL) == 0;
-  if (pow2 && below == (q > 0.0)) lim *= 0.5;
-  const bool pzero = __double_as_longlong(y) == 0;
-  return pzero || (normal && fabs(rr) < lim);
-}
+__device__ __forceinline__ double quot_mk(double y, double u, double r) { return dev::quot_mk(y, u, r); }
+__device__ __forceinline__ bool quot_exact(double y, double u, double q) { return dev::quot_is_rn(y, u, q); }
 
 // Row updates of rows that may sit above the pivot are guarded by a branch
 // around a chunk of CH fma's (a predicated fma is if-converted by ptxas into
@@ -417,3 +404,5 @@ cudaError_t launch_batched(int64_t n, double* A, int64_t lda, int64_t strideA, i
 }
 
 }  // namespace ebv
+
+EBV_DEBUG_SETTER(set_debug_batched)

@@ -14,6 +14,7 @@
 // with an identity: padded multipliers are exactly 0 and fma(-0, u, a) == a,
 // so the real entries see exactly the same operation sequence.
 #include "ebv_internal.cuh"
+#include "ebv_device.cuh"
 #include <cstdlib>
 
 namespace ebv {
@@ -107,27 +108,10 @@ __global__ void __launch_bounds__(W * GD) leaf_lu_kernel(int w, double* __restri
 // unverified quotient redoes its rows with true division, so every entry is
 // RN(x/u) — bitwise the oracle — and the chain per step is three dependent
 // fp64 operations instead of a division.
-__device__ __forceinline__ double quot_m(double y, double u, double r) {   // Markstein: q0 + r (y - u q0)
-  const double q0 = y * r;
-  return fma(r, fma(-u, q0, y), q0);
-}
-// exact test that q == RN(y / u): the remainder y - u q (exact by fma) is
-// below half an ulp of q times |u| (halved below a power of two on the side
-// of the smaller ulp); +0 dividends (the identity padding) are exact
-__device__ __forceinline__ bool quot_ok(double y, double u, double q) {
-  const double rr = fma(-u, q, y);
-  const long long qb = __double_as_longlong(q);
-  const long long e = qb & 0x7ff0000000000000LL;
-  const bool normal = e > (54LL << 52) && e < (0x7feLL << 52);
-  double lim = fabs(u) * __longlong_as_double(e - (53LL << 52));
-  const bool below = (rr < 0.0) != (u < 0.0);
-  const bool pow2 = (qb & 0x000fffffffffffffLL) == 0;
-  if (pow2 && below == (q > 0.0)) lim *= 0.5;
-  // y = +0 (the identity padding): the sequence returns +0 / -0 for u > 0 /
-  // u < 0, which is RN(y/u) exactly
-  const bool pzero = __double_as_longlong(y) == 0;
-  return pzero || (normal && fabs(rr) < lim);
-}
+__device__ __forceinline__ double quot_m(double y, double u, double r) { return dev::quot_mk(y, u, r); }
+// exact test that q == RN(y / u) (dev::quot_is_rn; +0 dividends — the
+// identity padding — are exact)
+__device__ __forceinline__ bool quot_ok(double y, double u, double q) { return dev::quot_is_rn(y, u, q); }
 
 // RR rows per lane group (independent chains interleaved): a CTA of 256
 // threads covers 32*RR rows, so the kernel holds few SM slots for its
@@ -584,3 +568,5 @@ cudaError_t launch_trsm_luu_batched(int64_t k, int64_t m, const double* U, int64
 }
 
 }  // namespace ebv
+
+EBV_DEBUG_SETTER(set_debug_leaf)

@@ -21,6 +21,7 @@
 // right-hand side, lane l owning rows l and l+32, shuffles broadcasting
 // y_k / x_k; the block's values are stored and its flag released.
 #include "ebv_internal.cuh"
+#include "ebv_device.cuh"
 
 namespace ebv {
 namespace {
@@ -44,7 +45,11 @@ __device__ __forceinline__ void wait_flag(const int* p, int v, bool next_in_chai
   // others (accumulating further tiles) back off, keeping the flag's L2
   // slice free for the release store on the critical path
   const unsigned ns = next_in_chain ? 32 : 1000;
-  while (ld_relaxed(p) != v) __nanosleep(ns);
+  dev::SpinGuard g;
+  while (ld_relaxed(p) != v) {
+    __nanosleep(ns);
+    g.poll();
+  }
   asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
 }
 __device__ __forceinline__ void st_release(int* p, int v) {
@@ -70,34 +75,14 @@ __device__ __forceinline__ unsigned long long gtime() {
   } while (0)
 #endif
 
-// y / u from a precomputed reciprocal r = RN(1/u): q = RN(y r), one Newton
-// correction with the exact residual (the divisor-independent tail of the
-// hardware division sequence), so the chained step costs three dependent
-// FP64 ops instead of a full division.  The owner lane verifies that q is
-// the correctly rounded quotient: with rr = y - q u (exact), the true
-// quotient is q + rr/u, and q = RN(y/u) iff |rr| < |u| ulp(q)/2 — or
-// |u| ulp(q)/4 when q is a power of two and the quotient lies below it;
-// ties and non-normal q count as unverified.  The caller redoes the block
-// with true division if any step is unverified, so the result is always
-// RN(y/u), bitwise the oracle's division.
-__device__ __forceinline__ double quot_nc(double y, double u, double r) {
-  const double q0 = y * r;
-  return fma(r, fma(-u, q0, y), q0);
-}
-// the exact test, applied after the block's sweep (off the step chain: the
-// owner lane keeps its step's dividend and quotient)
-__device__ __forceinline__ bool quot_chk(double y, double u, double q) {
-  const double rr = fma(-u, q, y);                                 // exact remainder y - q u
-  const long long qb = __double_as_longlong(q);
-  const long long e = qb & 0x7ff0000000000000LL;
-  const bool normal = e > (54LL << 52) && e < (0x7feLL << 52);
-  double lim = fabs(u) * __longlong_as_double(e - (53LL << 52));     // |u| ulp(q) / 2, exact
-  const bool below = (rr < 0.0) != (u < 0.0);                        // true quotient < |q| side
-  const bool pow2 = (qb & 0x000fffffffffffffLL) == 0;
-  if (pow2 && below == (q > 0.0)) lim *= 0.5;                        // toward zero from 2^e
-  const bool pzero = __double_as_longlong(y) == 0;                   // +0 / u: exact (skipped steps)
-  return pzero || (normal && fabs(rr) < lim);
-}
+// y / u from a precomputed reciprocal r = RN(1/u): the Markstein step
+// (dev::quot_mk, three dependent FP64 ops on the chain instead of a full
+// division); the owner lane keeps its step's dividend and quotient and the
+// exact test (dev::quot_is_rn) runs after the block's sweep, off the step
+// chain; a block with an unverified quotient is redone with true division,
+// so the result is always RN(y/u), bitwise the oracle's division.
+__device__ __forceinline__ double quot_nc(double y, double u, double r) { return dev::quot_mk(y, u, r); }
+__device__ __forceinline__ bool quot_chk(double y, double u, double q) { return dev::quot_is_rn(y, u, q); }
 
 // Window form (the multi-GPU ring solve, ebv_dist.cu): only the column
 // blocks [jlo, jhi) (units of BR) take part, addressed as
@@ -357,7 +342,10 @@ __global__ void __launch_bounds__(BR) solve_kernel(int64_t n, const double* __re
     // orders them at CTA scope; the gpu-scope release is cumulative)
     __syncthreads();
     EBV_TR(4);
-    if (i == 0) st_release(flags + I, epoch);
+    if (i == 0) {
+      dev::jitter((unsigned)I);
+      st_release(flags + I, epoch);
+    }
     EBV_TR(5);
   }
 }
@@ -404,7 +392,10 @@ cudaError_t launch_solve(int64_t n, const double* LU, int64_t lda, double* B, in
     const int nind = (int)((nrhs - g0) < kMaxInterleave ? (nrhs - g0) : kMaxInterleave);
     for (int pass = 0; pass < 2; pass++) {
       const bool fwd = pass == 0;
-      const int ep = (int)(((epoch * 64 + (g0 / kMaxInterleave) * 2 + pass) % 0x3FFFFFFF) + 1);
+      // epochs base+1 .. base+2*groups: one per (group, sweep) launch, so no
+      // two launches of this or any later call share one (the caller advances
+      // its counter by launch_solve_epochs(nrhs) after the call)
+      const int ep = (int)(((epoch + (g0 / kMaxInterleave) * 2 + pass) % 0x3FFFFFF0) + 1);
       cudaError_t e = cudaMemsetAsync(ticket_ws + pass, 0, sizeof(int), s);
       if (e != cudaSuccess) return e;
       e = fwd ? launch_one<true>(n, LU, lda, B + g0 * ldb, ldb, 1, ticket_ws, flags_ws, ep, NB, s, 0, NB, 0, nind, kl,
@@ -435,7 +426,11 @@ cudaError_t launch_solve_window(int64_t n, const double* LUw, int64_t ldl, int64
              : launch_one<false>(n, LUw, ldl, B, ldb, 1, ticket, flags, epoch, units, s, jlo, jhi, c0, nind);
 }
 
+int64_t launch_solve_epochs(int64_t nrhs) { return 2 * ((nrhs + kMaxInterleave - 1) / kMaxInterleave); }
+
 int64_t solve_max_rhs() { return MAXR; }
 int64_t solve_max_interleave() { return kMaxInterleave; }
 
 }  // namespace ebv
+
+EBV_DEBUG_SETTER(set_debug_solve)

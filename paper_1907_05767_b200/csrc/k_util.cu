@@ -55,6 +55,30 @@ __global__ void batched_prep_kernel(int64_t n, const double* __restrict__ A, int
   }
 }
 
+// distributed default floor: partial row absolute sums over a rank's local
+// columns (j ascending), accumulated into rs (first: overwrite)
+__global__ void rowabs_kernel(int64_t n, const double* __restrict__ A, int64_t lda, int64_t cols, double* rs,
+                              bool first) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = first ? 0.0 : rs[i];
+  for (int64_t j = 0; j < cols; j++) s += fabs(A[i + j * lda]);
+  rs[i] = s;
+}
+
+__global__ void tau_from_rows_kernel(int64_t n, const double* __restrict__ rs, double* tau_out) {
+  __shared__ double red[1024];
+  double m = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, rs[i]);
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *tau_out = (double)n * 2.220446049250313e-16 * red[0];
+}
+
 __global__ void info_to_i32_kernel(int64_t batch, const int64_t* info64, int32_t* info32) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s < batch) info32[s] = (int32_t)info64[s];
@@ -72,6 +96,18 @@ cudaError_t launch_batched_prep(int64_t n, const double* A, int64_t lda, int64_t
 cudaError_t launch_info_to_i32(int64_t batch, const int64_t* info64, int32_t* info32, cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
   info_to_i32_kernel<<<(unsigned)((batch + 255) / 256), 256, 0, s>>>(batch, info64, info32);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rowabs(int64_t n, const double* A, int64_t lda, int64_t cols, double* rs, bool first,
+                          cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  rowabs_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, A, lda, cols, rs, first);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tau_from_rows(int64_t n, const double* rs, double* tau_out, cudaStream_t s) {
+  tau_from_rows_kernel<<<1, 1024, 0, s>>>(n, rs, tau_out);
   return cudaGetLastError();
 }
 

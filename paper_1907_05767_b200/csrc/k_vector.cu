@@ -26,6 +26,7 @@
 // n = 1024): flag hop ~0.5 us, apply ~3.5 us, diagonal block ~3 us (eight
 // dependent divisions), rows below ~3.5 us.
 #include "ebv_internal.cuh"
+#include "ebv_device.cuh"
 
 #include <cstdlib>
 #include <type_traits>
@@ -43,8 +44,10 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 // saves the extra round trip of a relaxed poll followed by a fence
 __device__ __forceinline__ void wait_flag(const int* p, int v) {
   int t;
+  dev::SpinGuard g;
   do {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(t) : "l"(p) : "memory");
+    g.poll();
   } while (t != v);
 }
 
@@ -52,17 +55,8 @@ __device__ __forceinline__ void wait_flag(const int* p, int v) {
 // unless the exact remainder proves q correctly rounded (then the caller
 // redoes the row with true division) — same test as k_solve.cu's quot().
 __device__ __forceinline__ double quot(double y, double u, double r, bool& ok) {
-  const double q0 = y * r;
-  const double q = fma(r, fma(-u, q0, y), q0);
-  const double rr = fma(-u, q, y);
-  const long long qb = __double_as_longlong(q);
-  const long long e = qb & 0x7ff0000000000000LL;
-  const bool normal = e > (54LL << 52) && e < (0x7feLL << 52);
-  double lim = fabs(u) * __longlong_as_double(e - (53LL << 52));
-  const bool below = (rr < 0.0) != (u < 0.0);
-  const bool pow2 = (qb & 0x000fffffffffffffLL) == 0;
-  if (pow2 && below == (q > 0.0)) lim *= 0.5;
-  ok = ok && normal && fabs(rr) < lim;
+  const double q = dev::quot_mk(y, u, r);
+  ok = ok && dev::quot_is_rn(y, u, q);
   return q;
 }
 
@@ -393,7 +387,7 @@ int vector_max_ctas(int device, int64_t n) {
 }
 
 cudaError_t launch_vector_lu(int64_t n, double* A, int64_t lda, const double* tau, int64_t* info, int* flags_ws,
-                             double* lbuf_ws, int num_ctas, cudaStream_t s) {
+                             double* lbuf_ws, int num_ctas, int epoch, cudaStream_t s) {
   // lbuf_ws is used as the 8-byte info accumulator (min over failing steps)
   unsigned long long* info_min = reinterpret_cast<unsigned long long*>(lbuf_ws);
   cudaError_t e = cudaMemsetAsync(info_min, 0xFF, sizeof(unsigned long long), s);
@@ -410,8 +404,6 @@ cudaError_t launch_vector_lu(int64_t n, double* A, int64_t lda, const double* ta
   const size_t smem = smem_for(n, num_ctas, bw);
   e = cudaFuncSetAttribute(vector_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  static int epoch = 0;
-  epoch = (epoch % 0x3FFFFFF0) + 1;
   int nn = (int)n, ep = epoch, cy = cyclic, bwv = bw, mcv = mc, cbv = chunk_blocks();
   void* args[] = {&nn, &A, &lda, (void*)&tau, &info_min, &flags_ws, &ep, &cy, &bwv, &mcv, &cbv};
   e = cudaLaunchCooperativeKernel((void*)vector_lu_kernel, dim3(C), dim3(VT), args, smem, s);
@@ -421,3 +413,5 @@ cudaError_t launch_vector_lu(int64_t n, double* A, int64_t lda, const double* ta
 }
 
 }  // namespace ebv
+
+EBV_DEBUG_SETTER(set_debug_vector)

@@ -152,6 +152,38 @@ def test_dist_errors(dev, ctx):
     info = torch.zeros((), dtype=torch.int64, device=dev)
     # not a distributed context
     assert L.ebv_lu_factor_dist(ctx.handle, 4, None, 4, 0.0, info.data_ptr(), None) == 1
-    # default pivot floor is not available in the distributed schedule
-    st = ebv.ebv_lu_factor_dist_emulated(ctx.handle, 4, 2, 64, 0, [0, 0], 4, -1.0, info.data_ptr(), None)
-    assert st == 5
+    # a distributed context is rejected by the single-GPU entry points
+    uid = ebv.ebv_get_unique_id()
+    h = ebv.ebv_create_dist(0, uid, 0, 1, 64, 0)
+    try:
+        A = torch.eye(4, dtype=torch.float64, device=dev)
+        assert L.ebv_lu_factor(h, 4, A.data_ptr(), 4, 0.0, info.data_ptr(), None) == 1
+        assert L.ebv_lu_solve(h, 4, A.data_ptr(), 4, A.data_ptr(), 4, 1, None) == 1
+        assert L.ebv_lu_factor_host(h, 4, A.cpu().data_ptr(), 4, A.data_ptr(), 4, 0.0, info.data_ptr(), None) == 1
+    finally:
+        ebv.ebv_destroy(h)
+
+
+@pytest.mark.parametrize("P,nb,n", [(3, 64, 700), (2, 128, 1000), (1, 64, 300)])
+def test_emulated_dist_default_pivot_floor(dev, ctx, P, nb, n):
+    """tau < 0 in the distributed schedule: the default floor n*eps*||A||_inf
+    from the ranks' partial row sums (added in rank order here, by an NCCL
+    all-reduce on real ranks) — the same floor and the same info as the
+    single-GPU factorization (the generator's row sums are exact)."""
+    d = ebv_inputs.generate(n, seed=n + P, nrhs=1, device=dev)
+    At = d["At"].clone()
+    k = 2 * nb + 5
+    At[:, k] = 0.0             # row k and column k of A zero: an isolated 1 x 1 block,
+    At[k, :] = 0.0             # so u_kk = a_kk = 1e-300, far below the default floor
+    At[k, k] = 1e-300          # (info = k + 1), and every other factor entry stays finite
+    slabs, colmaps = slabs_for({"At": At}, n, nb, P, 0, dev)
+    info = torch.zeros((), dtype=torch.int64, device=dev)
+    sh = torch.cuda.current_stream().cuda_stream
+    assert ebv.ebv_lu_factor_dist_emulated(ctx.handle, n, P, nb, 0, [s.data_ptr() for s in slabs], n, -1.0,
+                                           info.data_ptr(), sh) == 0, ebv.ebv_last_error()
+    ctx.set_block(nb)
+    LU1, info1 = ebv.lu_factor(At.T, tau=-1.0, ctx=ctx)
+    ctx.set_block(0)
+    torch.cuda.synchronize()
+    assert int(info) == int(info1) > 0
+    assert bits_eq(assemble(slabs, colmaps, n), LU1.cpu().numpy())
