@@ -48,7 +48,10 @@ def parse():
     ap.add_argument("--impl", default="ebv", choices=["ebv", "reference"])
     ap.add_argument("--n", type=int, default=N_DEFAULT)
     ap.add_argument("--nrhs", type=int, default=1)
-    ap.add_argument("--nb", type=int, default=256, help="column block width of the multi-GPU layout")
+    ap.add_argument("--nb", type=int, default=256,
+                    help="column block width of the multi-GPU layout (every N, and the dist-schedule N=1 leg)")
+    ap.add_argument("--no-dist-n1", action="store_true",
+                    help="N=1: skip timing the multi-GPU schedule on one rank beside the headline")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-plain-first", action="store_true",
@@ -191,7 +194,10 @@ def cpu_baseline(args):
     return {"value": 2.0 / 3.0 * m ** 3 / dt / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
             "sample": (f"leading {m}x{m} principal submatrix of the n={args.n} matrix (same entries), one serial "
                        f"oracle factor + solve, {dt:.2f} s, GFLOP/s = (2/3) m^3 / t; correct={ok}"),
-            "seconds": dt}
+            "seconds": dt,
+            "extrapolated_full_n_seconds": dt * (args.n / m) ** 3,
+            "extrapolation": f"t(m) * (n/m)^3: the O(n^3) factor dominates; the oracle's rate at m={m} held "
+                             f"constant (context only, not measured at n={args.n})"}
 
 
 def dmma_peak_tflops():
@@ -231,18 +237,28 @@ def run_ebv(args, rank, world, local):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     n, nrhs, nb = args.n, args.nrhs, args.nb
-    stream = torch.cuda.current_stream(dev)
+    # everything on one non-default stream (the library captures the blocked
+    # schedule into a CUDA graph on non-default streams)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     sh = stream.cuda_stream
     info = torch.zeros((), dtype=torch.int64, device=dev)
     use_dist = world > 1 or args.force_dist
-    if use_dist:
-        # one system over all ranks: 1D block-cyclic slabs, NCCL panel broadcast
+    dctx = None       # distributed context (N > 1, or the dist-schedule leg at N = 1)
+
+    def make_dist_ctx():
         uid = [ebv.ebv_get_unique_id() if rank == 0 else None]
         if world > 1:
             dist.broadcast_object_list(uid, src=0)
-        handle = ebv.ebv_create_dist(local, uid[0], rank, world, nb, ebv.EBV_LAYOUT_CYCLIC)
-        ctx = ebv.Context.__new__(ebv.Context)
-        ctx.device, ctx.handle = local, handle
+        h = ebv.ebv_create_dist(local, uid[0], rank, world, nb, ebv.EBV_LAYOUT_CYCLIC)
+        c = ebv.Context.__new__(ebv.Context)
+        c.device, c.handle = local, h
+        return c
+
+    if use_dist:
+        # one system over all ranks: 1D block-cyclic slabs, NCCL panel broadcast
+        dctx = make_dist_ctx()
+        ctx = dctx
         cols = ebv.dist_local_columns(n, nb, rank, world, ebv.EBV_LAYOUT_CYCLIC)
         d = ebv_inputs.generate(n, seed=args.seed, nrhs=nrhs, device=dev,
                                 cols=torch.tensor(cols, dtype=torch.int64))
@@ -257,21 +273,21 @@ def run_ebv(args, rank, world, local):
     Aw = torch.empty_like(A0)
     Bw = torch.empty_like(B0)
 
-    def factor_solve(Ab=None, Bb=None):
+    def factor_solve(c, distp, Ab=None, Bb=None):
         Ab = Aw if Ab is None else Ab
         Bb = Bw if Bb is None else Bb
-        if use_dist:
-            s = ebv.ebv_lu_factor_dist(ctx.handle, n, Ab.data_ptr(), n, 0.0, info.data_ptr(), sh)
-            return s, lambda: ebv.ebv_lu_solve_dist(ctx.handle, n, Ab.data_ptr(), n, Bb.data_ptr(), n, nrhs, sh)
-        s = ebv.ebv_lu_factor(ctx.handle, n, Ab.data_ptr(), n, 0.0, info.data_ptr(), sh)
-        return s, lambda: ebv.ebv_lu_solve(ctx.handle, n, Ab.data_ptr(), n, Bb.data_ptr(), n, nrhs, sh)
+        if distp:
+            s = ebv.ebv_lu_factor_dist(c.handle, n, Ab.data_ptr(), n, 0.0, info.data_ptr(), sh)
+            return s, lambda: ebv.ebv_lu_solve_dist(c.handle, n, Ab.data_ptr(), n, Bb.data_ptr(), n, nrhs, sh)
+        s = ebv.ebv_lu_factor(c.handle, n, Ab.data_ptr(), n, 0.0, info.data_ptr(), sh)
+        return s, lambda: ebv.ebv_lu_solve(c.handle, n, Ab.data_ptr(), n, Bb.data_ptr(), n, nrhs, sh)
 
-    def step(ev=None):
+    def step(c, distp, ev=None):
         Aw.copy_(A0)
         Bw.copy_(B0)
         if ev:
             ev[0].record(stream)
-        s, solve = factor_solve()
+        s, solve = factor_solve(c, distp)
         if ev:
             ev[1].record(stream)
         s |= solve()
@@ -280,46 +296,69 @@ def run_ebv(args, rank, world, local):
         if s:
             raise RuntimeError(ebv.ebv_last_error())
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    ok = int(info) == 0
-    err = (Bw.T - Xtrue).abs().max().item()
-    ok = ok and err <= 1e-10
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
 
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    def measure(c, distp, steps, warmup, clk=None):
+        """warmup untimed steps, then `steps` timed ones bracketed by a barrier
+        and device syncs; the library's statistics stay OFF (graph replay on)."""
+        for _ in range(warmup):
+            step(c, distp)
+        torch.cuda.synchronize()
+        good = int(info) == 0
+        e = (Bw.T - Xtrue).abs().max().item()
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        if clk:
+            clk.start()
+        l0 = c.launch_count()
+        t0.record(stream)
+        for k in range(steps):
+            step(c, distp, evs[k])
+        t1.record(stream)
+        torch.cuda.synchronize()
+        nl = c.launch_count() - l0
+        ck = clk.stop() if clk else None
+        if world > 1:
+            dist.barrier()
+        ms = max_over_ranks(t0.elapsed_time(t1))
+        e = max(e, (Bw.T - Xtrue).abs().max().item())
+        good = good and int(info) == 0 and e <= 1e-10
+        return {"region_ms": ms, "f_ms": [x[0].elapsed_time(x[1]) for x in evs],
+                "s_ms": [x[1].elapsed_time(x[2]) for x in evs], "launches": nl, "clocks": ck,
+                "correct": bool(good), "err": e}
+
+    fl = 2.0 / 3.0 * n ** 3
     clk = ClockSampler(local)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clk.start()
+    main_run = measure(ctx, use_dist, args.steps, args.warmup, clk)
+    region_ms = main_run["region_ms"]
+    value = fl * args.steps / (region_ms / 1e3) / 1e9    # one system per step (strong scaling)
+    f_med = max_over_ranks(statistics.median(main_run["f_ms"]))
+    s_med = max_over_ranks(statistics.median(main_run["s_ms"]))
+
+    # ---- roofline: a separate instrumented pass (per-launch CUDA events on
+    # the launching streams; graphs off while instrumented), so the headline
+    # above is timed uninstrumented
     ctx.stats_reset()
     ctx.stats_enable(True)
-    l0 = ctx.launch_count()
-    t_start.record(stream)
-    for k in range(args.steps):
-        step(evs[k])
-    t_end.record(stream)
+    isteps = 1
+    for _ in range(isteps):
+        step(ctx, use_dist)
     torch.cuda.synchronize()
     ctx.stats_enable(False)
-    launches = ctx.launch_count() - l0
-    clocks = clk.stop()
-    if world > 1:
-        dist.barrier()
-    region_ms = t_start.elapsed_time(t_end)
-    f_ms = [e[0].elapsed_time(e[1]) for e in evs]
-    s_ms = [e[1].elapsed_time(e[2]) for e in evs]
     st = ctx.stats()
-    if world > 1:
-        t = torch.tensor([region_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        region_ms = t.item()
-    fl = 2.0 / 3.0 * n ** 3
-    value = fl * args.steps / (region_ms / 1e3) / 1e9    # one system per step (strong scaling)
     g = st["update"]   # the trailing rank-nb update (Eq 6-c) launches: the dominant kernel
     peak = dmma_peak_tflops()
     achieved = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else None
+    if world > 1:   # the slowest rank's kernel rate
+        achieved = -max_over_ranks(-(achieved or 0.0))
     traffic = ncu_traffic()
     total_kernel_ms = sum(v["ms"] for v in st.values())
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -329,11 +368,30 @@ def run_ebv(args, rank, world, local):
                 "traffic_algorithmic_bytes": (traffic or {}).get("algorithmic_bytes"),
                 "kernel": "gemm_tma_kernel as the trailing rank-nb update (TMA-fed DMMA.8x8x4, Eq 6-c); the "
                           "same kernel's small launches inside the recursive TRSMs / panels are class gemm_dmma",
-                "launches": g["launches"], "kernel_ms_per_step": g["ms"] / args.steps,
+                "measured_in": f"a separate instrumented pass of {isteps} step(s) after the timed region "
+                               "(library per-launch CUDA events on the launching streams)",
+                "launches": g["launches"], "kernel_ms_per_step": g["ms"] / isteps,
                 "share_of_step": g["ms"] / max(total_kernel_ms, 1e-9),
                 "algorithmic_flops_per_launch": g["flops"] / max(g["launches"], 1),
                 "peak_source": "measured: sm_100a DMMA.8x8x4 issue-rate probe M2 (profiles/r01_probe_dmma.jsonl); "
                                "cuBLAS DGEMM 16384^3 = 36.2 TF (profiles/r01_probe_torch.jsonl)"}
+    kst = {k: {**v, "per_step_ms": v["ms"] / isteps} for k, v in st.items()}
+
+    # ---- N = 1: the multi-GPU schedule on one rank, same nb as the N > 1
+    # runs, so scaling can also be read against the same schedule
+    dist_n1 = None
+    if world == 1 and not use_dist and not args.no_dist_n1:
+        try:
+            dctx = make_dist_ctx()
+            r = measure(dctx, True, max(2, min(args.steps, 3)), 1)
+            dist_n1 = {"value": fl * len(r["f_ms"]) / (r["region_ms"] / 1e3) / 1e9, "unit": "GFLOP/s",
+                       "ms_per_step": r["region_ms"] / len(r["f_ms"]),
+                       "factor_ms": statistics.median(r["f_ms"]), "solve_ms": statistics.median(r["s_ms"]),
+                       "nb": nb, "nccl_ranks": ebv.ebv_dist_nranks(dctx.handle), "correct": r["correct"],
+                       "path": "ebv_lu_factor_dist / ebv_lu_solve_dist: 1D block-cyclic schedule (NCCL panel "
+                               "broadcast, ring solve) on one rank — the N > 1 schedule's 1-GPU point"}
+        except Exception as ex:  # noqa: BLE001
+            dist_n1 = {"error": str(ex)}
 
     # ---- end to end through the public API from pinned host buffers
     e2e = None
@@ -392,7 +450,7 @@ def run_ebv(args, rank, world, local):
                 else:
                     next_copy(i, ksteps, False)
                     stream.wait_event(ev_in[i % 2])
-                    s, solve = factor_solve(Ab, Bb)
+                    s, solve = factor_solve(ctx, use_dist, Ab, Bb)
                     s |= solve()
                 hX.copy_(Bb, non_blocking=True)
                 ev_done[i % 2].record(stream)
@@ -411,11 +469,7 @@ def run_ebv(args, rank, world, local):
         e2e_run(ksteps)
         e1.record(stream)
         torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ems], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = t.item()
+        ems = max_over_ranks(e0.elapsed_time(e1))
         e2e_ok = (hX.T - Xtrue.cpu()).abs().max().item() <= 1e-10
         e2e = {"value": fl * ksteps / (ems / 1e3) / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": int(hA.numel() * 8 + hB.numel() * 8), "d2h_bytes_per_step": int(hX.numel() * 8),
@@ -429,11 +483,11 @@ def run_ebv(args, rank, world, local):
             # single-system latency, no cross-step overlap
             def host_step():
                 Bw.copy_(hB, non_blocking=True)
-                st = ebv.ebv_lu_factor_host(ctx.handle, n, hA.data_ptr(), n, Aw.data_ptr(), n, 0.0, info.data_ptr(),
-                                            sh)
-                st |= ebv.ebv_lu_solve(ctx.handle, n, Aw.data_ptr(), n, Bw.data_ptr(), n, nrhs, sh)
+                st_ = ebv.ebv_lu_factor_host(ctx.handle, n, hA.data_ptr(), n, Aw.data_ptr(), n, 0.0,
+                                             info.data_ptr(), sh)
+                st_ |= ebv.ebv_lu_solve(ctx.handle, n, Aw.data_ptr(), n, Bw.data_ptr(), n, nrhs, sh)
                 hX.copy_(Bw, non_blocking=True)
-                if st:
+                if st_:
                     raise RuntimeError(ebv.ebv_last_error())
             host_step()
             torch.cuda.synchronize()
@@ -444,14 +498,16 @@ def run_ebv(args, rank, world, local):
             hms = e0.elapsed_time(e1)
             e2e["single_system"] = {"api": "ebv_lu_factor_host + ebv_lu_solve", "ms": hms,
                                     "value": fl / (hms / 1e3) / 1e9,
+                                    "note": "per-system latency from pinned host memory (no cross-step overlap)",
                                     "correct": bool((hX.T - Xtrue.cpu()).abs().max().item() <= 1e-10)}
         del hA, hB, hX, Aw2, Bw2
 
+    nccl_ranks = ebv.ebv_dist_nranks(ctx.handle) if use_dist else None
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args)
     out = None
     if rank == 0:
-        cpu = None
-        if not args.no_cpu_baseline and world == 1:
-            cpu = cpu_baseline(args)
         out = {
             "metric": METRIC,
             "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -460,18 +516,22 @@ def run_ebv(args, rank, world, local):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (ebv_inputs counter-hash DD generator, on device)",
             "config": {"workload": f"dense diagonally dominant fp64 n={n}, {nrhs} rhs (BASELINE configs[3])",
                        "n": n, "nrhs": nrhs, "seed": args.seed,
-                       "path": ("1D block-cyclic over %d GPUs, nb=%d, NCCL panel broadcast" % (world, nb)) if use_dist
+                       "path": ("1D block-cyclic over %d GPUs, nb=%d, NCCL panel broadcast, ring solve"
+                                % (world, nb)) if use_dist
                        else "blocked right-looking nb=%d (size-adaptive), recursive panel, lookahead, "
                             "TMA-fed DMMA update" % ctx.block_width(n),
                        "parallelism": f"1d-block-cyclic x{world}" if use_dist else "1 GPU",
                        "l2": "inputs (8.6 GB) larger than L2 (126 MB); no flush needed"},
-            "factor_ms": statistics.median(f_ms), "solve_ms": statistics.median(s_ms),
-            "factor_gflops": fl / (statistics.median(f_ms) / 1e3) / 1e9,
-            "factor_frac_of_peak": fl / (statistics.median(f_ms) / 1e3) / 1e12 / peak,
-            "solve_gbs": 8.0 * n * n / (statistics.median(s_ms) / 1e3) / 1e9,
-            "correct": bool(ok), "max_abs_err_x": err,
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clocks, "kernel_stats": st,
+            "factor_ms": f_med, "solve_ms": s_med,
+            "factor_gflops": fl / (f_med / 1e3) / 1e9,
+            "factor_frac_of_peak": fl / (f_med / 1e3) / 1e12 / peak,
+            "solve_gbs": 8.0 * n * n / (s_med / 1e3) / 1e9,
+            "correct": main_run["correct"], "max_abs_err_x": main_run["err"],
+            "timing": "headline timed with the library statistics off (CUDA-graph replay on); roofline from a "
+                      "separate instrumented pass",
+            "nccl_ranks": nccl_ranks,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(main_run["launches"]),
+            "clocks": main_run["clocks"], "dist_schedule_n1": dist_n1, "kernel_stats": kst,
         }
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -480,9 +540,25 @@ def run_ebv(args, rank, world, local):
     return 0
 
 
+def self_launch(args) -> int:
+    """--gpus N > 1 without a torch.distributed environment: re-launch this
+    script as N ranks (one process per GPU) under torch.distributed.run."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     rank, world, local = dist_env()
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; running {world} ranks", file=sys.stderr)
     if args.impl == "reference":
         return run_reference(args, rank, world)
     return run_ebv(args, rank, world, local)

@@ -336,6 +336,11 @@ ebv_status_t ebv_get_unique_id(void* uid);
 ebv_status_t ebv_create_dist(ebv_context_t* ctx, int device, const void* uid, int rank, int nranks, int64_t nb,
                              ebv_layout_t layout);
 
+/* Number of ranks in the context's NCCL communicator (ncclCommCount; the
+ * nranks given to ebv_create_dist if NCCL cannot report it); -1 for a NULL
+ * or non-distributed context. */
+int ebv_dist_nranks(ebv_context_t ctx);
+
 /* Host, pure: the column blocks rank `rank` owns (ascending J; blocks may be
  * NULL to query the count), their count and the slab width local_cols. */
 ebv_status_t ebv_dist_local_blocks(int64_t n, int64_t nb, int rank, int nranks, ebv_layout_t layout, int64_t* blocks,

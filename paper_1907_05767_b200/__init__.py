@@ -77,6 +77,7 @@ SIGNATURES = {
                              ctypes.POINTER(_d)]),
     "ebv_launch_count": (_i64, [_vp]),
     "ebv_set_debug": (_int, [_int, ctypes.c_uint, _d]),
+    "ebv_dist_nranks": (_int, [_vp]),
 }
 EBV_DEBUG_FORCE_EXACT, EBV_DEBUG_JITTER = 1, 2
 
@@ -392,6 +393,10 @@ def ebv_create_dist(device: int, uid: bytes, rank: int, nranks: int, nb: int = 2
     _check(lib().ebv_create_dist(ctypes.byref(h), device, ctypes.create_string_buffer(uid, 128), rank, nranks,
                                  nb, layout), "ebv_create_dist")
     return h.value
+
+
+def ebv_dist_nranks(ctx) -> int:
+    return lib().ebv_dist_nranks(ctx)
 
 
 def ebv_dist_local_blocks(n: int, nb: int, rank: int, nranks: int, layout: int = EBV_LAYOUT_CYCLIC):

@@ -54,6 +54,7 @@ struct NcclApi {
   decltype(&ncclSend) Send = nullptr;
   decltype(&ncclRecv) Recv = nullptr;
   decltype(&ncclGetErrorString) GetErrorString = nullptr;
+  decltype(&ncclCommCount) CommCount = nullptr;
   bool ok = false;
 };
 
@@ -75,6 +76,7 @@ NcclApi& nccl() {
     EBV_SYM(Send);
     EBV_SYM(Recv);
     EBV_SYM(GetErrorString);
+    EBV_SYM(CommCount);
 #undef EBV_SYM
     api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Broadcast && api.AllReduce &&
              api.Send && api.Recv;
@@ -519,6 +521,14 @@ ebv_status_t ebv_create_dist(ebv_context_t* ctx, int device, const void* uid, in
   (*ctx)->dist = d;
   (*ctx)->nb = nb;
   return EBV_SUCCESS;
+}
+
+int ebv_dist_nranks(ebv_context_t c) {
+  if (!c || !c->dist) return -1;
+  if (!c->dist->comm || !nccl().CommCount) return c->dist->nranks;
+  int count = -1;
+  if (nccl().CommCount(c->dist->comm, &count) != ncclSuccess) return -1;
+  return count;
 }
 
 ebv_status_t ebv_dist_local_blocks(int64_t n, int64_t nb, int rank, int nranks, ebv_layout_t layout, int64_t* blocks,

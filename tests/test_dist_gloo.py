@@ -6,8 +6,10 @@ step schedule of ebv_dist.cu — owner factors the panel, broadcast, every
 rank substitutes / updates its blocks J > K — with numpy arithmetic and a
 gloo broadcast in place of the GPU kernels and NCCL.  The assembled factors
 must match the serial oracle (tolerance: numpy's summation order differs)
-and the ranks' blocks must partition the matrix.  This pins the planner,
-slab indexing, panel packing and the broadcast protocol on CPU."""
+and the ranks' blocks must partition the matrix; the ring solve's protocol
+(owner order, send / recv between consecutive owners, the final broadcast)
+must give every rank the oracle's X.  This pins the planner, slab indexing,
+panel packing and the broadcast / ring protocols on CPU."""
 import os
 import socket
 
@@ -31,6 +33,21 @@ def _panel_lu(P, w):
     for k in range(w):
         P[k + 1:, k] /= P[k, k]
         P[k + 1:, k + 1:w] -= np.outer(P[k + 1:, k], P[k, k + 1:w])
+
+
+def _collect(procs, q, count, timeout=240):
+    """count results from the queue; fails fast if a worker died."""
+    import queue
+    import time
+    out, t0 = [], time.time()
+    while len(out) < count:
+        try:
+            out.append(q.get(timeout=2))
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if not p.is_alive() and p.exitcode not in (0, None)]
+            assert not dead, f"worker failed: exit codes {dead}"
+            assert time.time() - t0 < timeout, "timed out waiting for the workers"
+    return out
 
 
 def _worker(rank, world, port, n, nb, layout, q):
@@ -69,11 +86,46 @@ def _worker(rank, world, port, n, nb, layout, q):
                 L11 = np.tril(panel[:w, :w], -1) + np.eye(w)
                 X[:] = np.linalg.solve(L11, X)            # U12 = L11^-1 A12
                 slab[c0 + w:, lc0:] -= panel[w:, :] @ X   # A22 -= L21 U12
+        # ---- the ring solve of ebv_dist.cu (dist_solve): forward K ascending,
+        # backward K descending; owner(K) receives the right-hand side from
+        # the previous block's owner (when that is another rank), applies its
+        # block column — diagonal block substituted, the rows below (forward)
+        # or above (backward) updated — and sends it to the next block's
+        # owner; X is broadcast from owner(0) at the end
+        d = ebv_inputs.generate(n, seed=3, nrhs=2)
+        b = d["B"].numpy().copy()
+        for fwd in (True, False):
+            order = range(N) if fwd else range(N - 1, -1, -1)
+            for K in order:
+                own = ebv.ebv_block_owner(K, N, world, layout)
+                prev, nxt = (K - 1, K + 1) if fwd else (K + 1, K - 1)
+                if own != rank:
+                    continue
+                bt = torch.from_numpy(b)
+                if 0 <= prev < N and ebv.ebv_block_owner(prev, N, world, layout) != rank:
+                    dist.recv(bt, src=ebv.ebv_block_owner(prev, N, world, layout))
+                b = bt.numpy()
+                c0, w = K * nb, min(nb, n - K * nb)
+                col = slab[:, loc[K]:loc[K] + w]
+                if fwd:
+                    L11 = np.tril(col[c0:c0 + w], -1) + np.eye(w)
+                    b[c0:c0 + w] = np.linalg.solve(L11, b[c0:c0 + w])
+                    b[c0 + w:] -= col[c0 + w:] @ b[c0:c0 + w]
+                else:
+                    U11 = np.triu(col[c0:c0 + w])
+                    b[c0:c0 + w] = np.linalg.solve(U11, b[c0:c0 + w])
+                    b[:c0] -= col[:c0] @ b[c0:c0 + w]
+                if 0 <= nxt < N and ebv.ebv_block_owner(nxt, N, world, layout) != rank:
+                    dist.send(torch.from_numpy(np.ascontiguousarray(b)),
+                              dst=ebv.ebv_block_owner(nxt, N, world, layout))
+        bt = torch.from_numpy(np.ascontiguousarray(b))
+        dist.broadcast(bt, src=ebv.ebv_block_owner(0, N, world, layout))
+        x_ring = bt.numpy().copy()
         out = torch.from_numpy(np.ascontiguousarray(slab.T))
         gathered = [None] * world
-        dist.all_gather_object(gathered, (rank, cols, out))
+        dist.all_gather_object(gathered, (rank, cols, out, x_ring))
         if rank == 0:   # plain numpy through the queue (no shared-memory tensors)
-            gathered = [(r, c, o.numpy().copy()) for r, c, o in gathered]
+            gathered = [(r, c, o.numpy().copy(), x) for r, c, o, x in gathered]
         q.put((rank, blocks, gathered if rank == 0 else None))
     finally:
         dist.destroy_process_group()
@@ -89,7 +141,7 @@ def test_gloo_world2_block_cyclic_schedule(n, nb, layout):
     procs = [ctx.Process(target=_worker, args=(r, world, port, n, nb, layout, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=240) for _ in range(world)]
+    res = _collect(procs, q, world)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -100,12 +152,20 @@ def test_gloo_world2_block_cyclic_schedule(n, nb, layout):
     assert all_blocks == list(range(N))
     gathered = res[0][2]
     full = np.zeros((n, n))
-    for _, cols, out in gathered:
+    for _, cols, out, _x in gathered:
         full[:, cols] = out.T
     import ebv_inputs
-    A = ebv_inputs.generate(n, seed=3)["At"].T.numpy()
+    d = ebv_inputs.generate(n, seed=3, nrhs=2)
+    A = d["At"].T.numpy()
     lu_o, _ = oracle.lu_factor(A)
     assert np.max(np.abs(full - lu_o)) <= 1e-12 * np.max(np.abs(lu_o))
+    # the ring solve: every rank ends with the same X, equal to the oracle's
+    # solve (tolerance: numpy's order) and to the exact solution
+    x_o = oracle.lu_solve(lu_o, d["B"].numpy())
+    xs = [x for _, _, _, x in gathered]
+    assert all(np.array_equal(xs[0], x) for x in xs)
+    assert np.max(np.abs(xs[0] - x_o)) <= 1e-12 * np.max(np.abs(x_o))
+    assert np.max(np.abs(xs[0] - d["X"].numpy())) <= 1e-10
 
 
 def _batched_worker(rank, world, port, batch, n, q):
@@ -143,7 +203,7 @@ def test_gloo_world2_batched_sharding(batch, n):
     procs = [ctx.Process(target=_batched_worker, args=(r, world, port, batch, n, q)) for r in range(world)]
     for p in procs:
         p.start()
-    gathered = q.get(timeout=240)
+    gathered = _collect(procs, q, 1)[0]
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
