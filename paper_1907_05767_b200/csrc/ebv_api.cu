@@ -151,6 +151,12 @@ static int64_t kSolveTrsmRhs = [] {
   const char* e = getenv("EBV_SOLVE_TRSM_RHS");
   return e ? (int64_t)atoll(e) : (int64_t)0;
 }();
+// EBV_SOLVE_CHAIN=0 selects the wavefront kernel (k_solve.cu) for the
+// few-right-hand-side solve instead of the chain-pipelined one (k_solve2.cu)
+static int kSolveChain = [] {
+  const char* e = getenv("EBV_SOLVE_CHAIN");
+  return e ? atoi(e) : 1;
+}();
 static bool solve_use_trsm(int64_t n, int64_t nrhs) {
   if (kSolveTrsmRhs > 0) return nrhs >= kSolveTrsmRhs;
   return nrhs > 128 || (n > 8192 && nrhs > 64) || (n > 16384 && nrhs > 40);
@@ -872,6 +878,21 @@ ebv_status_t ebv_lu_solve(ebv_context_t c, int64_t n, const double* LU, int64_t 
     if (e != cudaSuccess) return cuda_fail(e, "solve (trsm)");
     return EBV_SUCCESS;
   }
+  if (kSolveChain && solve_chain_eligible(n, LU, lda, nrhs)) {
+    // chain-pipelined solve (k_solve2.cu): one chain CTA per right-hand side
+    // walks the diagonal blocks, helper CTAs stream L / U
+    ebv_status_t st = ensure_flags(c, 2 * solve_chain_flags(n));
+    if (st != EBV_SUCCESS) return st;
+    const int64_t ep0 = c->solve_epoch;
+    c->solve_epoch += solve_chain_epochs(nrhs);
+    const int64_t groups = (nrhs + 15) / 16;
+    double by = (8.0 * n * n + 4.0 * 8.0 * n * nrhs), fl = 2.0 * n * n * nrhs;
+    cudaError_t e = timed(c, KC_SOLVE, fl, by, s, (int)(2 * groups), [&] {
+      return launch_solve_chain(n, LU, lda, B, ldb, nrhs, c->d_flags, ep0, s);
+    });
+    if (e != cudaSuccess) return cuda_fail(e, "solve (chain)");
+    return EBV_SUCCESS;
+  }
   const int64_t NB = (n + solve_block_rows() - 1) / solve_block_rows();
   ebv_status_t st = ensure_flags(c, 2 * NB * solve_max_interleave());   // interleaved columns per sweep
   if (st != EBV_SUCCESS) return st;
@@ -1229,6 +1250,7 @@ ebv_status_t ebv_set_debug(int device, unsigned flags, double spin_timeout_s) {
   if (e == cudaSuccess) e = set_debug_vector(cfg);
   if (e == cudaSuccess) e = set_debug_batched(cfg);
   if (e == cudaSuccess) e = set_debug_leaf(cfg);
+  if (e == cudaSuccess) e = set_debug_solve_chain(cfg);
   if (e != cudaSuccess) return cuda_fail(e, "ebv_set_debug");
   return EBV_SUCCESS;
 }

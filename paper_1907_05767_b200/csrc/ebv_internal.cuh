@@ -83,6 +83,14 @@ cudaError_t launch_solve(int64_t n, const double* LU, int64_t lda, double* B, in
                          int* ticket_ws, int* flags_ws, int64_t epoch, cudaStream_t s,
                          int64_t kl = -1, int64_t ku = -1);
 int64_t solve_block_rows();
+// Chain-pipelined solve (k_solve2.cu): eligibility, flag ints per sweep
+// (two sweeps: 2x), epochs consumed per call.
+bool solve_chain_eligible(int64_t n, const double* LU, int64_t lda, int64_t nrhs);
+int64_t solve_chain_flags(int64_t n);
+int64_t solve_chain_epochs(int64_t nrhs);
+cudaError_t launch_solve_chain(int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb, int64_t nrhs,
+                               int* flags_ws, int64_t epoch, cudaStream_t s);
+
 // flag epochs one launch_solve call consumes (base + 1 .. base + this)
 int64_t launch_solve_epochs(int64_t nrhs);
 
@@ -105,6 +113,7 @@ cudaError_t set_debug_solve(const DebugCfg& cfg);
 cudaError_t set_debug_vector(const DebugCfg& cfg);
 cudaError_t set_debug_batched(const DebugCfg& cfg);
 cudaError_t set_debug_leaf(const DebugCfg& cfg);
+cudaError_t set_debug_solve_chain(const DebugCfg& cfg);
 
 // Utilities.
 cudaError_t launch_set_info0(int64_t* info, cudaStream_t s);

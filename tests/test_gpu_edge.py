@@ -86,7 +86,7 @@ def check_factor_solve(ctx, A, B, path=ebv.EBV_PATH_AUTO, nb=0):
 
 
 @pytest.mark.parametrize("flavour", FLAVOURS)
-@pytest.mark.parametrize("n,nrhs,nb", [(700, 1, 0), (1537, 3, 128), (333, 16, -1)])
+@pytest.mark.parametrize("n,nrhs,nb", [(700, 1, 0), (1537, 3, 128), (1538, 3, 128), (333, 16, -1), (334, 16, 0)])
 def test_blocked_edge_bitwise(dev, ctx, force, flavour, n, nrhs, nb):
     """Blocked (panel leaf, U12 leaf solve, DMMA update) and the recursive
     schedule; wavefront solve with 1 / 3 / 16 right-hand sides."""
@@ -117,17 +117,18 @@ def test_batched_edge_bitwise(dev, ctx, force, flavour, n, batch, nrhs):
     db = ebv_inputs.generate_batched(batch, n, seed=n + batch + nrhs, nrhs=nrhs, device=dev)
     A = db["At"].transpose(1, 2)                    # logical (batch, n, n)
     A2, B2 = ebv_inputs.edge_flavour(A, db["B"], flavour, seed=n)
-    At = A2.transpose(1, 2).contiguous()
-    Bt = B2.transpose(1, 2).contiguous()
+    a_np, b_np = A2.cpu().numpy().copy(), B2.cpu().numpy().copy()   # before the in-place factorization
+    At = A2.transpose(1, 2).clone(memory_format=torch.contiguous_format)
+    Bt = B2.transpose(1, 2).clone(memory_format=torch.contiguous_format)
     info = ebv.lu_factor_batched(At, Bt, ctx=ctx)
     torch.cuda.synchronize()
-    lu_o, x_o, info_o = oracle.lu_factor_batched(A2.cpu().numpy(), B2.cpu().numpy())
+    lu_o, x_o, info_o = oracle.lu_factor_batched(a_np, b_np)
     assert bits_eq(info.cpu().numpy(), info_o)
     lu_g, x_g = At.transpose(1, 2).cpu().numpy(), Bt.transpose(1, 2).cpu().numpy()
     assert bits_eq(lu_g, lu_o), first_diff(lu_g, lu_o)
     assert bits_eq(x_g, x_o), first_diff(x_g, x_o)
     # solve-only on the factors (RG > 1 chains for 16 RHS)
-    Bt2 = B2.transpose(1, 2).contiguous()
+    Bt2 = torch.from_numpy(b_np).to(dev).transpose(1, 2).clone(memory_format=torch.contiguous_format)
     ebv.lu_solve_batched(At, Bt2, ctx=ctx)
     torch.cuda.synchronize()
     assert bits_eq(Bt2.transpose(1, 2).cpu().numpy(), x_o)
