@@ -152,7 +152,8 @@ static int64_t kSolveTrsmRhs = [] {
   return e ? (int64_t)atoll(e) : (int64_t)0;
 }();
 // EBV_SOLVE_CHAIN=0 selects the wavefront kernel (k_solve.cu) for the
-// few-right-hand-side solve instead of the chain-pipelined one (k_solve2.cu)
+// few-right-hand-side solve instead of the chain-pipelined one (k_solve2.cu);
+// 2 forces the chain kernel wherever it is eligible
 static int kSolveChain = [] {
   const char* e = getenv("EBV_SOLVE_CHAIN");
   return e ? atoi(e) : 1;
@@ -878,7 +879,13 @@ ebv_status_t ebv_lu_solve(ebv_context_t c, int64_t n, const double* LU, int64_t 
     if (e != cudaSuccess) return cuda_fail(e, "solve (trsm)");
     return EBV_SUCCESS;
   }
-  if (kSolveChain && solve_chain_eligible(n, LU, lda, nrhs)) {
+  // chain kernel: few right-hand sides, or up to 16 on large orders
+  // (profiles/r02_solve_chain.jsonl vs r02_solve_wave.jsonl: n = 8192 with
+  // 8 / 16 columns 2.0 / 2.3 ms vs 1.8 / 2.1 for the wavefront kernel; every
+  // other measured case favours the chain kernel, e.g. n = 32768, 1 RHS:
+  // 3.4 vs 6.6 ms)
+  const bool chain_shape = nrhs <= 4 || (n > 12288 && nrhs <= 16) || kSolveChain > 1;
+  if (kSolveChain && chain_shape && solve_chain_eligible(n, LU, lda, nrhs)) {
     // chain-pipelined solve (k_solve2.cu): one chain CTA per right-hand side
     // walks the diagonal blocks, helper CTAs stream L / U
     ebv_status_t st = ensure_flags(c, 2 * solve_chain_flags(n));

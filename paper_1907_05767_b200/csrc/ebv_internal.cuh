@@ -31,6 +31,11 @@ bool gemm_tma_eligible(int64_t M, int64_t N, int64_t K, const double* A, int64_t
 cudaError_t launch_gemm_sub_tma(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
                                 int64_t ldb, double* C, int64_t ldc, int variant, cudaStream_t s);
 
+// 2-D TMA descriptor (CUtensorMap, 128 bytes at `map`) of a column-major
+// fp64 matrix rows x cols with leading dimension ld and box box0 x box1
+// (out-of-range elements read as zero); false if the driver cannot make it.
+bool make_tma_map_2d(void* map, const double* ptr, int64_t rows, int64_t cols, int64_t ld, int box0, int box1);
+
 // Unblocked LU of one diagonal block (n <= 64) inside one CTA (Eq 6-a..c).
 // Pivot check against *tau (device); the first failing step (1-based,
 // global index koff + k + 1) is written to *info if *info is still 0.

@@ -440,6 +440,10 @@ using TMid3 = TCfg<128, 64, 4, 2, 16, 3, 2>;    // TMid with a 3-stage ring (les
 
 }  // namespace
 
+bool make_tma_map_2d(void* map, const double* ptr, int64_t rows, int64_t cols, int64_t ld, int box0, int box1) {
+  return make_map(reinterpret_cast<CUtensorMap*>(map), ptr, rows, cols, ld, box0, box1);
+}
+
 bool gemm_tma_eligible(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb) {
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return false;
   if ((lda & 1) || (ldb & 1)) return false;

@@ -41,6 +41,8 @@
 // Requirements (else the caller takes the wavefront kernel of k_solve.cu):
 // n even, lda even, LU 16-byte aligned (the diagonal tiles move as 16-byte
 // bulk copies), nrhs <= 16 per launch.
+#include <cuda.h>
+
 #include "ebv_internal.cuh"
 #include "ebv_device.cuh"
 
@@ -48,23 +50,32 @@ namespace ebv {
 namespace {
 
 constexpr int BR = 64;        // rows per block
-constexpr int HL = 6;         // helpers apply tiles s <= t - HL; the chain the last HL-1
+#ifndef EBV_CHAIN_HL
+#define EBV_CHAIN_HL 5
+#endif
+constexpr int HL = EBV_CHAIN_HL;         // helpers apply tiles s <= t - HL; the chain the last HL-1
 constexpr int HR = 8;         // y-history ring (steps)
 constexpr int NT = 192;       // threads per CTA (6 warps; helpers: 3 units of 64)
 constexpr int MAXC = 16;      // right-hand sides per launch (helper accumulators: NRT <= MAXC)
-constexpr int RING = 16;      // absorber register look-ahead (columns; double2 = 4 registers each)
+constexpr int HT = 32;        // columns per half-tile (TMA box 64 x 32: diagonal tiles, helper tiles)
+constexpr int QT = 16;        // columns per quarter-tile (TMA box 64 x 16: the absorbers' stream)
+constexpr int NSLOT = 4;      // quarter-tile slots per block-holder warp
 
 struct ChainSmem {
-  double diag[2][BR * BR];    // diagonal tiles, column-major, double buffered
-  double yh[HR][BR];          // y (x) values of recent steps, in processing order
-  int prog[HR];               // step s: s*128 + number of values produced
-  int fin[HR];                // step s final: 2*(s+1) + redo bit
-  int sdone;                  // solver steps completed
-  int pdone;                  // steps published to global memory
-  unsigned long long mbar[2];
+  double diag[2][BR * BR];        // diagonal tiles, column-major, double buffered (TMA)
+  double slot[4][NSLOT][BR * QT]; // per block-holder warp: quarter-tile slots (TMA)
+  double yh[HR][BR];              // y (x) values of recent steps, in processing order
+  int prog[HR];                   // slot of step s started (sentinels written): s + 1
+  int fin[HR];                    // step s final: 2*(s+1) + redo bit
+  int sdone;                      // solver steps completed
+  int pdone;                      // steps published to global memory
+  unsigned long long mbar_d[2];
+  unsigned long long mbar_s[4][NSLOT];
 };
 struct HelperSmem {
+  double st[NT / 64][2][BR * BR];  // per unit: two tile stages (TMA)
   double ys[NT / 64][BR * MAXC];   // per unit: the published y of one block
+  unsigned long long mbar[NT / 64][2];
 };
 constexpr size_t kSmem = sizeof(ChainSmem) > sizeof(HelperSmem) ? sizeof(ChainSmem) : sizeof(HelperSmem);
 
@@ -99,16 +110,54 @@ __device__ __forceinline__ void wait_sflag_ge(const int* p, int v) {
   dev::SpinGuard g;
   while (ld_acq_cta(p) < v) g.poll();
 }
-
-// the absorbers' wait for the next group of 8 produced values
-__device__ __noinline__ int wait_prog(const int* p, int need) {
-  int cur = ld_acq_cta(p);
+// the same for warps off the critical path: back off so the spin does not
+// take issue slots from the block holder sharing the SM sub-partition
+__device__ __forceinline__ void wait_sflag_ge_slow(const int* p, int v) {
   dev::SpinGuard g;
-  while (cur < need) {
+  while (ld_acq_cta(p) < v) {
+    __nanosleep(64);
     g.poll();
-    cur = ld_acq_cta(p);
   }
-  return cur;
+}
+
+// y (x) values reach the absorbers through the shared history with no
+// per-value fence: the solver fills a step's slot with a sentinel (a
+// signalling-NaN payload no arithmetic produces: results are quiet NaNs)
+// when the step starts, the owner lanes then store each value (a naturally
+// aligned 64-bit store: single-copy atomic), and a reader spins until the
+// values it needs are not the sentinel.
+constexpr long long kSent = 0x7FF4DEADBEEF0001LL;
+__device__ __forceinline__ bool is_sent(double v) { return __double_as_longlong(v) == kSent; }
+__device__ __forceinline__ double2 ld_vol2(const double* p) {
+  double2 v;
+  asm volatile("ld.volatile.shared::cta.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ double ld_vol(const double* p) {
+  double v;
+  asm volatile("ld.volatile.shared::cta.f64 %0, [%1];\n" : "=d"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+// the 8 values yh[j0 .. j0+7] (j0 a multiple of 8), once all are produced
+__device__ __forceinline__ void wait_y8(const double* yh, double (&y)[8]) {
+  dev::SpinGuard g;
+  for (;;) {
+    const double2 a = ld_vol2(yh), b = ld_vol2(yh + 2), c = ld_vol2(yh + 4), d = ld_vol2(yh + 6);
+    y[0] = a.x; y[1] = a.y; y[2] = b.x; y[3] = b.y; y[4] = c.x; y[5] = c.y; y[6] = d.x; y[7] = d.y;
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < 8; i++) ok = ok && !is_sent(y[i]);
+    if (ok) return;
+    g.poll();
+  }
+}
+__device__ __forceinline__ double wait_y1(const double* p) {
+  dev::SpinGuard g;
+  for (;;) {
+    const double v = ld_vol(p);
+    if (!is_sent(v)) return v;
+    g.poll();
+  }
 }
 
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
@@ -131,18 +180,43 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
     if (!done) g.poll();
   } while (!done);
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int row, int col, unsigned long long* bar) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(row), "r"(col), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
-}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ void unit_sync(int unit) {   // 64 threads of one helper unit
   asm volatile("bar.sync %0, 64;\n" ::"r"(unit + 1) : "memory");
 }
+
+#ifdef EBV_CHAIN_TRACE
+// probes/chain_trace.cu: %globaltimer stamps of the chain CTA (column 0)
+__device__ unsigned long long g_ct[4096][14];
+__device__ unsigned long long g_cq[64][4];   // quarter-level stamps of block 20
+#define EBV_CQ(t, q, slot)                                                                 \
+  do {                                                                                     \
+    if (FWD == (EBV_CHAIN_TRACE_FWD != 0) && lane == 0 && (t) == 20 && (q) < 64)           \
+      g_cq[(q)][(slot)] = dev::gtimer();                                                   \
+  } while (0)
+#ifndef EBV_CHAIN_TRACE_FWD
+#define EBV_CHAIN_TRACE_FWD 0
+#endif
+#define EBV_CT(t, slot)                                                                    \
+  do {                                                                                     \
+    if (FWD == (EBV_CHAIN_TRACE_FWD != 0) && lane == 0 && (t) < 4096)                      \
+      g_ct[(t)][(slot)] = dev::gtimer();                                                   \
+  } while (0)
+#else
+#define EBV_CT(t, slot) \
+  do {                  \
+  } while (0)
+#define EBV_CQ(t, q, slot) \
+  do {                     \
+  } while (0)
+#endif
 
 struct Args {
   int64_t n;
@@ -159,6 +233,8 @@ struct Args {
 
 template <bool FWD>
 struct Geo {
+  const double* LU;
+  int64_t lda;
   int64_t n, NB;
   int nvlast;   // valid rows of the last physical block
   __device__ __forceinline__ int64_t phys(int64_t s) const { return FWD ? s : NB - 1 - s; }
@@ -168,45 +244,75 @@ struct Geo {
 };
 
 // ---------------------------------------------------------------------------- helper
+// Tiles (tb, tj), tj = 0 .. tb-HL, stream through two shared-memory stages
+// (2-D TMA, two 64 x 32 boxes each, zero fill past n) one tile ahead of the
+// one being applied; the unit's thread 0 issues them.
+template <bool FWD>
+__device__ __forceinline__ void helper_issue(const CUtensorMap* map, const Geo<FWD>& g, HelperSmem& hs, int unit,
+                                             int64_t tb, int64_t tj) {
+  const int k = (int)(tj & 1);
+  const int r = (int)(g.phys(tb) * BR), c = (int)(g.phys(tj) * BR);
+  mbar_expect_tx(&hs.mbar[unit][k], (uint32_t)(BR * BR * 8));
+  tma_2d(hs.st[unit][k], map, r, c, &hs.mbar[unit][k]);
+  tma_2d(hs.st[unit][k] + BR * HT, map, r, c + HT, &hs.mbar[unit][k]);
+}
+
 template <bool FWD, int NRT>
-__device__ void helper_unit(const Args& a, const Geo<FWD>& g, int64_t tb, int tid, int unit, double* ys) {
+__device__ void helper_unit(const Args& a, const CUtensorMap* map, const Geo<FWD>& g, HelperSmem& hs, int64_t tb,
+                            int tid, int unit, uint32_t (&uses)[2]) {
   const int64_t ntiles = tb - HL + 1;
   if (ntiles <= 0) return;                      // blocks the chain absorbs entirely: nothing to do
   const int64_t IB = g.phys(tb);
   const int64_t row = IB * BR + tid;
   const bool rv = row < a.n;
   const int nr = a.nr;
+  double* ys = hs.ys[unit];
+  if (tid == 0) {
+    helper_issue<FWD>(map, g, hs, unit, tb, 0);
+    if (ntiles > 1) helper_issue<FWD>(map, g, hs, unit, tb, 1);
+  }
   double acc[NRT];
 #pragma unroll
   for (int c = 0; c < NRT; c++) acc[c] = (rv && c < nr) ? a.B[row + (int64_t)c * a.ldb] : 0.0;
   for (int64_t tj = 0; tj < ntiles; tj++) {
     const int64_t JB = g.phys(tj);
     const int nvj = g.nv(tj);
-    double l[BR];
-    const double* src = a.LU + (rv ? row : 0) + JB * BR * a.lda;
-#pragma unroll
-    for (int k = 0; k < BR; k++) l[k] = (rv && k < nvj) ? __ldg(src + (int64_t)k * a.lda) : 0.0;
-    if (tid < nr) wait_gflag(a.yflag + (int64_t)tid * g.NB + tj, a.epoch, 100);
+    const int k2 = (int)(tj & 1);
+    if (tid < nr) wait_gflag(a.yflag + (int64_t)tid * g.NB + tj, a.epoch, 64);
+#ifdef EBV_CHAIN_TRACE
+    if (tid == 0 && tj + 1 == ntiles && FWD == (EBV_CHAIN_TRACE_FWD != 0) && tb < 4096) g_ct[tb][12] = dev::gtimer();
+#endif
     unit_sync(unit);
     for (int idx = tid; idx < BR * nr; idx += 64) {
       const int k = idx % BR, c = idx / BR;
       ys[k * NRT + c] = (k < nvj) ? __ldcg(a.B + JB * BR + k + (int64_t)c * a.ldb) : 0.0;
     }
+    mbar_wait(&hs.mbar[unit][k2], uses[k2] & 1u);
+    uses[k2]++;
     unit_sync(unit);
+    const double* L = hs.st[unit][k2] + tid;     // column k of the tile at L[k * 64]
     if (FWD) {
-#pragma unroll
-      for (int k = 0; k < BR; k++)
+#pragma unroll 16
+      for (int k = 0; k < BR; k++) {
+        const double l = L[k * BR];
 #pragma unroll
         for (int c = 0; c < NRT; c++)
-          if (c < nr) acc[c] = fma(-l[k], ys[k * NRT + c], acc[c]);
+          if (c < nr) acc[c] = fma(-l, ys[k * NRT + c], acc[c]);
+      }
     } else {
-#pragma unroll
-      for (int k = BR - 1; k >= 0; k--)
+#pragma unroll 16
+      for (int k = BR - 1; k >= 0; k--) {
+        const double l = L[k * BR];
 #pragma unroll
         for (int c = 0; c < NRT; c++)
-          if (c < nr) acc[c] = fma(-l[k], ys[k * NRT + c], acc[c]);
+          if (c < nr) acc[c] = fma(-l, ys[k * NRT + c], acc[c]);
+      }
     }
-    unit_sync(unit);                           // ys is restaged for the next tile
+    unit_sync(unit);                           // stage and ys free again
+    if (tid == 0 && tj + 2 < ntiles) {
+      fence_proxy_async();
+      helper_issue<FWD>(map, g, hs, unit, tb, tj + 2);
+    }
   }
 #pragma unroll
   for (int c = 0; c < NRT; c++)
@@ -215,97 +321,127 @@ __device__ void helper_unit(const Args& a, const Geo<FWD>& g, int64_t tb, int ti
   if (tid == 0) {
     dev::jitter((unsigned)tb);
     st_release_gpu(a.hflag + tb, a.epoch);
+#ifdef EBV_CHAIN_TRACE
+    if (FWD == (EBV_CHAIN_TRACE_FWD != 0) && tb < 4096) g_ct[tb][13] = dev::gtimer();
+#endif
   }
 }
 
 // ---------------------------------------------------------------------------- chain
-// absorb tiles (t, s) for s in [s0, t) into rows 2l, 2l+1 of block t (v0, v1),
-// in logical order, each term as soon as its value is produced.  The L (U)
-// values stream through a register ring RING columns ahead (the loader warp
-// prefetched the tiles to L2); the term order inside a tile is the
-// processing order j (column k = j forward, 63 - j backward).
+// The tiles a block holder absorbs stream through its two shared-memory
+// half-tile slots (2-D TMA, 64 rows x 32 columns, zero fill past n): the
+// absorb sequence of block t is the half-tiles of tiles s0 .. t-1 in
+// processing order; half-tile h goes to slot h & 1, and slot k's uses are
+// counted so the mbarrier parity is known.
+struct SlotState {
+  uint32_t q;   // quarters consumed by this warp so far: slot q % NSLOT, parity (q / NSLOT) & 1
+};
+
 template <bool FWD>
-__device__ __forceinline__ void absorb_redo(const Args& a, const Geo<FWD>& g, ChainSmem& sm, int64_t s,
-                                            const double* rowp, double& v0, double& v1) {
-  const int nvs = g.nv(s);
-  const int slot = (int)(s % HR);
+__device__ __forceinline__ void issue_quarter(const CUtensorMap* mapq, const Geo<FWD>& g, ChainSmem& sm, int w,
+                                              int64_t t, int64_t s0, int q, uint32_t qabs) {
+  const int64_t sT = s0 + q / 4;
+  const int qq = q & 3;
+  const int cq = FWD ? qq : 3 - qq;
+  const int k = (int)(qabs % NSLOT);
+  mbar_expect_tx(&sm.mbar_s[w][k], (uint32_t)(BR * QT * 8));
+  tma_2d(sm.slot[w][k], mapq, (int)(g.phys(t) * BR), (int)(g.phys(sT) * BR + cq * QT), &sm.mbar_s[w][k]);
+}
+
+template <bool FWD>
+__device__ __noinline__ void redo_tile(const Geo<FWD>& g, ChainSmem& sm, int64_t t, int64_t sT, int lane, double& v0,
+                                       double& v1) {
+  const int64_t r0 = g.phys(t) * BR + 2 * lane;
+  const double* rowp = g.LU + (r0 < g.n ? r0 : 0);
+  const int nvs = g.nv(sT);
+  const int hs = (int)(sT % HR);
   for (int jj = 0; jj < nvs; jj++) {
-    const double2 l = __ldg(reinterpret_cast<const double2*>(rowp + (g.phys(s) * BR + g.kof(s, jj)) * a.lda));
-    const double y = sm.yh[slot][jj];
+    const double2 l = __ldg(reinterpret_cast<const double2*>(rowp + (g.phys(sT) * BR + g.kof(sT, jj)) * g.lda));
+    const double y = sm.yh[hs][jj];
     v0 = fma(-l.x, y, v0);
     v1 = fma(-l.y, y, v1);
   }
 }
 
 template <bool FWD>
-__device__ __forceinline__ void absorb(const Args& a, const Geo<FWD>& g, ChainSmem& sm, int64_t t, int64_t s0,
-                                       int lane, double& v0, double& v1) {
-  if (s0 >= t) return;
-  const int64_t r0 = g.phys(t) * BR + 2 * lane;
-  const double* rowp = a.LU + (r0 < a.n ? r0 : 0);    // n even: rows 2l, 2l+1 valid together
-  const int64_t lda = a.lda;
-  const int64_t dl = FWD ? lda : -lda;                 // next column in processing order
-  // column k(j) of tile s: forward k = j, backward k = 63 - j (full tiles)
-  auto col0 = [&](int64_t s) -> const double* { return rowp + (g.phys(s) * BR + (FWD ? 0 : BR - 1)) * lda; };
-  double2 ring[RING];
-  const double* pn = col0(s0);                         // next column to load into the ring
-  if (g.nv(s0) == BR) {
-#pragma unroll
-    for (int i = 0; i < RING; i++) {
-      ring[i] = __ldg(reinterpret_cast<const double2*>(pn));
-      pn += dl;
+__device__ __forceinline__ void absorb(const CUtensorMap* mapq, const Geo<FWD>& g, ChainSmem& sm, int w, int64_t t,
+                                       int64_t s0, int lane, SlotState& ss, double& v0, double& v1) {
+  const int nq = (int)(4 * (t - s0));                 // quarters to absorb (the first NSLOT already issued)
+  const uint32_t q0abs = ss.q;
+  double ck0 = v0, ck1 = v1;                          // checkpoint at the tile's start (backward redo)
+  bool done = false;                                  // the current tile's step is final
+  for (int q = 0; q < nq; q++) {
+    const int64_t sT = s0 + q / 4;
+    const int qq = q & 3;
+    const uint32_t qa = q0abs + (uint32_t)q;
+    const int k = (int)(qa % NSLOT);
+    const int hs = (int)(sT % HR);
+    const int nvs = g.nv(sT);
+    const double* yh = sm.yh[hs];
+    if (qq == 0) {
+      ck0 = v0;
+      ck1 = v1;
+      wait_sflag_ge(&sm.prog[hs], (int)(sT + 1));     // the slot holds step sT (sentinels or values)
+      // a step already final: plain loads for the whole tile, no per-value checks
+      done = ld_acq_cta(&sm.fin[hs]) >= (int)(2 * (sT + 1));
     }
-  }
-  for (int64_t s = s0; s < t; s++) {
-    const int slot = (int)(s % HR);
-    const int base = (int)(s * 128);
-    const bool nextfull = s + 1 < t && g.nv(s + 1) == BR;
-    if (g.nv(s) != BR) {
-      // the ragged block (backward: logical block 0): plain loads
-      wait_sflag_ge(&sm.fin[slot], (int)(2 * (s + 1)));
-      absorb_redo<FWD>(a, g, sm, s, rowp, v0, v1);
-      if (nextfull) {
-        pn = col0(s + 1);
+    EBV_CQ(t, q, 0);
+    mbar_wait(&sm.mbar_s[w][k], (qa / NSLOT) & 1u);
+    EBV_CQ(t, q, 1);
+    const double* S = sm.slot[w][k];
+    if (nvs == BR) {
 #pragma unroll
-        for (int i = 0; i < RING; i++) {
-          ring[i] = __ldg(reinterpret_cast<const double2*>(pn));
-          pn += dl;
+      for (int h8 = 0; h8 < QT; h8 += 8) {
+        double y[8];
+        if (done) {
+#pragma unroll
+          for (int i = 0; i < 8; i++) y[i] = yh[qq * QT + h8 + i];
+        } else {
+          wait_y8(yh + qq * QT + h8, y);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+          const int c = FWD ? h8 + i : QT - 1 - h8 - i;  // column inside the quarter
+          const double2 l = *reinterpret_cast<const double2*>(S + c * BR + 2 * lane);
+          v0 = fma(-l.x, y[i], v0);
+          v1 = fma(-l.y, y[i], v1);
         }
       }
-      continue;
-    }
-    const double ck0 = v0, ck1 = v1;   // checkpoint (backward redo)
-    int cur = -1;
-#pragma unroll 1
-    for (int jc = 0; jc < BR; jc += RING) {
-      const bool last = jc + RING == BR;                 // the loads of this chunk go to the next tile
-      if (last && nextfull) pn = col0(s + 1);
-      const bool ld = !last || nextfull;
-#pragma unroll
-      for (int i = 0; i < RING; i++) {
-        const int j = jc + i;
-        const double2 l = ring[i];
-        if (ld) {
-          ring[i] = __ldg(reinterpret_cast<const double2*>(pn));
-          pn += dl;
-        }
-        if ((i & 7) == 0 && cur < base + j + 8) cur = wait_prog(&sm.prog[slot], base + j + 8);
-        const double y = sm.yh[slot][j];
-        v0 = fma(-l.x, y, v0);
-        v1 = fma(-l.y, y, v1);
+    } else {
+      // the ragged block (backward: logical block 0): processing indices j
+      // whose column k(j) lies in this quarter, in ascending j
+      const int c0 = (FWD ? qq : 3 - qq) * QT;
+      for (int j = 0; j < nvs; j++) {
+        const int kc = g.kof(sT, j) - c0;
+        if (kc < 0 || kc >= QT) continue;
+        const double yv = wait_y1(yh + j);
+        const double2 l = *reinterpret_cast<const double2*>(S + kc * BR + 2 * lane);
+        v0 = fma(-l.x, yv, v0);
+        v1 = fma(-l.y, yv, v1);
       }
     }
-    if (!FWD) {
-      // the tile's values must be final (verified) before the next tile; on a
-      // redo of step s, restore and re-apply its corrected values
-      wait_sflag_ge(&sm.fin[slot], (int)(2 * (s + 1)));
-      if (ld_acq_cta(&sm.fin[slot]) & 1) {
-        v0 = ck0;
-        v1 = ck1;
-        absorb_redo<FWD>(a, g, sm, s, rowp, v0, v1);
+    EBV_CQ(t, q, 2);
+    __syncwarp();
+#ifndef EBV_CHAIN_NOFENCE
+    fence_proxy_async();
+#endif
+    if (lane == 0 && q + NSLOT < nq) issue_quarter<FWD>(mapq, g, sm, w, t, s0, q + NSLOT, qa + NSLOT);
+    EBV_CQ(t, q, 3);
+    if (qq == 3) {
+      EBV_CT(t, (int)(2 + (sT - s0)));
+      if (!FWD) {
+        // the tile's values must be final (verified) before the next tile;
+        // on a redo of step sT, restore and re-apply its corrected values
+        wait_sflag_ge(&sm.fin[hs], (int)(2 * (sT + 1)));
+        if (ld_acq_cta(&sm.fin[hs]) & 1) {
+          v0 = ck0;
+          v1 = ck1;
+          redo_tile<FWD>(g, sm, t, sT, lane, v0, v1);
+        }
       }
     }
   }
+  ss.q = q0abs + (uint32_t)nq;
 }
 
 // solve diagonal block t (rows 2l, 2l+1 in v0, v1; all earlier tiles applied)
@@ -314,13 +450,20 @@ __device__ __forceinline__ void solve_diag(const Geo<FWD>& g, ChainSmem& sm, int
                                            double& v1) {
   const int buf = (int)(t & 1);
   if (t >= HR) wait_sflag_ge(&sm.pdone, (int)(t - HR + 1));   // slot t % HR published (free)
-  mbar_wait(&sm.mbar[buf], (uint32_t)((t >> 1) & 1));
+  EBV_CT(t, 7);
+  mbar_wait(&sm.mbar_d[buf], (uint32_t)((t >> 1) & 1));
+  EBV_CT(t, 8);
   const double* D = sm.diag[buf];
   const int slot = (int)(t % HR);
   const int nvs = g.nv(t);
   const int np = nvs / 2;
-  int* prog = &sm.prog[slot];
   double* yh = sm.yh[slot];
+  {
+    const double sent = __longlong_as_double(kSent);
+    *reinterpret_cast<double2*>(yh + 2 * lane) = make_double2(sent, sent);
+    __syncwarp();
+    if (lane == 0) st_rel_cta(&sm.prog[slot], (int)(t + 1));   // slot of step t started
+  }
   if (FWD) {
 #pragma unroll 4
     for (int p = 0; p < np; p++) {
@@ -329,11 +472,7 @@ __device__ __forceinline__ void solve_diag(const Geo<FWD>& g, ChainSmem& sm, int
       const double t1 = fma(-c0.y, v0, v1);             // owner lane: y_{2p+1} from its own y_{2p}
       const double y0 = __shfl_sync(0xffffffffu, v0, p);
       const double y1 = __shfl_sync(0xffffffffu, t1, p);
-      if (lane == p) {
-        yh[2 * p] = v0;
-        yh[2 * p + 1] = t1;
-        st_rel_cta(prog, (int)(t * 128) + 2 * p + 2);
-      }
+      if (lane == p) *reinterpret_cast<double2*>(yh + 2 * p) = make_double2(v0, t1);
       const double n0 = fma(-c1.x, y1, fma(-c0.x, y0, v0));
       const double n1 = fma(-c1.y, y1, fma(-c0.y, y0, v1));
       v0 = lane > p ? n0 : v0;
@@ -359,9 +498,7 @@ __device__ __forceinline__ void solve_diag(const Geo<FWD>& g, ChainSmem& sm, int
       const int j = 2 * (np - 1 - p);
       if (lane == p) {
         ya = v1; qa = q1; yb = t0; qb = q0;
-        yh[j] = q1;
-        yh[j + 1] = q0;
-        st_rel_cta(prog, (int)(t * 128) + j + 2);
+        *reinterpret_cast<double2*>(yh + j) = make_double2(q1, q0);
       }
       const double n0 = fma(-c0.x, x0, fma(-c1.x, x1, v0));
       const double n1 = fma(-c0.y, x0, fma(-c1.y, x1, v1));
@@ -384,10 +521,7 @@ __device__ __forceinline__ void solve_diag(const Geo<FWD>& g, ChainSmem& sm, int
         const double x1 = __shfl_sync(0xffffffffu, q1, p);
         const double x0 = __shfl_sync(0xffffffffu, q0, p);
         const int j = 2 * (np - 1 - p);
-        if (lane == p) {
-          yh[j] = q1;
-          yh[j + 1] = q0;
-        }
+        if (lane == p) *reinterpret_cast<double2*>(yh + j) = make_double2(q1, q0);
         const double n0 = fma(-c0.x, x0, fma(-c1.x, x1, v0));
         const double n1 = fma(-c0.y, x0, fma(-c1.y, x1, v1));
         v0 = lane < p ? n0 : (lane == p ? q0 : v0);
@@ -395,68 +529,98 @@ __device__ __forceinline__ void solve_diag(const Geo<FWD>& g, ChainSmem& sm, int
       }
       __syncwarp();
     }
+    __syncwarp();
     if (lane == 0) st_rel_cta(&sm.fin[slot], (int)(2 * (t + 1)) + redo);
   }
   __syncwarp();
+  EBV_CT(t, 9);
   if (lane == 0) st_rel_cta(&sm.sdone, (int)(t + 1));   // diag buffer (t & 1) may be refilled
 }
 
 template <bool FWD>
-__device__ void chain_cta(const Args& a, const Geo<FWD>& g, ChainSmem& sm, int col) {
+__device__ __forceinline__ void issue_diag(const CUtensorMap* map, const Geo<FWD>& g, ChainSmem& sm, int64_t t) {
+  const int buf = (int)(t & 1);
+  const int r = (int)(g.phys(t) * BR);
+  mbar_expect_tx(&sm.mbar_d[buf], (uint32_t)(BR * BR * 8));
+  tma_2d(sm.diag[buf], map, r, r, &sm.mbar_d[buf]);
+  tma_2d(sm.diag[buf] + BR * HT, map, r, r + HT, &sm.mbar_d[buf]);
+}
+
+__device__ __forceinline__ void prefetch_tile(const CUtensorMap* map, int64_t row, int64_t col) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];\n" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"((int)row), "r"((int)col)
+               : "memory");
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];\n" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"((int)row), "r"((int)(col + HT))
+               : "memory");
+}
+
+// the L2 prefetch warp measured no gain (the tiles come through TMA in time);
+// EBV_CHAIN_PREFETCH turns it on for experiments
+#ifdef EBV_CHAIN_PREFETCH
+constexpr bool kNoPrefetch = false;
+#else
+constexpr bool kNoPrefetch = true;
+#endif
+
+template <bool FWD>
+__device__ void chain_cta(const Args& a, const CUtensorMap* map, const CUtensorMap* mapq, const Geo<FWD>& g,
+                          ChainSmem& sm, int col) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t NB = g.NB;
   double* Bc = a.B + (int64_t)col * a.ldb;
   int* yflag = a.yflag + (int64_t)col * NB;
   if (warp < 4) {
+    SlotState ss{0u};
     for (int64_t t = warp; t < NB; t += 4) {
+      const int64_t s0 = t - HL + 1 > 0 ? t - HL + 1 : 0;
+      const int nq = (int)(4 * (t - s0));
+      if (lane == 0)
+        for (int q = 0; q < NSLOT && q < nq; q++) issue_quarter<FWD>(mapq, g, sm, warp, t, s0, q, ss.q + q);
       // pick up block t: the helper's partial sums (tiles s <= t - HL)
-      const int64_t IB = g.phys(t);
-      const int64_t r0 = IB * BR + 2 * lane;
+      const int64_t r0 = g.phys(t) * BR + 2 * lane;
+      EBV_CT(t, 0);
       if (t - HL + 1 > 0) {
-        if (lane == 0) wait_gflag(a.hflag + t, a.epoch, 64);
+        if (lane == 0) wait_gflag(a.hflag + t, a.epoch, 32);
         __syncwarp();
       }
+      EBV_CT(t, 1);
       double v0 = 0.0, v1 = 0.0;
       if (r0 < a.n) {
         const double2 b2 = __ldcg(reinterpret_cast<const double2*>(Bc + r0));
         v0 = b2.x;
         v1 = b2.y;
       }
-      const int64_t s0 = t - HL + 1 > 0 ? t - HL + 1 : 0;
-      absorb<FWD>(a, g, sm, t, s0, lane, v0, v1);
+      absorb<FWD>(mapq, g, sm, warp, t, s0, lane, ss, v0, v1);
       solve_diag<FWD>(g, sm, t, lane, v0, v1);
+      // diagonal buffer t & 1 is free: the tile of step t + 2 into it
+      fence_proxy_async();
+      if (lane == 0 && t + 2 < NB) issue_diag<FWD>(map, g, sm, t + 2);
     }
-  } else if (warp == 4) {
-    // loader: diagonal tile of step t into buffer t & 1 once step t - 2 is done;
-    // L2 prefetch of the tiles the block picked up after step t absorbs
+  } else if (warp == 4 && !kNoPrefetch) {
+    // L2 prefetch two steps ahead of the chain: step t+2's live tiles
+    // (t+3..t+5, t+2), the complete tiles the block picked up after it takes
+    // ((t+6, t+1), (t+6, t+2)) and the diagonal tile of step t+3
     for (int64_t t = 0; t < NB; t++) {
-      const int buf = (int)(t & 1);
-      if (t >= 2) wait_sflag_ge(&sm.sdone, (int)(t - 1));
-      const int64_t IB = g.phys(t);
-      const int nvs = g.nv(t);
-      const uint32_t colbytes = (uint32_t)nvs * 8u;
-      if (lane == 0) mbar_expect_tx(&sm.mbar[buf], colbytes * (uint32_t)nvs);
-      __syncwarp();
-      for (int k = lane; k < nvs; k += 32)
-        bulk_g2s(sm.diag[buf] + k * BR, a.LU + IB * BR + (IB * BR + k) * a.lda, colbytes, &sm.mbar[buf]);
-      // block t + 4 is picked up after step t; it absorbs tiles t-1 .. t+3
-      const int64_t tp = t + 4;
-      if (tp < NB) {
-        const int64_t TB = g.phys(tp);
-        const int rows = g.nv(tp);
-        for (int64_t s = (tp - HL + 1 > 0 ? tp - HL + 1 : 0); s < tp; s++) {
-          const int64_t JB = g.phys(s);
-          const int nvj = g.nv(s);
-          for (int k = lane; k < nvj; k += 32)
-            prefetch_l2(a.LU + TB * BR + (JB * BR + k) * a.lda, (uint32_t)rows * 8u);
+      if (t >= 1) wait_sflag_ge_slow(&sm.sdone, (int)t);   // step t-1 done
+      if (lane == 0) {
+        const int64_t sc = t + 2;
+        if (sc < NB) {
+          for (int64_t b = sc + 1; b <= sc + 3 && b < NB; b++) prefetch_tile(map, g.phys(b) * BR, g.phys(sc) * BR);
+          if (sc + 4 < NB) {
+            prefetch_tile(map, g.phys(sc + 4) * BR, g.phys(sc - 1 >= 0 ? sc - 1 : 0) * BR);
+            prefetch_tile(map, g.phys(sc + 4) * BR, g.phys(sc) * BR);
+          }
+          if (sc + 1 < NB) prefetch_tile(map, g.phys(sc + 1) * BR, g.phys(sc + 1) * BR);
         }
       }
+      __syncwarp();
     }
-  } else {
+  } else if (warp == 5) {
     // publisher: every final block to B (global), then its release flag
     for (int64_t t = 0; t < NB; t++) {
       const int slot = (int)(t % HR);
-      wait_sflag_ge(&sm.fin[slot], (int)(2 * (t + 1)));
+      wait_sflag_ge_slow(&sm.fin[slot], (int)(2 * (t + 1)));
       const int64_t IB = g.phys(t);
       const int nvs = g.nv(t);
       for (int j = lane; j < nvs; j += 32) Bc[IB * BR + g.kof(t, j)] = sm.yh[slot][j];
@@ -466,16 +630,20 @@ __device__ void chain_cta(const Args& a, const Geo<FWD>& g, ChainSmem& sm, int c
         st_release_gpu(yflag + t, a.epoch);
         st_rel_cta(&sm.pdone, (int)(t + 1));
       }
+      EBV_CT(t, 11);
       __syncwarp();
     }
   }
 }
 
 template <bool FWD, int NRT>
-__global__ void __launch_bounds__(NT, 1) solve_chain_kernel(Args a) {
+__global__ void __launch_bounds__(NT, 1) solve_chain_kernel(const __grid_constant__ CUtensorMap map,
+                                                             const __grid_constant__ CUtensorMap mapq, Args a) {
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ int s_ticket;
   Geo<FWD> g;
+  g.LU = a.LU;
+  g.lda = a.lda;
   g.n = a.n;
   g.NB = (a.n + BR - 1) / BR;
   g.nvlast = (int)(a.n - (g.NB - 1) * BR);
@@ -490,36 +658,58 @@ __global__ void __launch_bounds__(NT, 1) solve_chain_kernel(Args a) {
     if (tk < a.nr) {
       ChainSmem& sm = *reinterpret_cast<ChainSmem*>(smraw);
       if (threadIdx.x < HR) {
-        sm.prog[threadIdx.x] = -1;
+        sm.prog[threadIdx.x] = 0;
         sm.fin[threadIdx.x] = 0;
       }
       if (threadIdx.x == 0) {
         sm.sdone = 0;
         sm.pdone = 0;
-        mbar_init(&sm.mbar[0], 1);
-        mbar_init(&sm.mbar[1], 1);
+        mbar_init(&sm.mbar_d[0], 1);
+        mbar_init(&sm.mbar_d[1], 1);
+        for (int w = 0; w < 4; w++)
+          for (int k = 0; k < NSLOT; k++) mbar_init(&sm.mbar_s[w][k], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        fence_proxy_async();
       }
       __syncthreads();
-      chain_cta<FWD>(a, g, sm, (int)tk);
+      if (threadIdx.x == 0) {
+        issue_diag<FWD>(&map, g, sm, 0);
+        if (g.NB > 1) issue_diag<FWD>(&map, g, sm, 1);
+      }
+      chain_cta<FWD>(a, &map, &mapq, g, sm, (int)tk);
       __syncthreads();
       if (threadIdx.x == 0) {
-        asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&sm.mbar[0])) : "memory");
-        asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&sm.mbar[1])) : "memory");
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&sm.mbar_d[0])) : "memory");
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&sm.mbar_d[1])) : "memory");
+        for (int w = 0; w < 4; w++)
+          for (int k = 0; k < NSLOT; k++)
+            asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&sm.mbar_s[w][k])) : "memory");
       }
       __syncthreads();
     } else {
       HelperSmem& hs = *reinterpret_cast<HelperSmem*>(smraw);
       const int unit = threadIdx.x / 64, tid = threadIdx.x % 64;
+      if (threadIdx.x < NT / 64) {
+        mbar_init(&hs.mbar[threadIdx.x][0], 1);
+        mbar_init(&hs.mbar[threadIdx.x][1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      }
+      __syncthreads();
+      uint32_t uses[2] = {0u, 0u};
       const int64_t tb = (tk - a.nr) * (NT / 64) + unit;
-      if (tb < nunits) helper_unit<FWD, NRT>(a, g, tb, tid, unit, hs.ys[unit]);
+      if (tb < nunits) helper_unit<FWD, NRT>(a, &map, g, hs, tb, tid, unit, uses);
+      __syncthreads();
+      if (threadIdx.x < NT / 64) {
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&hs.mbar[threadIdx.x][0])) : "memory");
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&hs.mbar[threadIdx.x][1])) : "memory");
+      }
       __syncthreads();
     }
   }
 }
 
 template <bool FWD, int NRT>
-cudaError_t launch_sweep(const Args& a, cudaStream_t s) {
+cudaError_t launch_sweep(const CUtensorMap& map, const CUtensorMap& mapq, const Args& a, cudaStream_t s) {
   const void* fn = reinterpret_cast<const void*>(solve_chain_kernel<FWD, NRT>);
   cudaError_t e = ensure_max_dyn_smem(fn, (int)kSmem);
   if (e != cudaSuccess) return e;
@@ -532,14 +722,16 @@ cudaError_t launch_sweep(const Args& a, cudaStream_t s) {
   const int64_t want = a.nr + (NB + (NT / 64) - 1) / (NT / 64);
   const int64_t cap = (int64_t)sms * per_sm;
   const int64_t grid = want < cap ? want : cap;
-  solve_chain_kernel<FWD, NRT><<<(unsigned)grid, NT, kSmem, s>>>(a);
+  solve_chain_kernel<FWD, NRT><<<(unsigned)grid, NT, kSmem, s>>>(map, mapq, a);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 bool solve_chain_eligible(int64_t n, const double* LU, int64_t lda, int64_t nrhs) {
-  return n >= 2 && n % 2 == 0 && lda % 2 == 0 && (reinterpret_cast<uintptr_t>(LU) & 15) == 0 && nrhs >= 1;
+  alignas(64) unsigned char probe[128];
+  return n >= 2 && n % 2 == 0 && lda % 2 == 0 && (reinterpret_cast<uintptr_t>(LU) & 15) == 0 && nrhs >= 1 &&
+         n <= INT32_MAX && make_tma_map_2d(probe, LU, n, n, lda, BR, HT);
 }
 
 int64_t solve_chain_flags(int64_t n) {   // ints per sweep and column group: yflag[MAXC][NB] + hflag[NB] + ticket
@@ -552,6 +744,9 @@ cudaError_t launch_solve_chain(int64_t n, const double* LU, int64_t lda, double*
   if (n <= 0 || nrhs <= 0) return cudaSuccess;
   const int64_t per = solve_chain_flags(n);
   const int64_t NB = (n + BR - 1) / BR;
+  CUtensorMap map, mapq;
+  if (!make_tma_map_2d(&map, LU, n, n, lda, BR, HT) || !make_tma_map_2d(&mapq, LU, n, n, lda, BR, QT))
+    return cudaErrorNotSupported;
   int64_t idx = 0;
   for (int64_t c0 = 0; c0 < nrhs; c0 += MAXC, idx++) {
     const int nr = (int)((nrhs - c0) < MAXC ? (nrhs - c0) : MAXC);
@@ -570,9 +765,10 @@ cudaError_t launch_solve_chain(int64_t n, const double* LU, int64_t lda, double*
       a.epoch = (int)(((epoch + idx * 2 + pass) % 0x3FFFFFF0) + 1);
       cudaError_t e = cudaMemsetAsync(a.ticket, 0, sizeof(int), s);
       if (e != cudaSuccess) return e;
-      if (nr == 1) e = pass == 0 ? launch_sweep<true, 1>(a, s) : launch_sweep<false, 1>(a, s);
-      else if (nr <= 4) e = pass == 0 ? launch_sweep<true, 4>(a, s) : launch_sweep<false, 4>(a, s);
-      else e = pass == 0 ? launch_sweep<true, MAXC>(a, s) : launch_sweep<false, MAXC>(a, s);
+      if (nr == 1) e = pass == 0 ? launch_sweep<true, 1>(map, mapq, a, s) : launch_sweep<false, 1>(map, mapq, a, s);
+      else if (nr <= 4) e = pass == 0 ? launch_sweep<true, 4>(map, mapq, a, s) : launch_sweep<false, 4>(map, mapq, a, s);
+      else if (nr <= 8) e = pass == 0 ? launch_sweep<true, 8>(map, mapq, a, s) : launch_sweep<false, 8>(map, mapq, a, s);
+      else e = pass == 0 ? launch_sweep<true, MAXC>(map, mapq, a, s) : launch_sweep<false, MAXC>(map, mapq, a, s);
       if (e != cudaSuccess) return e;
     }
   }

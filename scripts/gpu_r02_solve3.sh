@@ -1,0 +1,7 @@
+#!/bin/bash
+cd "$(dirname "$0")/.."
+timeout 120 ./probes/chain_trace 8192 > gpurun_out/chain_trace_8192.txt 2>&1; echo "trace rc=$?"; head -40 gpurun_out/chain_trace_8192.txt
+timeout 600 python -m pytest tests/test_gpu_solve_chain.py -q -x -p no:cacheprovider > gpurun_out/solve_chain_tests.log 2>&1
+echo "chain tests rc=$?"; tail -3 gpurun_out/solve_chain_tests.log
+timeout 300 python scripts/bench_solve.py 1024x1 8192x1 8192x16 32768x1 > gpurun_out/bench_solve_chain.jsonl 2>&1; echo "bench chain rc=$?"
+cat gpurun_out/bench_solve_chain.jsonl
