@@ -703,6 +703,12 @@ ebv_status_t ebv_set_vector_ctas(ebv_context_t c, int64_t ctas) {
   return EBV_SUCCESS;
 }
 
+// EBV_GRAPH_PRIO=0 instantiates the captured schedule without per-node priorities
+static const unsigned long long kGraphFlags = [] {
+  const char* e = getenv("EBV_GRAPH_PRIO");
+  return (e && atoi(e) == 0) ? 0ull : (unsigned long long)cudaGraphInstantiateFlagUseNodePriority;
+}();
+
 ebv_status_t ebv_lu_factor(ebv_context_t c, int64_t n, double* A, int64_t lda, double tau, int64_t* d_info,
                            void* stream) {
   if (!c) return invalid("ebv_lu_factor: NULL ctx");
@@ -755,7 +761,11 @@ ebv_status_t ebv_lu_factor(ebv_context_t c, int64_t n, double* A, int64_t lda, d
     cudaError_t e = cudaStreamEndCapture(s, &graph);
     if (st != EBV_SUCCESS) { if (graph) cudaGraphDestroy(graph); return st; }
     if (e != cudaSuccess) return cuda_fail(e, "end capture");
-    e = cudaGraphInstantiate(&ge->exec, graph, 0);
+    // per-node priorities: the lookahead panels were captured from the
+    // high-priority side stream; without this flag the replay runs every
+    // node at the launching stream's priority and the panel chain queues
+    // behind the update (measured n = 32768: 725 ms replayed vs 710 direct)
+    e = cudaGraphInstantiateWithFlags(&ge->exec, graph, kGraphFlags);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) { ge->exec = nullptr; return cuda_fail(e, "graph instantiate"); }
     ge->launches = c->launches - l0;
