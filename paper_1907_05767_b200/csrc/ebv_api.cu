@@ -272,7 +272,7 @@ cudaError_t lu_blocked(ebv_context* c, int64_t n, double* A, int64_t lda, int64_
     if (e != cudaSuccess) return e;
   }
   auto clip = [](int64_t a, int64_t b) { return a < b ? a : b; };
-  const bool u12la = la && (kU12La >= 0 ? kU12La != 0 : n >= 16384);
+  const bool u12la = la && (kU12La >= 0 ? kU12La != 0 : n >= 8192);
   bool u12_done = false;   // U12 of the current step was solved on the side stream
   {
     const int64_t w0 = step_w(0);

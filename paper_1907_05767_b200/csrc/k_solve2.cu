@@ -363,81 +363,133 @@ __device__ __noinline__ void redo_tile(const Geo<FWD>& g, ChainSmem& sm, int64_t
   }
 }
 
+// Quarter q of block t's absorb sequence lives in slot (qa % NSLOT) once its
+// mbarrier phase (qa / NSLOT) & 1 completes (qa: the warp's running quarter
+// count).  Full tiles are software pipelined: the next quarter's L values
+// are read from shared memory into registers while the current quarter's
+// 16 terms are applied.
+struct AbsorbCtx {
+  double ck0, ck1;   // checkpoint at the current tile's start (backward redo)
+  bool done;         // the current tile's step is final: plain loads, no sentinel checks
+};
+
+template <bool FWD>
+__device__ __forceinline__ void load_quarter(const ChainSmem& sm, int w, uint32_t qa, int lane, double2 (&L)[QT]) {
+  const int k = (int)(qa % NSLOT);
+  mbar_wait(const_cast<unsigned long long*>(&sm.mbar_s[w][k]), (qa / NSLOT) & 1u);
+  const double* S = sm.slot[w][k];
+#pragma unroll
+  for (int i = 0; i < QT; i++) L[i] = *reinterpret_cast<const double2*>(S + (FWD ? i : QT - 1 - i) * BR + 2 * lane);
+}
+
+// the end of quarter q: release its slot (refill with quarter q + NSLOT) and,
+// after a tile's last quarter, the backward redo check
+template <bool FWD>
+__device__ __forceinline__ void quarter_done(const CUtensorMap* mapq, const Geo<FWD>& g, ChainSmem& sm, int w,
+                                             int64_t t, int64_t s0, int q, int nq, uint32_t qa, int lane,
+                                             AbsorbCtx& ac, double& v0, double& v1) {
+  __syncwarp();
+  fence_proxy_async();
+  if (lane == 0 && q + NSLOT < nq) issue_quarter<FWD>(mapq, g, sm, w, t, s0, q + NSLOT, qa + NSLOT);
+  if ((q & 3) == 3) {
+    const int64_t sT = s0 + q / 4;
+    const int hs = (int)(sT % HR);
+    EBV_CT(t, (int)(2 + (sT - s0)));
+    if (!FWD) {
+      // the tile's values must be final (verified) before the next tile;
+      // on a redo of step sT, restore and re-apply its corrected values
+      wait_sflag_ge(&sm.fin[hs], (int)(2 * (sT + 1)));
+      if (ld_acq_cta(&sm.fin[hs]) & 1) {
+        v0 = ac.ck0;
+        v1 = ac.ck1;
+        redo_tile<FWD>(g, sm, t, sT, lane, v0, v1);
+      }
+    }
+  }
+}
+
+template <bool FWD>
+__device__ __forceinline__ void tile_start(const Geo<FWD>& g, ChainSmem& sm, int64_t sT, AbsorbCtx& ac, double v0,
+                                           double v1) {
+  const int hs = (int)(sT % HR);
+  ac.ck0 = v0;
+  ac.ck1 = v1;
+  wait_sflag_ge(&sm.prog[hs], (int)(sT + 1));          // the slot holds step sT (sentinels or values)
+  ac.done = ld_acq_cta(&sm.fin[hs]) >= (int)(2 * (sT + 1));
+}
+
+// apply the 16 terms of quarter q (full tile) held in L
+template <bool FWD>
+__device__ __forceinline__ void apply_quarter(ChainSmem& sm, int64_t s0, int q, const AbsorbCtx& ac,
+                                              const double2 (&L)[QT], double& v0, double& v1) {
+  const int64_t sT = s0 + q / 4;
+  const double* yh = sm.yh[sT % HR] + (q & 3) * QT;
+#pragma unroll
+  for (int h8 = 0; h8 < QT; h8 += 8) {
+    double y[8];
+    if (ac.done) {
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) {
+        const double2 y2 = *reinterpret_cast<const double2*>(yh + h8 + i);
+        y[i] = y2.x;
+        y[i + 1] = y2.y;
+      }
+    } else {
+      wait_y8(yh + h8, y);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      v0 = fma(-L[h8 + i].x, y[i], v0);
+      v1 = fma(-L[h8 + i].y, y[i], v1);
+    }
+  }
+}
+
 template <bool FWD>
 __device__ __forceinline__ void absorb(const CUtensorMap* mapq, const Geo<FWD>& g, ChainSmem& sm, int w, int64_t t,
                                        int64_t s0, int lane, SlotState& ss, double& v0, double& v1) {
   const int nq = (int)(4 * (t - s0));                 // quarters to absorb (the first NSLOT already issued)
   const uint32_t q0abs = ss.q;
-  double ck0 = v0, ck1 = v1;                          // checkpoint at the tile's start (backward redo)
-  bool done = false;                                  // the current tile's step is final
-  for (int q = 0; q < nq; q++) {
-    const int64_t sT = s0 + q / 4;
-    const int qq = q & 3;
-    const uint32_t qa = q0abs + (uint32_t)q;
-    const int k = (int)(qa % NSLOT);
-    const int hs = (int)(sT % HR);
-    const int nvs = g.nv(sT);
-    const double* yh = sm.yh[hs];
-    if (qq == 0) {
-      ck0 = v0;
-      ck1 = v1;
-      wait_sflag_ge(&sm.prog[hs], (int)(sT + 1));     // the slot holds step sT (sentinels or values)
-      // a step already final: plain loads for the whole tile, no per-value checks
-      done = ld_acq_cta(&sm.fin[hs]) >= (int)(2 * (sT + 1));
-    }
-    EBV_CQ(t, q, 0);
-    mbar_wait(&sm.mbar_s[w][k], (qa / NSLOT) & 1u);
-    EBV_CQ(t, q, 1);
-    const double* S = sm.slot[w][k];
-    if (nvs == BR) {
-#pragma unroll
-      for (int h8 = 0; h8 < QT; h8 += 8) {
-        double y[8];
-        if (done) {
-#pragma unroll
-          for (int i = 0; i < 8; i++) y[i] = yh[qq * QT + h8 + i];
-        } else {
-          wait_y8(yh + qq * QT + h8, y);
-        }
-#pragma unroll
-        for (int i = 0; i < 8; i++) {
-          const int c = FWD ? h8 + i : QT - 1 - h8 - i;  // column inside the quarter
-          const double2 l = *reinterpret_cast<const double2*>(S + c * BR + 2 * lane);
-          v0 = fma(-l.x, y[i], v0);
-          v1 = fma(-l.y, y[i], v1);
-        }
-      }
-    } else {
-      // the ragged block (backward: logical block 0): processing indices j
-      // whose column k(j) lies in this quarter, in ascending j
-      const int c0 = (FWD ? qq : 3 - qq) * QT;
+  AbsorbCtx ac{v0, v1, false};
+  int q = 0;
+  // the ragged block (backward: logical block 0, nvs < 64): its quarters
+  // one by one, processing indices j whose column k(j) lies in the quarter
+  if (nq > 0 && g.nv(s0) != BR) {
+    const int nvs = g.nv(s0);
+    const int hs = (int)(s0 % HR);
+    tile_start<FWD>(g, sm, s0, ac, v0, v1);
+    for (; q < 4; q++) {
+      const uint32_t qa = q0abs + (uint32_t)q;
+      const int k = (int)(qa % NSLOT);
+      mbar_wait(&sm.mbar_s[w][k], (qa / NSLOT) & 1u);
+      const double* S = sm.slot[w][k];
+      const int c0 = (FWD ? q : 3 - q) * QT;
       for (int j = 0; j < nvs; j++) {
-        const int kc = g.kof(sT, j) - c0;
+        const int kc = g.kof(s0, j) - c0;
         if (kc < 0 || kc >= QT) continue;
-        const double yv = wait_y1(yh + j);
+        const double yv = wait_y1(sm.yh[hs] + j);
         const double2 l = *reinterpret_cast<const double2*>(S + kc * BR + 2 * lane);
         v0 = fma(-l.x, yv, v0);
         v1 = fma(-l.y, yv, v1);
       }
+      quarter_done<FWD>(mapq, g, sm, w, t, s0, q, nq, qa, lane, ac, v0, v1);
     }
-    EBV_CQ(t, q, 2);
-    __syncwarp();
-#ifndef EBV_CHAIN_NOFENCE
-    fence_proxy_async();
-#endif
-    if (lane == 0 && q + NSLOT < nq) issue_quarter<FWD>(mapq, g, sm, w, t, s0, q + NSLOT, qa + NSLOT);
-    EBV_CQ(t, q, 3);
-    if (qq == 3) {
-      EBV_CT(t, (int)(2 + (sT - s0)));
-      if (!FWD) {
-        // the tile's values must be final (verified) before the next tile;
-        // on a redo of step sT, restore and re-apply its corrected values
-        wait_sflag_ge(&sm.fin[hs], (int)(2 * (sT + 1)));
-        if (ld_acq_cta(&sm.fin[hs]) & 1) {
-          v0 = ck0;
-          v1 = ck1;
-          redo_tile<FWD>(g, sm, t, sT, lane, v0, v1);
-        }
+  }
+  // full tiles, two quarters per iteration: La holds quarter q, Lb quarter q+1
+  if (q < nq) {
+    double2 La[QT], Lb[QT];
+    load_quarter<FWD>(sm, w, q0abs + (uint32_t)q, lane, La);
+    for (; q < nq; q += 2) {
+      if ((q & 3) == 0) tile_start<FWD>(g, sm, s0 + q / 4, ac, v0, v1);
+      if (q + 1 < nq) load_quarter<FWD>(sm, w, q0abs + (uint32_t)(q + 1), lane, Lb);
+      EBV_CQ(t, q, 1);
+      apply_quarter<FWD>(sm, s0, q, ac, La, v0, v1);
+      EBV_CQ(t, q, 2);
+      quarter_done<FWD>(mapq, g, sm, w, t, s0, q, nq, q0abs + (uint32_t)q, lane, ac, v0, v1);
+      if (q + 1 < nq) {
+        if (q + 2 < nq) load_quarter<FWD>(sm, w, q0abs + (uint32_t)(q + 2), lane, La);
+        apply_quarter<FWD>(sm, s0, q + 1, ac, Lb, v0, v1);
+        quarter_done<FWD>(mapq, g, sm, w, t, s0, q + 1, nq, q0abs + (uint32_t)(q + 1), lane, ac, v0, v1);
       }
     }
   }

@@ -77,6 +77,57 @@ __global__ void k(const __grid_constant__ CUtensorMap map, int nq, double* out, 
   out[lane] = v0 + v1;
   if (lane == 0) { cyc[0] = t1 - t0; cyc[1] = tw; cyc[2] = tc; }
 }
+// software-pipelined: the next quarter's L values are loaded (after its
+// mbarrier wait) while the current quarter's 16 terms are applied
+__global__ void k2(const __grid_constant__ CUtensorMap map, int nq, double* out, long long* cyc) {
+  extern __shared__ __align__(128) unsigned char raw[];
+  double* slot = reinterpret_cast<double*>(raw);
+  __shared__ unsigned long long bar[NSLOT];
+  __shared__ __align__(16) double yh[64];
+  const int lane = threadIdx.x;
+  if (lane < NSLOT) mbar_init(&bar[lane], 1);
+  yh[lane] = 1.0 + lane; yh[lane + 32] = 2.0 + lane;
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) for (int q = 0; q < NSLOT; q++) { expect_tx(&bar[q], BR * QT * 8); tma(slot + q * BR * QT, &map, 0, q * QT, &bar[q]); }
+  double v0 = lane, v1 = lane + 0.5;
+  double2 La[QT], Lb[QT];
+  long long t0 = clock64();
+  mwait(&bar[0], 0);
+#pragma unroll
+  for (int i = 0; i < QT; i++) La[i] = *reinterpret_cast<const double2*>(slot + i * BR + 2 * lane);
+  for (int q = 0; q < nq; q += 2) {
+    // quarter q in La; fetch q+1 into Lb
+    {
+      const int k1 = (q + 1) % NSLOT;
+      mwait(&bar[k1], ((q + 1) / NSLOT) & 1);
+#pragma unroll
+      for (int i = 0; i < QT; i++) Lb[i] = *reinterpret_cast<const double2*>(slot + k1 * BR * QT + i * BR + 2 * lane);
+#pragma unroll
+      for (int i = 0; i < QT; i++) { const double y = yh[(q & 3) * QT + i]; v0 = fma(-La[i].x, y, v0); v1 = fma(-La[i].y, y, v1); }
+      __syncwarp();
+      const int k0 = q % NSLOT;
+      if (lane == 0 && q + NSLOT < nq) { expect_tx(&bar[k0], BR * QT * 8); tma(slot + k0 * BR * QT, &map, 0, ((q + NSLOT) * QT) % 8192, &bar[k0]); }
+    }
+    {
+      const int k2n = (q + 2) % NSLOT;
+      if (q + 2 < nq) {
+        mwait(&bar[k2n], ((q + 2) / NSLOT) & 1);
+#pragma unroll
+        for (int i = 0; i < QT; i++) La[i] = *reinterpret_cast<const double2*>(slot + k2n * BR * QT + i * BR + 2 * lane);
+      }
+#pragma unroll
+      for (int i = 0; i < QT; i++) { const double y = yh[((q + 1) & 3) * QT + i]; v0 = fma(-Lb[i].x, y, v0); v1 = fma(-Lb[i].y, y, v1); }
+      __syncwarp();
+      const int k1 = (q + 1) % NSLOT;
+      if (lane == 0 && q + 1 + NSLOT < nq) { expect_tx(&bar[k1], BR * QT * 8); tma(slot + k1 * BR * QT, &map, 0, ((q + 1 + NSLOT) * QT) % 8192, &bar[k1]); }
+    }
+  }
+  long long t1 = clock64();
+  out[lane] = v0 + v1;
+  if (lane == 0) { cyc[0] = t1 - t0; }
+}
+
 int main() {
   const int64_t n = 8192;
   double* A; cudaMalloc(&A, 64 * n * 8 * 2);
@@ -95,5 +146,13 @@ int main() {
       printf("fence=%d rep %d: %s  %.0f cycles/quarter (wait %.0f, consume %.0f)\n", mode, rep, cudaGetErrorString(e),
              (double)c[0] / nq, (double)c[1] / nq, (double)c[2] / nq);
     }
+  cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  for (int rep = 0; rep < 3; rep++) {
+    const int nq = 512;
+    k2<<<1, 32, smem>>>(map, nq, out, cyc);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long c[1]; cudaMemcpy(c, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("pipelined rep %d: %s  %.0f cycles/quarter\n", rep, cudaGetErrorString(e), (double)c[0] / nq);
+  }
   return 0;
 }
