@@ -869,6 +869,9 @@ ebv_status_t ebv_stream_wait_host_copy(ebv_context_t c, void* stream) {
   return EBV_SUCCESS;
 }
 
+static ebv_status_t solve_body(ebv_context_t c, int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb,
+                               int64_t nrhs, void* stream);
+
 ebv_status_t ebv_lu_solve(ebv_context_t c, int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb,
                           int64_t nrhs, void* stream) {
   if (!c) return invalid("ebv_lu_solve: NULL ctx");
@@ -877,6 +880,13 @@ ebv_status_t ebv_lu_solve(ebv_context_t c, int64_t n, const double* LU, int64_t 
   if (n == 0 || nrhs == 0) return EBV_SUCCESS;
   if (!LU || !B) return invalid("ebv_lu_solve: NULL pointer");
   if (c->dist) return invalid("ebv_lu_solve: distributed context (use ebv_lu_solve_dist)");
+  return solve_body(c, n, LU, lda, B, ldb, nrhs, stream);
+}
+
+// the single-GPU solve (also the one-rank case of the distributed solve,
+// whose slab is then the whole matrix in the same layout)
+static ebv_status_t solve_body(ebv_context_t c, int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb,
+                               int64_t nrhs, void* stream) {
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   if (solve_use_trsm(n, nrhs)) {
@@ -1342,5 +1352,18 @@ ebv_status_t ebv_stats_get(ebv_context_t c, int kclass, int64_t* launches, doubl
 }
 
 int64_t ebv_launch_count(ebv_context_t c) { return c ? c->launches : -1; }
+
+}  // extern "C"
+
+namespace ebv {
+namespace sched {
+ebv_status_t solve_full(ebv_context* c, int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb,
+                        int64_t nrhs, cudaStream_t s) {
+  return solve_body(c, n, LU, lda, B, ldb, nrhs, s);
+}
+}  // namespace sched
+}  // namespace ebv
+
+extern "C" {
 
 }  // extern "C"

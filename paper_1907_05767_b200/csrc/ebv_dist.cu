@@ -362,6 +362,11 @@ ebv_status_t dist_solve(ebv_context* c, ebv_dist_state* d, std::vector<View>& vi
   const bool real = d->comm && d->nranks > 1;
   const size_t cnt = (size_t)(ldb * (nrhs - 1) + n);
   if (n <= 0 || nrhs <= 0) return EBV_SUCCESS;
+  if (d->nranks == 1 && views.size() == 1) {
+    // one rank: its slab is the whole matrix (blocks in ascending order),
+    // so the ring has no hop — the single-GPU solve, same per-entry order
+    return solve_full(c, n, views[0].A, views[0].lda, B, ldb, nrhs, s);
+  }
   auto find = [&](int64_t J) -> View* {
     for (auto& v : views)
       if (v.plan.rank == p0.owner(J)) return &v;

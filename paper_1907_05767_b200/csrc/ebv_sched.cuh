@@ -121,6 +121,9 @@ cudaError_t lu_left(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* 
 cudaError_t lu_blocked_stream(ebv_context* c, int64_t n, double* A, int64_t lda, int64_t* info, cudaStream_t s,
                               const double* hA, int64_t ldh);
 void dist_release(ebv_context* c);   // ebv_dist.cu
+// the single-GPU solve (chain / wavefront / TRSM by shape), ebv_api.cu
+ebv_status_t solve_full(ebv_context* c, int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb,
+                        int64_t nrhs, cudaStream_t s);
 
 }  // namespace sched
 }  // namespace ebv
