@@ -611,8 +611,10 @@ __device__ __forceinline__ void prefetch_tile(const CUtensorMap* map, int64_t ro
 // EBV_CHAIN_PREFETCH turns it on for experiments
 #ifdef EBV_CHAIN_PREFETCH
 constexpr bool kNoPrefetch = false;
+constexpr int kPF = EBV_CHAIN_PREFETCH;
 #else
 constexpr bool kNoPrefetch = true;
+constexpr int kPF = 3;
 #endif
 
 template <bool FWD>
@@ -650,21 +652,15 @@ __device__ void chain_cta(const Args& a, const CUtensorMap* map, const CUtensorM
       if (lane == 0 && t + 2 < NB) issue_diag<FWD>(map, g, sm, t + 2);
     }
   } else if (warp == 4 && !kNoPrefetch) {
-    // L2 prefetch two steps ahead of the chain: step t+2's live tiles
-    // (t+3..t+5, t+2), the complete tiles the block picked up after it takes
-    // ((t+6, t+1), (t+6, t+2)) and the diagonal tile of step t+3
+    // (experiment, off by default: measured no gain) L2 prefetch of the
+    // tiles the absorbers take PF steps from now: (s+d, s), d = 1 .. HL-1,
+    // of column block s = t + PF, and the diagonal tile of step s
     for (int64_t t = 0; t < NB; t++) {
       if (t >= 1) wait_sflag_ge_slow(&sm.sdone, (int)t);   // step t-1 done
-      if (lane == 0) {
-        const int64_t sc = t + 2;
-        if (sc < NB) {
-          for (int64_t b = sc + 1; b <= sc + 3 && b < NB; b++) prefetch_tile(map, g.phys(b) * BR, g.phys(sc) * BR);
-          if (sc + 4 < NB) {
-            prefetch_tile(map, g.phys(sc + 4) * BR, g.phys(sc - 1 >= 0 ? sc - 1 : 0) * BR);
-            prefetch_tile(map, g.phys(sc + 4) * BR, g.phys(sc) * BR);
-          }
-          if (sc + 1 < NB) prefetch_tile(map, g.phys(sc + 1) * BR, g.phys(sc + 1) * BR);
-        }
+      const int64_t sc = t + kPF;
+      if (lane == 0 && sc < NB) {
+        for (int d = 1; d < HL && sc + d < NB; d++) prefetch_tile(map, g.phys(sc + d) * BR, g.phys(sc) * BR);
+        prefetch_tile(map, g.phys(sc) * BR, g.phys(sc) * BR);
       }
       __syncwarp();
     }
