@@ -43,6 +43,8 @@
 // bulk copies), nrhs <= 16 per launch.
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "ebv_internal.cuh"
 #include "ebv_device.cuh"
 

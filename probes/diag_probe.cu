@@ -53,6 +53,47 @@ __global__ void k(double* out, long long* cyc, int reps) {
   out[lane] = v0 + v1;
   if (lane == 0) *cyc = t1 - t0;
 }
+// four rows per lane (k_solve2.cu solve_diag4), forward
+__global__ void kq(double* out, long long* cyc, int reps) {
+  __shared__ __align__(16) double Dm[BR * BR];
+  __shared__ __align__(16) double yh[64];
+  const int lane = threadIdx.x;
+  for (int i = lane; i < BR * BR; i += 32) Dm[i] = (i % 65 == 0) ? 2.0 : 1e-3 * (i % 13);
+  __syncwarp();
+  double r0 = 1.0 + lane, r1 = 2.0 + lane, r2 = 3.0 + lane, r3 = 4.0 + lane;
+  const double* D = Dm + 4 * (lane & 15);
+  long long t0 = clock64();
+  for (int r = 0; r < reps; r++) {
+#pragma unroll 2
+    for (int p = 0; p < 16; p++) {
+      const double2 c0a = *reinterpret_cast<const double2*>(D + (4 * p) * BR), c0b = *reinterpret_cast<const double2*>(D + (4 * p) * BR + 2);
+      const double2 c1a = *reinterpret_cast<const double2*>(D + (4 * p + 1) * BR), c1b = *reinterpret_cast<const double2*>(D + (4 * p + 1) * BR + 2);
+      const double2 c2a = *reinterpret_cast<const double2*>(D + (4 * p + 2) * BR), c2b = *reinterpret_cast<const double2*>(D + (4 * p + 2) * BR + 2);
+      const double2 c3a = *reinterpret_cast<const double2*>(D + (4 * p + 3) * BR), c3b = *reinterpret_cast<const double2*>(D + (4 * p + 3) * BR + 2);
+      const double t1 = fma(-c0a.y, r0, r1);
+      const double t2 = fma(-c1b.x, t1, fma(-c0b.x, r0, r2));
+      const double t3 = fma(-c2b.y, t2, fma(-c1b.y, t1, fma(-c0b.y, r0, r3)));
+      const double y0 = __shfl_sync(0xffffffffu, r0, p);
+      const double y1 = __shfl_sync(0xffffffffu, t1, p);
+      const double y2 = __shfl_sync(0xffffffffu, t2, p);
+      const double y3 = __shfl_sync(0xffffffffu, t3, p);
+      if (lane == p) { *reinterpret_cast<double2*>(yh + 4 * p) = make_double2(r0, t1); *reinterpret_cast<double2*>(yh + 4 * p + 2) = make_double2(t2, t3); }
+      const double n0 = fma(-c3a.x, y3, fma(-c2a.x, y2, fma(-c1a.x, y1, fma(-c0a.x, y0, r0))));
+      const double n1 = fma(-c3a.y, y3, fma(-c2a.y, y2, fma(-c1a.y, y1, fma(-c0a.y, y0, r1))));
+      const double n2 = fma(-c3b.x, y3, fma(-c2b.x, y2, fma(-c1b.x, y1, fma(-c0b.x, y0, r2))));
+      const double n3 = fma(-c3b.y, y3, fma(-c2b.y, y2, fma(-c1b.y, y1, fma(-c0b.y, y0, r3))));
+      const bool below = lane > p, own = lane == p;
+      r0 = below ? n0 : r0;
+      r1 = below ? n1 : (own ? t1 : r1);
+      r2 = below ? n2 : (own ? t2 : r2);
+      r3 = below ? n3 : (own ? t3 : r3);
+    }
+  }
+  long long t1c = clock64();
+  out[lane] = r0 + r1 + r2 + r3 + yh[lane];
+  if (lane == 0) *cyc = t1c - t0;
+}
+
 int main() {
   double* out; long long* cyc; cudaMalloc(&out, 256); cudaMalloc(&cyc, 8);
   const int reps = 2000;
@@ -65,5 +106,8 @@ int main() {
   run(k<0>, "forward with history stores");
   run(k<1>, "forward no stores");
   run(k<2>, "backward (Markstein) with stores");
+  kq<<<1, 32>>>(out, cyc, reps); cudaDeviceSynchronize();
+  kq<<<1, 32>>>(out, cyc, reps); cudaDeviceSynchronize();
+  { long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost); printf("%-34s %.1f cycles per pair\n", "forward, 4 rows per lane", (double)c / (reps * 32)); }
   return 0;
 }

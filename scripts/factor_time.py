@@ -15,10 +15,12 @@ ap.add_argument("--graphs", type=int, default=1, help="CUDA-graph replay of the 
 ap.add_argument("--stats", type=int, default=0, help="library per-launch statistics on (disables graphs)")
 ap.add_argument("--legacy", action="store_true", help="the legacy default stream instead of a created one")
 ap.add_argument("--nb", type=int, default=0, help="block width (0: size-adaptive)")
+ap.add_argument("--leaf", type=int, default=0, help="leaf width (0: 64)")
 a = ap.parse_args()
 dev = torch.device("cuda:0")
 ctx = ebv.Context(0)
 ctx.set_graphs(bool(a.graphs))
+ctx.set_leaf(a.leaf)
 ctx.set_block(a.nb)
 ctx.stats_enable(bool(a.stats))
 s = torch.cuda.default_stream(dev) if a.legacy else torch.cuda.Stream(dev)
@@ -38,6 +40,6 @@ for n in a.n:
             if r >= 3:
                 ts.append(e0.elapsed_time(e1))
     ts.sort()
-    print(json.dumps({"n": n, "ms_median": ts[len(ts) // 2], "ms_min": ts[0], "u12la": os.environ.get("EBV_U12_LA", "auto"), "graphs": a.graphs, "nb": ctx.block_width(n), "stats": a.stats, "legacy": a.legacy,
+    print(json.dumps({"n": n, "ms_median": ts[len(ts) // 2], "ms_min": ts[0], "u12la": os.environ.get("EBV_U12_LA", "auto"), "graphs": a.graphs, "nb": ctx.block_width(n), "leaf": a.leaf or 64, "stats": a.stats, "legacy": a.legacy,
                       "tflops": 2 / 3 * n ** 3 / (ts[len(ts) // 2] * 1e-3) / 1e12}), flush=True)
     del A, A0
