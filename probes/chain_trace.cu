@@ -14,25 +14,26 @@
 
 int main(int argc, char** argv) {
   const int64_t n = argc > 1 ? atoll(argv[1]) : 8192;
-  const int fwd_only = argc > 2 ? atoi(argv[2]) : 0;
+  const int nrhs = argc > 2 ? atoi(argv[2]) : 1;
+  const int fwd_only = 0;
   std::vector<double> h(n * n);
   for (int64_t j = 0; j < n; j++)
     for (int64_t i = 0; i < n; i++) h[i + j * n] = (i == j) ? 2.0 + (i % 7) : ((i * 31 + j * 17) % 13 - 6) * 1e-4;
   double *LU, *B;
   int* flags;
   cudaMalloc(&LU, n * n * 8);
-  cudaMalloc(&B, n * 8);
+  cudaMalloc(&B, n * 8 * nrhs);
   cudaMalloc(&flags, 2 * ebv::solve_chain_flags(n) * 4);
   cudaMemset(flags, 0, 2 * ebv::solve_chain_flags(n) * 4);
   cudaMemcpy(LU, h.data(), n * n * 8, cudaMemcpyHostToDevice);
-  std::vector<double> b(n, 1.0);
+  std::vector<double> b(n * nrhs, 1.0);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   for (int rep = 0; rep < 3; rep++) {
-    cudaMemcpy(B, b.data(), n * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(B, b.data(), n * 8 * nrhs, cudaMemcpyHostToDevice);
     cudaEventRecord(e0);
-    cudaError_t e = ebv::launch_solve_chain(n, LU, n, B, n, 1, flags, 100 * rep, 0);
+    cudaError_t e = ebv::launch_solve_chain(n, LU, n, B, n, nrhs, flags, 100 * rep, 0);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0;
