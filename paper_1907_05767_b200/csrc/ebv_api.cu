@@ -151,15 +151,19 @@ static int64_t kSolveTrsmRhs = [] {
   const char* e = getenv("EBV_SOLVE_TRSM_RHS");
   return e ? (int64_t)atoll(e) : (int64_t)0;
 }();
-// EBV_SOLVE_CHAIN=0 selects the wavefront kernel (k_solve.cu) for the
-// few-right-hand-side solve instead of the chain-pipelined one (k_solve2.cu);
-// 2 forces the chain kernel wherever it is eligible
+// EBV_SOLVE_CHAIN=0 selects the wavefront kernel (k_solve.cu) instead of the
+// chain-pipelined one (k_solve2.cu) for the non-TRSM solves
 static int kSolveChain = [] {
   const char* e = getenv("EBV_SOLVE_CHAIN");
   return e ? atoi(e) : 1;
 }();
-static bool solve_use_trsm(int64_t n, int64_t nrhs) {
+static bool solve_use_trsm(int64_t n, int64_t nrhs, bool chain) {
   if (kSolveTrsmRhs > 0) return nrhs >= kSolveTrsmRhs;
+  // against the chain kernel (16 columns per launch, ~0.9 ms per group at
+  // n = 8192, ~8.9 ms at n = 32768; TRSM ~12.5 / ~55 ms flat:
+  // profiles/r02_solve_chain_many.jsonl, r02_solve_trsm_many.jsonl)
+  if (chain) return nrhs > 192 || (n > 12288 && nrhs > 96);
+  // against the wavefront kernel (profiles/r01_solve_rhs_sweep.jsonl)
   return nrhs > 128 || (n > 8192 && nrhs > 64) || (n > 16384 && nrhs > 40);
 }
 
@@ -889,7 +893,8 @@ static ebv_status_t solve_body(ebv_context_t c, int64_t n, const double* LU, int
                                int64_t nrhs, void* stream) {
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
-  if (solve_use_trsm(n, nrhs)) {
+  const bool chain = kSolveChain && solve_chain_eligible(n, LU, lda, nrhs);
+  if (solve_use_trsm(n, nrhs, chain)) {
     // many right-hand sides (factor once, solve many — SURVEY §8f f1): the
     // substitutions as recursive TRSMs, L^-1 then U^-1, whose off-diagonal
     // blocks are DMMA updates (k ascending forward, descending backward):
@@ -899,13 +904,11 @@ static ebv_status_t solve_body(ebv_context_t c, int64_t n, const double* LU, int
     if (e != cudaSuccess) return cuda_fail(e, "solve (trsm)");
     return EBV_SUCCESS;
   }
-  // chain kernel: few right-hand sides, or up to 16 on large orders
-  // (profiles/r02_solve_chain.jsonl vs r02_solve_wave.jsonl: n = 8192 with
-  // 8 / 16 columns 2.0 / 2.3 ms vs 1.8 / 2.1 for the wavefront kernel; every
-  // other measured case favours the chain kernel, e.g. n = 32768, 1 RHS:
-  // 3.4 vs 6.6 ms)
-  const bool chain_shape = nrhs <= 4 || (n > 12288 && nrhs <= 16) || kSolveChain > 1;
-  if (kSolveChain && chain_shape && solve_chain_eligible(n, LU, lda, nrhs)) {
+  // chain kernel wherever eligible (even n, even lda, aligned): measured
+  // faster than the wavefront kernel at every order and column count tried
+  // (profiles/r02_solve_chain*.jsonl vs r02_solve_wave.jsonl, e.g. n =
+  // 32768, 1 RHS 3.5 vs 6.6 ms; n = 8192, 16 RHS 0.90 vs 2.1 ms)
+  if (chain) {
     // chain-pipelined solve (k_solve2.cu): one chain CTA per right-hand side
     // walks the diagonal blocks, helper CTAs stream L / U
     ebv_status_t st = ensure_flags(c, 2 * solve_chain_flags(n));

@@ -58,7 +58,11 @@ constexpr int BR = 64;        // rows per block
 constexpr int HL = EBV_CHAIN_HL;         // helpers apply tiles s <= t - HL; the chain the last HL-1
 constexpr int HR = 8;         // y-history ring (steps)
 constexpr int NT = 192;       // threads per CTA (6 warps; helpers: 3 units of 64)
-constexpr int MAXC = 16;      // right-hand sides per launch (helper accumulators: NRT <= MAXC)
+constexpr int MAXC = 16;      // right-hand sides per launch
+#ifndef EBV_CHAIN_CGW
+#define EBV_CHAIN_CGW 4
+#endif
+constexpr int kCGW = EBV_CHAIN_CGW;   // right-hand sides per helper unit (column group)
 constexpr int HT = 32;        // columns per half-tile (TMA box 64 x 32: diagonal tiles, helper tiles)
 constexpr int QT = 16;        // columns per quarter-tile (TMA box 64 x 16: the absorbers' stream)
 constexpr int NSLOT = 4;      // quarter-tile slots per block-holder warp
@@ -229,7 +233,9 @@ struct Args {
   int nr;          // right-hand sides (chain CTAs) in this launch, <= MAXC
   int* ticket;
   int* yflag;      // [nr][NB], logical block order
-  int* hflag;      // [NB]
+  int* hflag;      // [ngroups][NB]: helper partial of (column group, block) stored
+  int cgw;         // right-hand sides per helper column group (<= NRT)
+  int ngroups;     // column groups: helper units are (block, group) pairs
   int epoch;
 };
 
@@ -261,13 +267,19 @@ __device__ __forceinline__ void helper_issue(const CUtensorMap* map, const Geo<F
 
 template <bool FWD, int NRT>
 __device__ void helper_unit(const Args& a, const CUtensorMap* map, const Geo<FWD>& g, HelperSmem& hs, int64_t tb,
-                            int tid, int unit, uint32_t (&uses)[2]) {
+                            int cg, int tid, int unit, uint32_t (&uses)[2]) {
   const int64_t ntiles = tb - HL + 1;
   if (ntiles <= 0) return;                      // blocks the chain absorbs entirely: nothing to do
   const int64_t IB = g.phys(tb);
   const int64_t row = IB * BR + tid;
   const bool rv = row < a.n;
-  const int nr = a.nr;
+  // this unit's right-hand sides: columns c0 .. c0 + nr - 1 of the launch
+  // (NRT == 1: compile-time constants — the runtime form measured 13% slower
+  // on the one-right-hand-side solve, n = 32768: 3.98 vs 3.50 ms)
+  const int c0 = NRT == 1 ? cg : cg * a.cgw;
+  const int nr = NRT == 1 ? 1 : ((a.nr - c0) < a.cgw ? (a.nr - c0) : a.cgw);
+  double* const B = a.B + (int64_t)c0 * a.ldb;
+  const int* const yflag = a.yflag + (int64_t)c0 * g.NB;
   double* ys = hs.ys[unit];
   if (tid == 0) {
     helper_issue<FWD>(map, g, hs, unit, tb, 0);
@@ -275,19 +287,19 @@ __device__ void helper_unit(const Args& a, const CUtensorMap* map, const Geo<FWD
   }
   double acc[NRT];
 #pragma unroll
-  for (int c = 0; c < NRT; c++) acc[c] = (rv && c < nr) ? a.B[row + (int64_t)c * a.ldb] : 0.0;
+  for (int c = 0; c < NRT; c++) acc[c] = (rv && c < nr) ? B[row + (int64_t)c * a.ldb] : 0.0;
   for (int64_t tj = 0; tj < ntiles; tj++) {
     const int64_t JB = g.phys(tj);
     const int nvj = g.nv(tj);
     const int k2 = (int)(tj & 1);
-    if (tid < nr) wait_gflag(a.yflag + (int64_t)tid * g.NB + tj, a.epoch, 64);
+    if (tid < nr) wait_gflag(yflag + (int64_t)tid * g.NB + tj, a.epoch, 64);
 #ifdef EBV_CHAIN_TRACE
     if (tid == 0 && tj + 1 == ntiles && FWD == (EBV_CHAIN_TRACE_FWD != 0) && tb < 4096) g_ct[tb][12] = dev::gtimer();
 #endif
     unit_sync(unit);
     for (int idx = tid; idx < BR * nr; idx += 64) {
       const int k = idx % BR, c = idx / BR;
-      ys[k * NRT + c] = (k < nvj) ? __ldcg(a.B + JB * BR + k + (int64_t)c * a.ldb) : 0.0;
+      ys[k * NRT + c] = (k < nvj) ? __ldcg(B + JB * BR + k + (int64_t)c * a.ldb) : 0.0;
     }
     mbar_wait(&hs.mbar[unit][k2], uses[k2] & 1u);
     uses[k2]++;
@@ -318,11 +330,11 @@ __device__ void helper_unit(const Args& a, const CUtensorMap* map, const Geo<FWD
   }
 #pragma unroll
   for (int c = 0; c < NRT; c++)
-    if (rv && c < nr) a.B[row + (int64_t)c * a.ldb] = acc[c];
+    if (rv && c < nr) B[row + (int64_t)c * a.ldb] = acc[c];
   unit_sync(unit);
   if (tid == 0) {
     dev::jitter((unsigned)tb);
-    st_release_gpu(a.hflag + tb, a.epoch);
+    st_release_gpu(a.hflag + (int64_t)cg * g.NB + tb, a.epoch);
 #ifdef EBV_CHAIN_TRACE
     if (FWD == (EBV_CHAIN_TRACE_FWD != 0) && tb < 4096) g_ct[tb][13] = dev::gtimer();
 #endif
@@ -637,7 +649,7 @@ __device__ void chain_cta(const Args& a, const CUtensorMap* map, const CUtensorM
       const int64_t r0 = g.phys(t) * BR + 2 * lane;
       EBV_CT(t, 0);
       if (t - HL + 1 > 0) {
-        if (lane == 0) wait_gflag(a.hflag + t, a.epoch, 32);
+        if (lane == 0) wait_gflag(a.hflag + (int64_t)(col / a.cgw) * NB + t, a.epoch, 32);
         __syncwarp();
       }
       EBV_CT(t, 1);
@@ -697,7 +709,7 @@ __global__ void __launch_bounds__(NT, 1) solve_chain_kernel(const __grid_constan
   g.n = a.n;
   g.NB = (a.n + BR - 1) / BR;
   g.nvlast = (int)(a.n - (g.NB - 1) * BR);
-  const int64_t nunits = g.NB;
+  const int64_t nunits = g.NB * a.ngroups;      // helper units: (block, column group), blocks ascending
   const int64_t nhelp = (nunits + (NT / 64) - 1) / (NT / 64);
   for (;;) {
     if (threadIdx.x == 0) s_ticket = atomicAdd(a.ticket, 1);
@@ -746,8 +758,8 @@ __global__ void __launch_bounds__(NT, 1) solve_chain_kernel(const __grid_constan
       }
       __syncthreads();
       uint32_t uses[2] = {0u, 0u};
-      const int64_t tb = (tk - a.nr) * (NT / 64) + unit;
-      if (tb < nunits) helper_unit<FWD, NRT>(a, &map, g, hs, tb, tid, unit, uses);
+      const int64_t u = (tk - a.nr) * (NT / 64) + unit;
+      if (u < nunits) helper_unit<FWD, NRT>(a, &map, g, hs, u / a.ngroups, (int)(u % a.ngroups), tid, unit, uses);
       __syncthreads();
       if (threadIdx.x < NT / 64) {
         asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&hs.mbar[threadIdx.x][0])) : "memory");
@@ -769,7 +781,7 @@ cudaError_t launch_sweep(const CUtensorMap& map, const CUtensorMap& mapq, const 
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_chain_kernel<FWD, NRT>, NT, kSmem);
   if (per_sm < 1) per_sm = 1;
   const int64_t NB = (a.n + BR - 1) / BR;
-  const int64_t want = a.nr + (NB + (NT / 64) - 1) / (NT / 64);
+  const int64_t want = a.nr + (NB * a.ngroups + (NT / 64) - 1) / (NT / 64);
   const int64_t cap = (int64_t)sms * per_sm;
   const int64_t grid = want < cap ? want : cap;
   solve_chain_kernel<FWD, NRT><<<(unsigned)grid, NT, kSmem, s>>>(map, mapq, a);
@@ -784,9 +796,9 @@ bool solve_chain_eligible(int64_t n, const double* LU, int64_t lda, int64_t nrhs
          n <= INT32_MAX && make_tma_map_2d(probe, LU, n, n, lda, BR, HT);
 }
 
-int64_t solve_chain_flags(int64_t n) {   // ints per sweep and column group: yflag[MAXC][NB] + hflag[NB] + ticket
+int64_t solve_chain_flags(int64_t n) {   // ints per sweep: yflag[MAXC][NB] + hflag[MAXC][NB] + ticket
   const int64_t NB = (n + BR - 1) / BR;
-  return (int64_t)(MAXC + 1) * NB + 4;
+  return (int64_t)(2 * MAXC) * NB + 4;
 }
 
 cudaError_t launch_solve_chain(int64_t n, const double* LU, int64_t lda, double* B, int64_t ldb, int64_t nrhs,
@@ -809,16 +821,20 @@ cudaError_t launch_solve_chain(int64_t n, const double* LU, int64_t lda, double*
       a.B = B + c0 * ldb;
       a.ldb = ldb;
       a.nr = nr;
-      a.ticket = base + (MAXC + 1) * NB;
+      a.ticket = base + (2 * MAXC) * NB;
       a.yflag = base;
       a.hflag = base + MAXC * NB;
+      // helper column groups of up to kCGW right-hand sides: a (block,
+      // group) unit applies its tiles to kCGW columns only (16 columns in
+      // one unit made the helpers the limit: a 4x longer fma stream per tile)
+      a.cgw = nr < kCGW ? nr : kCGW;
+      a.ngroups = (nr + a.cgw - 1) / a.cgw;
       a.epoch = (int)(((epoch + idx * 2 + pass) % 0x3FFFFFF0) + 1);
       cudaError_t e = cudaMemsetAsync(a.ticket, 0, sizeof(int), s);
       if (e != cudaSuccess) return e;
-      if (nr == 1) e = pass == 0 ? launch_sweep<true, 1>(map, mapq, a, s) : launch_sweep<false, 1>(map, mapq, a, s);
-      else if (nr <= 4) e = pass == 0 ? launch_sweep<true, 4>(map, mapq, a, s) : launch_sweep<false, 4>(map, mapq, a, s);
-      else if (nr <= 8) e = pass == 0 ? launch_sweep<true, 8>(map, mapq, a, s) : launch_sweep<false, 8>(map, mapq, a, s);
-      else e = pass == 0 ? launch_sweep<true, MAXC>(map, mapq, a, s) : launch_sweep<false, MAXC>(map, mapq, a, s);
+      if (a.cgw == 1) e = pass == 0 ? launch_sweep<true, 1>(map, mapq, a, s) : launch_sweep<false, 1>(map, mapq, a, s);
+      else if (a.cgw <= 2) e = pass == 0 ? launch_sweep<true, 2>(map, mapq, a, s) : launch_sweep<false, 2>(map, mapq, a, s);
+      else e = pass == 0 ? launch_sweep<true, 4>(map, mapq, a, s) : launch_sweep<false, 4>(map, mapq, a, s);
       if (e != cudaSuccess) return e;
     }
   }
