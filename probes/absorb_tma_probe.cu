@@ -128,6 +128,49 @@ __global__ void k2(const __grid_constant__ CUtensorMap map, int nq, double* out,
   if (lane == 0) { cyc[0] = t1 - t0; }
 }
 
+__device__ __forceinline__ void pf_tensor(const CUtensorMap* m, int r, int c) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"((uint64_t)m), "r"(r), "r"(c) : "memory");
+}
+// streaming: quarter q at column q*QT of a wide slab (never reused: HBM
+// latency), optional tensor prefetch to L2 `pf` quarters ahead
+__global__ void k3(const __grid_constant__ CUtensorMap map, int nq, int pf, double* out, long long* cyc) {
+  extern __shared__ __align__(128) unsigned char raw[];
+  double* slot = reinterpret_cast<double*>(raw);
+  __shared__ unsigned long long bar[NSLOT];
+  __shared__ __align__(16) double yh[64];
+  const int lane = threadIdx.x;
+  if (lane < NSLOT) mbar_init(&bar[lane], 1);
+  yh[lane] = 1.0 + lane; yh[lane + 32] = 2.0 + lane;
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    if (pf) for (int q = 0; q < pf && q < nq; q++) pf_tensor(&map, 0, q * QT);
+    for (int q = 0; q < NSLOT; q++) { expect_tx(&bar[q], BR * QT * 8); tma(slot + q * BR * QT, &map, 0, q * QT, &bar[q]); }
+  }
+  double v0 = lane, v1 = lane + 0.5;
+  long long t0 = clock64();
+  for (int q = 0; q < nq; q++) {
+    const int k = q % NSLOT;
+    mwait(&bar[k], (q / NSLOT) & 1);
+    const double* S = slot + k * BR * QT;
+#pragma unroll
+    for (int i = 0; i < QT; i++) {
+      const double2 l = *reinterpret_cast<const double2*>(S + i * BR + 2 * lane);
+      const double y = yh[(q & 3) * QT + i];
+      v0 = fma(-l.x, y, v0); v1 = fma(-l.y, y, v1);
+    }
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (lane == 0) {
+      if (pf && q + pf < nq) pf_tensor(&map, 0, (q + pf) * QT);
+      if (q + NSLOT < nq) { expect_tx(&bar[k], BR * QT * 8); tma(slot + k * BR * QT, &map, 0, (q + NSLOT) * QT, &bar[k]); }
+    }
+  }
+  long long t1 = clock64();
+  out[lane] = v0 + v1;
+  if (lane == 0) cyc[0] = t1 - t0;
+}
+
 int main() {
   const int64_t n = 8192;
   double* A; cudaMalloc(&A, 64 * n * 8 * 2);
@@ -153,6 +196,21 @@ int main() {
     cudaError_t e = cudaDeviceSynchronize();
     long long c[1]; cudaMemcpy(c, cyc, 8, cudaMemcpyDeviceToHost);
     printf("pipelined rep %d: %s  %.0f cycles/quarter\n", rep, cudaGetErrorString(e), (double)c[0] / nq);
+  }
+  {
+    const int64_t ncol = 1 << 20;          // 64 x 1M doubles = 512 MB, streamed
+    double* Bg; cudaMalloc(&Bg, 64 * ncol * 8);
+    cudaMemset(Bg, 0, 64 * ncol * 8);
+    alignas(64) CUtensorMap mb;
+    ebv::make_tma_map_2d(&mb, Bg, 64, ncol, 64, BR, QT);
+    cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int pf : {0, 8, 16, 32, 64}) {
+      const int nq = 4096;
+      k3<<<1, 32, smem>>>(mb, nq, pf, out, cyc);
+      cudaError_t e = cudaDeviceSynchronize();
+      long long c[1]; cudaMemcpy(c, cyc, 8, cudaMemcpyDeviceToHost);
+      printf("streaming from HBM, prefetch %2d quarters ahead: %s  %.0f cycles/quarter\n", pf, cudaGetErrorString(e), (double)c[0] / nq);
+    }
   }
   return 0;
 }
