@@ -189,9 +189,13 @@ static int64_t kTailRows = [] {
   return e ? (int64_t)atoll(e) : (int64_t)0;
 }();
 
+// panels up to this many rows take the fused panel-leaf kernel (round 2,
+// with the graph replay keeping the side stream's priority: 4096 measured
+// best — n = 8192 16.76 vs 17.26 ms at 8192, n = 32768 707.5 vs 709.1;
+// profiles/r02_panel_fused_rows.txt)
 static int64_t kPanelLeafFusedRows = [] {
   const char* e = getenv("EBV_PANEL_FUSED_ROWS");
-  return e ? (int64_t)atoll(e) : (int64_t)8192;
+  return e ? (int64_t)atoll(e) : (int64_t)4096;
 }();
 
 cudaError_t panel_rec(ebv_context* c, int64_t M, int64_t w, double* P, int64_t lda, int64_t koff, int64_t* info,
