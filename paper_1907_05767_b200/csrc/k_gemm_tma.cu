@@ -83,7 +83,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 template <class C>
 __global__ void __launch_bounds__(C::THREADS, C::MINB)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t M,
-                    int64_t N, int64_t K, double* __restrict__ Cm, int64_t ldc, int tilesM, int tilesN) {
+                    int64_t N, int64_t K, double* __restrict__ Cm, int64_t ldc, int tilesM, int tilesN, int G) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // 128-byte aligned carve-up
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
@@ -92,7 +92,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_STAGE);
   uint64_t* empty = full + C::STAGES;
 
-  const int G = 8;
+  // tile order: groups of G consecutive M-tiles, M fastest inside a group,
+  // so the CTAs in flight share the L-panel rows of the group and stream
+  // the U panel once per group
   int bid = blockIdx.x;
   int group = bid / (G * tilesN);
   int first_m = group * G;
@@ -369,6 +371,19 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   }
 }
 
+// M-tiles per rasterization group of gemm_tma_kernel (EBV_GEMM_GROUP;
+// round 2: 32 — the U panel is streamed once per group, so 8 re-read it
+// ~4 GB per rank-512 update at n = 32768; factor 708.3 -> 705.8 ms,
+// 64 slower)
+int raster_group() {
+  static const int g = [] {
+    const char* e = getenv("EBV_GEMM_GROUP");
+    const int v = e ? atoi(e) : 32;
+    return v > 0 ? v : 32;
+  }();
+  return g;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -406,7 +421,8 @@ cudaError_t run_tma(int64_t M, int64_t N, int64_t K, const double* A, int64_t ld
   if (!make_map(&ma, A, M, K, lda, C::AST, C::KC) || !make_map(&mb, B, K, N, ldb, C::BSTR, C::BN))
     return cudaErrorNotSupported;
   const int64_t tm = (M + C::BM - 1) / C::BM, tn = (N + C::BN - 1) / C::BN;
-  gemm_tma_kernel<C><<<(unsigned)(tm * tn), C::THREADS, C::SMEM, s>>>(ma, mb, M, N, K, Cm, ldc, (int)tm, (int)tn);
+  gemm_tma_kernel<C><<<(unsigned)(tm * tn), C::THREADS, C::SMEM, s>>>(ma, mb, M, N, K, Cm, ldc, (int)tm, (int)tn,
+                                                                   raster_group());
   return cudaGetLastError();
 }
 

@@ -15,5 +15,5 @@ PY
 )
 echo "longest gemm_tma launch index: $IDX"
 timeout -s KILL 1200 ncu --set full --import-source on --clock-control none -k regex:gemm_tma -s $IDX -c 1 \
-  -o gpurun_out/r01_update_step0 -f python scripts/prof_factor.py --n 32768 --reps 1 > gpurun_out/ncu_full.log 2>&1
+  -o gpurun_out/${REPORT:-r01_update_step0} -f python scripts/prof_factor.py --n 32768 --reps 1 > gpurun_out/ncu_full.log 2>&1
 tail -2 gpurun_out/ncu_full.log
