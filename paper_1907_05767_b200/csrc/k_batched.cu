@@ -269,6 +269,145 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
   }
 }
 
+// ---------------------------------------------------------------- n <= 32, nrhs <= 1
+// The same lane map with the forward substitution L y = b riding in the
+// factor as a 33rd column: at step k, y_i <- fma(-l_ik, y_k, y_i) for the
+// rows below k, y_k being final at step k — per entry the same ascending fma
+// chain as the separate sweep (Eq 1), so bitwise equal; it removes that
+// sweep's 32 shuffle + fma hops (C5: 0.631 -> 0.597 ms).  Measured and not
+// kept: Markstein quotients from a per-step rcp_approx(pivot) with the exact
+// test folded into a flag and a redo with true division (0.75 ms: the extra
+// instructions cost more than the shorter division chain saves).  Guards
+// stay branches: predicated-PTX fma's come out of ptxas as DFMA + 2 FSEL.
+template <bool FULL, bool HASB>
+__global__ void __launch_bounds__(128) batched1_kernel(int n, double* __restrict__ A, int64_t lda, int64_t strideA,
+                                                       int64_t batch, double* __restrict__ B, int64_t strideB,
+                                                       const double* __restrict__ tau_ptr, int tau_default,
+                                                       double tau_value, int32_t* __restrict__ info) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int h = lane >> 4, t = lane & 15;
+  const int64_t sys = 2 * warp + h;
+  const bool act = sys < batch;
+  const int r0 = t, r1 = NP - 1 - t;
+  const bool v0 = act && (FULL || r0 < n), v1 = act && (FULL || r1 < n);
+  double* As = A + (act ? sys : 0) * strideA;
+  double* Bs = HASB ? B + (act ? sys : 0) * strideB : nullptr;
+  const int hb = h << 4;
+
+  double ra[NP], rb[NP], ya = 0.0, yb = 0.0;
+#pragma unroll
+  for (int j = 0; j < NP; j++) {
+    if (FULL) {
+      ra[j] = act ? As[r0 + (int64_t)j * lda] : (r0 == j ? 1.0 : 0.0);
+      rb[j] = act ? As[r1 + (int64_t)j * lda] : (r1 == j ? 1.0 : 0.0);
+    } else {
+      ra[j] = (v0 && j < n) ? As[r0 + (int64_t)j * lda] : (r0 == j ? 1.0 : 0.0);
+      rb[j] = (v1 && j < n) ? As[r1 + (int64_t)j * lda] : (r1 == j ? 1.0 : 0.0);
+    }
+  }
+  if (HASB) {
+    ya = v0 ? Bs[r0] : 0.0;
+    yb = v1 ? Bs[r1] : 0.0;
+  }
+
+  double tv = tau_value;
+  if (tau_default) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < NP; j++) {
+      if (FULL || j < n) { s0 += fabs(ra[j]); s1 += fabs(rb[j]); }
+    }
+    double nm = fmax(v0 ? s0 : 0.0, v1 ? s1 : 0.0);
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) nm = fmax(nm, __shfl_xor_sync(0xffffffffu, nm, o));
+    tv = (double)n * 2.220446049250313e-16 * nm;
+  } else if (tau_ptr) {
+    tv = *tau_ptr;
+  }
+
+  int inf = 0;
+#pragma unroll
+  for (int k = 0; k < NP; k++) {
+    const int src = hb + (k < 16 ? k : NP - 1 - k);
+    const double piv = __shfl_sync(0xffffffffu, k < 16 ? ra[k] : rb[k], src);
+    if ((FULL || k < n) && inf == 0 && fabs(piv) <= tv) inf = k + 1;
+    if (k < 16) {
+      const bool a0 = r0 > k;
+      if (a0) ra[k] = ra[k] / piv;                     // Eq 6-a
+      rb[k] = rb[k] / piv;
+      const double n0 = -ra[k], n1 = -rb[k];
+#pragma unroll
+      for (int j0 = k + 1; j0 < NP; j0 += CH) {
+        double u[CH];
+#pragma unroll
+        for (int q = 0; q < CH; q++)
+          if (j0 + q < NP) u[q] = __shfl_sync(0xffffffffu, ra[j0 + q], src);   // Eq 6-b (row k)
+#pragma unroll
+        for (int q = 0; q < CH; q++)
+          if (j0 + q < NP) rb[j0 + q] = fma(n1, u[q], rb[j0 + q]);            // Eq 6-c
+        if (a0) {
+#pragma unroll
+          for (int q = 0; q < CH; q++)
+            if (j0 + q < NP) ra[j0 + q] = fma(n0, u[q], ra[j0 + q]);
+        }
+      }
+      if (HASB) {   // the forward substitution's step k (Eq 1, L y = b)
+        const double yk = __shfl_sync(0xffffffffu, ya, src);
+        yb = fma(n1, yk, yb);
+        if (a0) ya = fma(n0, yk, ya);
+      }
+    } else {
+      const bool a1 = r1 > k;
+      if (a1) rb[k] = rb[k] / piv;
+      const double n1 = -rb[k];
+#pragma unroll
+      for (int j0 = k + 1; j0 < NP; j0 += CH) {
+        double u[CH];
+#pragma unroll
+        for (int q = 0; q < CH; q++)
+          if (j0 + q < NP) u[q] = __shfl_sync(0xffffffffu, rb[j0 + q], src);
+        if (a1) {
+#pragma unroll
+          for (int q = 0; q < CH; q++)
+            if (j0 + q < NP) rb[j0 + q] = fma(n1, u[q], rb[j0 + q]);
+        }
+      }
+      if (HASB) {
+        const double yk = __shfl_sync(0xffffffffu, yb, src);
+        if (a1) yb = fma(n1, yk, yb);
+      }
+    }
+  }
+  if (act && t == 0 && info) info[sys] = inf;
+
+  if (HASB) {   // backward: U x = y (Eq 1)
+#pragma unroll
+    for (int k = NP - 1; k >= 0; k--) {
+      const int src = hb + (k < 16 ? k : NP - 1 - k);
+      if (k < 16) {
+        if (t == k) ya = ya / ra[k];
+      } else {
+        if (t == NP - 1 - k) yb = yb / rb[k];
+      }
+      const double xk = __shfl_sync(0xffffffffu, k < 16 ? ya : yb, src);
+      if (k < 16) {
+        if (r0 < k) ya = fma(-ra[k], xk, ya);   // rows 31-t >= 16 > k never
+      } else {
+        ya = fma(-ra[k], xk, ya);               // rows t < 16 <= k always
+        if (r1 < k) yb = fma(-rb[k], xk, yb);
+      }
+    }
+    if (v0) Bs[r0] = ya;
+    if (v1) Bs[r1] = yb;
+  }
+#pragma unroll
+  for (int j = 0; j < NP; j++) {
+    if (v0 && (FULL || j < n)) As[r0 + (int64_t)j * lda] = ra[j];
+    if (v1 && (FULL || j < n)) As[r1 + (int64_t)j * lda] = rb[j];
+  }
+}
+
 // ---------------------------------------------------------------- 33 <= n <= 64
 // SURVEY §8f f2 (batched medium systems, CTA per system).  One CTA of 128
 // threads per system: row i is owned by the lane pair (2i, 2i+1), lane j of
@@ -388,6 +527,22 @@ cudaError_t launch_batched(int64_t n, double* A, int64_t lda, int64_t strideA, i
   const int64_t blocks = (warps * 32 + 127) / 128;
   const int so = solve_only ? 1 : 0, td = tau_default ? 1 : 0;
   const unsigned g = (unsigned)blocks;
+  static const bool v1 = [] {   // EBV_BATCHED_V1=0: the separate-sweep kernel for nrhs <= 1
+    const char* e = getenv("EBV_BATCHED_V1");
+    return !(e && atoi(e) == 0);
+  }();
+  if (v1 && !solve_only && nrhs <= 1) {
+    const bool hasb = B && nrhs == 1;
+    if (n == NP && hasb)
+      batched1_kernel<true, true><<<g, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, strideB, tau, td, tau_value, info);
+    else if (n == NP)
+      batched1_kernel<true, false><<<g, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, strideB, tau, td, tau_value, info);
+    else if (hasb)
+      batched1_kernel<false, true><<<g, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, strideB, tau, td, tau_value, info);
+    else
+      batched1_kernel<false, false><<<g, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, strideB, tau, td, tau_value, info);
+    return cudaGetLastError();
+  }
   if (n == NP && nrhs <= 1)
     batched_kernel<true, 1><<<g, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, ldb, strideB, (int)nrhs, tau, td,
                                              tau_value, info, so);
