@@ -274,12 +274,17 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
 // factor as a 33rd column: at step k, y_i <- fma(-l_ik, y_k, y_i) for the
 // rows below k, y_k being final at step k — per entry the same ascending fma
 // chain as the separate sweep (Eq 1), so bitwise equal; it removes that
-// sweep's 32 shuffle + fma hops (C5: 0.631 -> 0.597 ms).  Measured and not
-// kept: Markstein quotients from a per-step rcp_approx(pivot) with the exact
-// test folded into a flag and a redo with true division (0.75 ms: the extra
-// instructions cost more than the shorter division chain saves).  Guards
-// stay branches: predicated-PTX fma's come out of ptxas as DFMA + 2 FSEL.
-template <bool FULL, bool HASB>
+// sweep's 32 shuffle + fma hops (C5: 0.631 -> 0.597 ms).  MKB (n = 32): the
+// backward sweep's quotients are Markstein steps from reciprocals of the
+// lane's two diagonals (captured as the pivots of steps t and 31-t), the
+// exact test deferred to after the sweep, a redo with true division if any
+// fails (0.591 -> 0.581 ms).  Measured and not kept: Markstein quotients in
+// the factor from a per-step rcp_approx(pivot) (0.75 ms) and backward tests
+// done in place (0.69 ms) — warps issue in order, so a test's dependent ops
+// inside the owner's branch stall the chain they were meant to leave.
+// Guards stay branches: predicated-PTX fma's come out of ptxas as DFMA + 2
+// FSEL.
+template <bool FULL, bool HASB, bool MKB = false>
 __global__ void __launch_bounds__(128) batched1_kernel(int n, double* __restrict__ A, int64_t lda, int64_t strideA,
                                                        int64_t batch, double* __restrict__ B, int64_t strideB,
                                                        const double* __restrict__ tau_ptr, int tau_default,
@@ -327,11 +332,16 @@ __global__ void __launch_bounds__(128) batched1_kernel(int n, double* __restrict
   }
 
   int inf = 0;
+  double d0 = 1.0, d1 = 1.0;   // MKB: the lane's own diagonals u_tt, u_(31-t)(31-t) (the pivots of steps t, 31-t)
 #pragma unroll
   for (int k = 0; k < NP; k++) {
     const int src = hb + (k < 16 ? k : NP - 1 - k);
     const double piv = __shfl_sync(0xffffffffu, k < 16 ? ra[k] : rb[k], src);
     if ((FULL || k < n) && inf == 0 && fabs(piv) <= tv) inf = k + 1;
+    if (MKB && HASB) {
+      if (k < 16) d0 = t == k ? piv : d0;
+      else        d1 = t == NP - 1 - k ? piv : d1;
+    }
     if (k < 16) {
       const bool a0 = r0 > k;
       if (a0) ra[k] = ra[k] / piv;                     // Eq 6-a
@@ -382,21 +392,47 @@ __global__ void __launch_bounds__(128) batched1_kernel(int n, double* __restrict
   if (act && t == 0 && info) info[sys] = inf;
 
   if (HASB) {   // backward: U x = y (Eq 1)
+    const double ya_f = ya, yb_f = yb;
+    // MKB: the owner's quotient is a Markstein step from the reciprocal of
+    // its diagonal (formed before the sweep, off the chain); the two
+    // (dividend, quotient) pairs per lane are tested after the sweep and a
+    // warp with an unverified one sweeps again with true division
+    double yo0 = 0.0, qo0 = 0.0, yo1 = 0.0, qo1 = 0.0;
+    const double rd0 = MKB ? rcp_approx(d0) : 0.0, rd1 = MKB ? rcp_approx(d1) : 0.0;
+    auto sweep = [&](auto mk_tag) {
+      constexpr bool MK = decltype(mk_tag)::value;
 #pragma unroll
-    for (int k = NP - 1; k >= 0; k--) {
-      const int src = hb + (k < 16 ? k : NP - 1 - k);
-      if (k < 16) {
-        if (t == k) ya = ya / ra[k];
-      } else {
-        if (t == NP - 1 - k) yb = yb / rb[k];
+      for (int k = NP - 1; k >= 0; k--) {
+        const int src = hb + (k < 16 ? k : NP - 1 - k);
+        if (k < 16) {
+          if (t == k) {
+            if (MK) { yo0 = ya; ya = quot_mk(ya, d0, rd0); qo0 = ya; }
+            else ya = ya / ra[k];
+          }
+        } else {
+          if (t == NP - 1 - k) {
+            if (MK) { yo1 = yb; yb = quot_mk(yb, d1, rd1); qo1 = yb; }
+            else yb = yb / rb[k];
+          }
+        }
+        const double xk = __shfl_sync(0xffffffffu, k < 16 ? ya : yb, src);
+        if (k < 16) {
+          if (r0 < k) ya = fma(-ra[k], xk, ya);   // rows 31-t >= 16 > k never
+        } else {
+          ya = fma(-ra[k], xk, ya);               // rows t < 16 <= k always
+          if (r1 < k) yb = fma(-rb[k], xk, yb);
+        }
       }
-      const double xk = __shfl_sync(0xffffffffu, k < 16 ? ya : yb, src);
-      if (k < 16) {
-        if (r0 < k) ya = fma(-ra[k], xk, ya);   // rows 31-t >= 16 > k never
-      } else {
-        ya = fma(-ra[k], xk, ya);               // rows t < 16 <= k always
-        if (r1 < k) yb = fma(-rb[k], xk, yb);
+    };
+    if (MKB) {
+      sweep(std::true_type{});
+      const bool ok = quot_exact(yo0, d0, qo0) && quot_exact(yo1, d1, qo1);
+      if (__any_sync(0xffffffffu, !ok)) {   // rare: again with true division
+        ya = ya_f; yb = yb_f;
+        sweep(std::false_type{});
       }
+    } else {
+      sweep(std::false_type{});
     }
     if (v0) Bs[r0] = ya;
     if (v1) Bs[r1] = yb;
@@ -534,7 +570,7 @@ cudaError_t launch_batched(int64_t n, double* A, int64_t lda, int64_t strideA, i
   if (v1 && !solve_only && nrhs <= 1) {
     const bool hasb = B && nrhs == 1;
     if (n == NP && hasb)
-      batched1_kernel<true, true><<<g, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, strideB, tau, td, tau_value, info);
+      batched1_kernel<true, true, true><<<g, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, strideB, tau, td, tau_value, info);
     else if (n == NP)
       batched1_kernel<true, false><<<g, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, strideB, tau, td, tau_value, info);
     else if (hasb)
