@@ -278,7 +278,8 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
 // backward sweep's quotients are Markstein steps from reciprocals of the
 // lane's two diagonals (captured as the pivots of steps t and 31-t), the
 // exact test deferred to after the sweep, a redo with true division if any
-// fails (0.591 -> 0.581 ms).  Measured and not kept: Markstein quotients in
+// fails (0.591 -> 0.581 ms).  The first chunk of each step's U_(k) row is
+// shuffled before the divisions (0.581 -> 0.571 ms).  Measured and not kept: Markstein quotients in
 // the factor from a per-step rcp_approx(pivot) (0.75 ms) and backward tests
 // done in place (0.69 ms) — warps issue in order, so a test's dependent ops
 // inside the owner's branch stall the chain they were meant to leave.
@@ -342,17 +343,26 @@ __global__ void __launch_bounds__(128) batched1_kernel(int n, double* __restrict
       if (k < 16) d0 = t == k ? piv : d0;
       else        d1 = t == NP - 1 - k ? piv : d1;
     }
+    // the first chunk of the U_(k) row (and y_k) is shuffled before the
+    // divisions: their slow-path branch ends the basic block, so nothing
+    // after it can be scheduled into the division's latency
+    double u0[CH], yk = 0.0;
+    const int j1 = k + 1;
+#pragma unroll
+    for (int q = 0; q < CH; q++)
+      if (j1 + q < NP) u0[q] = __shfl_sync(0xffffffffu, k < 16 ? ra[j1 + q] : rb[j1 + q], src);   // Eq 6-b (row k)
+    if (HASB) yk = __shfl_sync(0xffffffffu, k < 16 ? ya : yb, src);
     if (k < 16) {
       const bool a0 = r0 > k;
       if (a0) ra[k] = ra[k] / piv;                     // Eq 6-a
       rb[k] = rb[k] / piv;
       const double n0 = -ra[k], n1 = -rb[k];
 #pragma unroll
-      for (int j0 = k + 1; j0 < NP; j0 += CH) {
+      for (int j0 = j1; j0 < NP; j0 += CH) {
         double u[CH];
 #pragma unroll
         for (int q = 0; q < CH; q++)
-          if (j0 + q < NP) u[q] = __shfl_sync(0xffffffffu, ra[j0 + q], src);   // Eq 6-b (row k)
+          if (j0 + q < NP) u[q] = j0 == j1 ? u0[q] : __shfl_sync(0xffffffffu, ra[j0 + q], src);
 #pragma unroll
         for (int q = 0; q < CH; q++)
           if (j0 + q < NP) rb[j0 + q] = fma(n1, u[q], rb[j0 + q]);            // Eq 6-c
@@ -363,7 +373,6 @@ __global__ void __launch_bounds__(128) batched1_kernel(int n, double* __restrict
         }
       }
       if (HASB) {   // the forward substitution's step k (Eq 1, L y = b)
-        const double yk = __shfl_sync(0xffffffffu, ya, src);
         yb = fma(n1, yk, yb);
         if (a0) ya = fma(n0, yk, ya);
       }
@@ -372,21 +381,18 @@ __global__ void __launch_bounds__(128) batched1_kernel(int n, double* __restrict
       if (a1) rb[k] = rb[k] / piv;
       const double n1 = -rb[k];
 #pragma unroll
-      for (int j0 = k + 1; j0 < NP; j0 += CH) {
+      for (int j0 = j1; j0 < NP; j0 += CH) {
         double u[CH];
 #pragma unroll
         for (int q = 0; q < CH; q++)
-          if (j0 + q < NP) u[q] = __shfl_sync(0xffffffffu, rb[j0 + q], src);
+          if (j0 + q < NP) u[q] = j0 == j1 ? u0[q] : __shfl_sync(0xffffffffu, rb[j0 + q], src);
         if (a1) {
 #pragma unroll
           for (int q = 0; q < CH; q++)
             if (j0 + q < NP) rb[j0 + q] = fma(n1, u[q], rb[j0 + q]);
         }
       }
-      if (HASB) {
-        const double yk = __shfl_sync(0xffffffffu, yb, src);
-        if (a1) yb = fma(n1, yk, yb);
-      }
+      if (HASB && a1) yb = fma(n1, yk, yb);
     }
   }
   if (act && t == 0 && info) info[sys] = inf;
