@@ -4,7 +4,8 @@
 // publisher stamps.  Input: a synthetic unit-lower / DD-upper factor (timing
 // only, not a parity check).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo \
-//     -I<nccl include> probes/chain_trace.cu -o probes/chain_trace
+//     -I<nccl include> probes/chain_trace.cu -o probes/chain_trace \
+//     -Lpaper_1907_05767_b200 -lebv -Xlinker -rpath,\$ORIGIN/../paper_1907_05767_b200
 #define EBV_CHAIN_TRACE 1
 #include "../paper_1907_05767_b200/csrc/k_solve2.cu"
 #include "../paper_1907_05767_b200/csrc/k_util.cu"
