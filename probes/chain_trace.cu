@@ -59,10 +59,11 @@ int main(int argc, char** argv) {
   }
   static unsigned long long cq[64][4];
   cudaMemcpyFromSymbol(cq, ebv::g_cq, sizeof(cq));
-  printf("block 20 quarters: before-wait after-wait consumed issued (us from first)\n");
-  for (int q = 0; q < 20; q++)
-    printf("q%2d %8.3f %8.3f %8.3f %8.3f\n", q, (cq[q][0] - cq[0][0]) * 1e-3, (cq[q][1] - cq[0][0]) * 1e-3,
-           (cq[q][2] - cq[0][0]) * 1e-3, (cq[q][3] - cq[0][0]) * 1e-3);
+  printf("block %d quarters (us, relative to q0 start): start  loaded  applied  done | load apply done\n", EBV_CQ_T);
+  for (int q = 0; q < 16; q++) {
+    auto r = [&](int k) { return (cq[q][k] - cq[0][0]) * 1e-3; };
+    printf("q%2d %7.3f %7.3f %7.3f %7.3f | %6.3f %6.3f %6.3f\n", q, r(0), r(1), r(2), r(3), r(1) - r(0), r(2) - r(1), r(3) - r(2));
+  }
   (void)fwd_only;
   return 0;
 }
