@@ -7,7 +7,8 @@
 // per-step barrier removed, timing only) and of trsm_ru give cycles per
 // elimination step.  Results: profiles/r01_probe_leaf.jsonl.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 \
-//        -I paper_1907_05767_b200/csrc probes/leaf_probe.cu -o probes/leaf_probe
+//        -I paper_1907_05767_b200/csrc probes/leaf_probe.cu -o probes/leaf_probe \
+//        -Lpaper_1907_05767_b200 -lebv -Xlinker -rpath,\$ORIGIN/../paper_1907_05767_b200
 #include "k_leaf.cu"
 #include <cstdio>
 #include <vector>
@@ -39,7 +40,28 @@ static void fill(std::vector<double>& h, int64_t M, int64_t ld) {
 // stamps each step.  MODE 0: as the library; 1: multiply instead of divide
 // (timing only); 2: no __syncthreads (timing only, wrong values);
 // 3: divide by the reciprocal published with the row (timing of the
-// reciprocal scheme)
+// reciprocal scheme); 4: the row's owner publishes rcp_approx(u_kk) with
+// the row, the consumers take the Markstein quotient and test it after each
+// block of GD steps (deferred; the redo is not timed)
+__device__ __forceinline__ double rcp_a(double u) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(u));
+  double e = fma(-u, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-u, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double qmk(double y, double u, double r) { const double q0 = y * r; return fma(r, fma(-u, q0, y), q0); }
+__device__ __forceinline__ bool qok(double y, double u, double q) {
+  const double rr = fma(-u, q, y);
+  const long long qb = __double_as_longlong(q);
+  const long long e = qb & 0x7ff0000000000000LL;
+  const bool normal = e > (54LL << 52) && e < (0x7feLL << 52);
+  double lim = fabs(u) * __longlong_as_double(e - (53LL << 52));
+  const bool below = (rr < 0.0) != (u < 0.0);
+  if ((qb & 0x000fffffffffffffLL) == 0 && below == (q > 0.0)) lim *= 0.5;
+  return __double_as_longlong(y) == 0 || (normal && fabs(rr) < lim);
+}
 template <int GD, int MODE>
 __global__ void leaf_steps(double* A, int64_t lda, long long* stamps) {
   constexpr int QD = W / GD;
@@ -47,6 +69,8 @@ __global__ void leaf_steps(double* A, int64_t lda, long long* stamps) {
   __shared__ double rc[2];
   const int tid = threadIdx.x, i = tid / GD, j = tid % GD, lane = tid & 31, base = lane & ~(GD - 1);
   double a[QD];
+  double yck = 0.0, qck = 0.0, uck = 1.0;
+  bool okb = true;
   for (int q = 0; q < QD; q++) a[q] = A[i + (int64_t)(j + GD * q) * lda];
   __syncthreads();
   const long long t0 = clock64();
@@ -60,12 +84,14 @@ __global__ void leaf_steps(double* A, int64_t lda, long long* stamps) {
 #pragma unroll
         for (int q = 0; q < QD; q++) ur[j + GD * q] = a[q];
         if (MODE == 3 && j == o) rc[o & 1] = 1.0 / a[0];
+        if ((MODE == 4 || MODE == 5) && j == o) rc[o & 1] = rcp_a(a[0]);
       }
       if (MODE != 2) __syncthreads();
       const double piv = ur[o];
       if (i > k && j == o) {
         if (MODE == 0) a[0] = a[0] / piv;
         else if (MODE == 3) a[0] = a[0] * rc[o & 1];
+        else if (MODE == 4 || MODE == 5) { yck = a[0]; a[0] = qmk(a[0], piv, rc[o & 1]); qck = a[0]; uck = piv; }
         else a[0] = a[0] * piv;
       }
       const double l = __shfl_sync(0xffffffffu, a[0], base + o);
@@ -75,11 +101,17 @@ __global__ void leaf_steps(double* A, int64_t lda, long long* stamps) {
         for (int q = 1; q < QD; q++) a[q] = fma(-l, ur[j + GD * q], a[q]);
       }
     }
+    if (MODE == 4) okb = okb & qok(yck, uck, qck);
+    if (MODE == 5) {
+      const bool bad = (i > qk * GD + j) && !qok(yck, uck, qck);
+      if (__syncthreads_or(bad)) okb = false;   // CTA-wide vote per block (the redo is not timed)
+    }
     A[i + (int64_t)(j + GD * qk) * lda] = a[0];
     for (int q = 0; q < QD - 1; q++) a[q] = a[q + 1];
     a[QD - 1] = 0.0;
   }
   if (tid == 0) stamps[0] = clock64() - t0;
+  if (!okb) stamps[1] = 1;
 }
 template <int GD, int MODE>
 void leaf_steps_run(double* d, int64_t ld, long long* st, const char* name) {
@@ -271,6 +303,10 @@ int main() {
   leaf_steps_run<4, 1>(d, ld, st, "mul");
   leaf_steps_run<4, 2>(d, ld, st, "nosync");
   leaf_steps_run<4, 3>(d, ld, st, "rcp");
+  leaf_steps_run<4, 4>(d, ld, st, "rcp_markstein_deferred");
+  leaf_steps_run<4, 5>(d, ld, st, "rcp_markstein_vote");
+  leaf_steps_run<8, 4>(d, ld, st, "rcp_markstein_deferred");
+  leaf_steps_run<8, 5>(d, ld, st, "rcp_markstein_vote");
   leaf_steps_run<2, 0>(d, ld, st, "div");
   leaf_steps_run<8, 0>(d, ld, st, "div");
   leaf_steps_run<8, 1>(d, ld, st, "mul");
