@@ -43,7 +43,7 @@ CPU_SAMPLE_M = 4096
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ebv", choices=["ebv", "reference"])
     ap.add_argument("--n", type=int, default=N_DEFAULT)
