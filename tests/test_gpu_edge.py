@@ -109,23 +109,28 @@ def test_vector_path_edge_bitwise(dev, ctx, force, flavour, n):
 
 
 @pytest.mark.parametrize("flavour", FLAVOURS)
-@pytest.mark.parametrize("n,batch,nrhs", [(32, 500, 1), (32, 64, 16), (20, 40, 2), (64, 60, 1), (200, 4, 3)])
+@pytest.mark.parametrize("n,batch,nrhs", [(32, 500, 1), (32, 64, 16), (20, 40, 2), (20, 41, 1), (32, 33, 0),
+                                          (64, 60, 1), (200, 4, 3)])
 def test_batched_edge_bitwise(dev, ctx, force, flavour, n, batch, nrhs):
-    """n = 32 (lane-paired kernel, 1 and 16 RHS — the Markstein backward
-    sweep), n = 20 (padding), n = 64 (CTA per system), n = 200 (the batched
-    blocked schedule)."""
-    db = ebv_inputs.generate_batched(batch, n, seed=n + batch + nrhs, nrhs=nrhs, device=dev)
+    """n = 32 (lane-paired kernels: 1 RHS — forward fused into the factor,
+    Markstein backward with the deferred test — and 16 RHS), n = 20
+    (padding; 1 and 2 RHS), factor only (nrhs = 0), n = 64 (CTA per
+    system), n = 200 (the batched blocked schedule)."""
+    db = ebv_inputs.generate_batched(batch, n, seed=n + batch + nrhs, nrhs=max(nrhs, 1), device=dev)
     A = db["At"].transpose(1, 2)                    # logical (batch, n, n)
     A2, B2 = ebv_inputs.edge_flavour(A, db["B"], flavour, seed=n)
     a_np, b_np = A2.cpu().numpy().copy(), B2.cpu().numpy().copy()   # before the in-place factorization
     At = A2.transpose(1, 2).clone(memory_format=torch.contiguous_format)
-    Bt = B2.transpose(1, 2).clone(memory_format=torch.contiguous_format)
+    Bt = B2.transpose(1, 2).clone(memory_format=torch.contiguous_format) if nrhs else None
     info = ebv.lu_factor_batched(At, Bt, ctx=ctx)
     torch.cuda.synchronize()
-    lu_o, x_o, info_o = oracle.lu_factor_batched(a_np, b_np)
+    lu_o, x_o, info_o = oracle.lu_factor_batched(a_np, b_np if nrhs else None)
     assert bits_eq(info.cpu().numpy(), info_o)
-    lu_g, x_g = At.transpose(1, 2).cpu().numpy(), Bt.transpose(1, 2).cpu().numpy()
+    lu_g = At.transpose(1, 2).cpu().numpy()
     assert bits_eq(lu_g, lu_o), first_diff(lu_g, lu_o)
+    if not nrhs:
+        return
+    x_g = Bt.transpose(1, 2).cpu().numpy()
     assert bits_eq(x_g, x_o), first_diff(x_g, x_o)
     # solve-only on the factors (RG > 1 chains for 16 RHS)
     Bt2 = torch.from_numpy(b_np).to(dev).transpose(1, 2).clone(memory_format=torch.contiguous_format)
