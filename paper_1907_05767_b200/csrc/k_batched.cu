@@ -38,6 +38,11 @@ __device__ __forceinline__ double rcp_approx(double u) {
   return fma(r, e, r);
 }
 __device__ __forceinline__ double quot_mk(double y, double u, double r) { return dev::quot_mk(y, u, r); }
+// the division of the padded kernels (n below the tile: identity rows give
+// zero dividends, dev::div_z); unpadded ones keep the plain division (the
+// extra test cost ~15% at n = 32)
+template <bool PAD>
+__device__ __forceinline__ double divp(double y, double u) { return PAD ? dev::div_z(y, u) : y / u; }
 __device__ __forceinline__ bool quot_exact(double y, double u, double q) { return dev::quot_is_rn(y, u, q); }
 
 // Row updates of rows that may sit above the pivot are guarded by a branch
@@ -101,8 +106,8 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
     if ((FULL || k < n) && inf == 0 && fabs(piv) <= tv) inf = k + 1;
     if (k < 16) {
       const bool a0 = r0 > k;
-      if (a0) ra[k] = ra[k] / piv;                     // Eq 6-a
-      rb[k] = rb[k] / piv;
+      if (a0) ra[k] = divp<!FULL>(ra[k], piv);                     // Eq 6-a
+      rb[k] = divp<!FULL>(rb[k], piv);
       const double n0 = -ra[k], n1 = -rb[k];
 #pragma unroll
       for (int j0 = k + 1; j0 < NP; j0 += CH) {
@@ -121,7 +126,7 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
       }
     } else {
       const bool a1 = r1 > k;
-      if (a1) rb[k] = rb[k] / piv;
+      if (a1) rb[k] = divp<!FULL>(rb[k], piv);
       const double n1 = -rb[k];
 #pragma unroll
       for (int j0 = k + 1; j0 < NP; j0 += CH) {
@@ -176,8 +181,8 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
         const int src = hb + (k < 16 ? k : NP - 1 - k);
 #pragma unroll
         for (int g = 0; g < RG; g++) {
-          if (k < 16) { if (t == k) y0[g] = y0[g] / ra[k]; }
-          else        { if (t == NP - 1 - k) y1[g] = y1[g] / rb[k]; }
+          if (k < 16) { if (t == k) y0[g] = divp<!FULL>(y0[g], ra[k]); }
+          else        { if (t == NP - 1 - k) y1[g] = divp<!FULL>(y1[g], rb[k]); }
         }
 #pragma unroll
         for (int g = 0; g < RG; g++) {
@@ -215,7 +220,7 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
               d0 = ra[k];
 #pragma unroll
               for (int g = 0; g < RG; g++) {
-                const double q = EXACT ? y0[g] / ra[k] : quot_mk(y0[g], ra[k], rk);
+                const double q = EXACT ? divp<!FULL>(y0[g], ra[k]) : quot_mk(y0[g], ra[k], rk);
                 yo0[g] = y0[g]; qo0[g] = q; y0[g] = q;
               }
             }
@@ -225,7 +230,7 @@ __global__ void __launch_bounds__(128) batched_kernel(int n, double* __restrict_
               d1 = rb[k];
 #pragma unroll
               for (int g = 0; g < RG; g++) {
-                const double q = EXACT ? y1[g] / rb[k] : quot_mk(y1[g], rb[k], rk);
+                const double q = EXACT ? divp<!FULL>(y1[g], rb[k]) : quot_mk(y1[g], rb[k], rk);
                 yo1[g] = y1[g]; qo1[g] = q; y1[g] = q;
               }
             }
@@ -354,8 +359,8 @@ __global__ void __launch_bounds__(128) batched1_kernel(int n, double* __restrict
     if (HASB) yk = __shfl_sync(0xffffffffu, k < 16 ? ya : yb, src);
     if (k < 16) {
       const bool a0 = r0 > k;
-      if (a0) ra[k] = ra[k] / piv;                     // Eq 6-a
-      rb[k] = rb[k] / piv;
+      if (a0) ra[k] = divp<!FULL>(ra[k], piv);                     // Eq 6-a
+      rb[k] = divp<!FULL>(rb[k], piv);
       const double n0 = -ra[k], n1 = -rb[k];
 #pragma unroll
       for (int j0 = j1; j0 < NP; j0 += CH) {
@@ -378,7 +383,7 @@ __global__ void __launch_bounds__(128) batched1_kernel(int n, double* __restrict
       }
     } else {
       const bool a1 = r1 > k;
-      if (a1) rb[k] = rb[k] / piv;
+      if (a1) rb[k] = divp<!FULL>(rb[k], piv);
       const double n1 = -rb[k];
 #pragma unroll
       for (int j0 = j1; j0 < NP; j0 += CH) {
@@ -413,12 +418,12 @@ __global__ void __launch_bounds__(128) batched1_kernel(int n, double* __restrict
         if (k < 16) {
           if (t == k) {
             if (MK) { yo0 = ya; ya = quot_mk(ya, d0, rd0); qo0 = ya; }
-            else ya = ya / ra[k];
+            else ya = divp<!FULL>(ya, ra[k]);
           }
         } else {
           if (t == NP - 1 - k) {
             if (MK) { yo1 = yb; yb = quot_mk(yb, d1, rd1); qo1 = yb; }
-            else yb = yb / rb[k];
+            else yb = divp<!FULL>(yb, rb[k]);
           }
         }
         const double xk = __shfl_sync(0xffffffffu, k < 16 ? ya : yb, src);
@@ -462,6 +467,7 @@ __global__ void __launch_bounds__(128) batched1_kernel(int n, double* __restrict
 // rows / columns is exactly neutral.  Per entry the oracle's operations.
 constexpr int N64 = 64, QB = N64 / 2;
 
+template <bool FULL64>
 __global__ void __launch_bounds__(128, 3) batched64_kernel(int n, double* __restrict__ A, int64_t lda, int64_t strideA,
                                                         int64_t batch, double* __restrict__ B, int64_t ldb,
                                                         int64_t strideB, int nrhs, int tau_default, double tau_value,
@@ -510,7 +516,7 @@ __global__ void __launch_bounds__(128, 3) batched64_kernel(int n, double* __rest
       const double piv = ur[k];
       if (k < n && inf == 0 && fabs(piv) <= tv) inf = k + 1;
       const int qk = k >> 1;
-      if (i > k && j == (k & 1)) a[qk] = a[qk] / piv;                       // Eq 6-a
+      if (i > k && j == (k & 1)) a[qk] = divp<!FULL64>(a[qk], piv);                       // Eq 6-a
       const double l = __shfl_sync(0xffffffffu, a[qk], pair | (k & 1));
       if (i > k) {
 #pragma unroll
@@ -536,7 +542,7 @@ __global__ void __launch_bounds__(128, 3) batched64_kernel(int n, double* __rest
 #pragma unroll
       for (int k = N64 - 1; k >= 0; k--) {       // backward: UX = Y
         const double u = __shfl_sync(0xffffffffu, a[k >> 1], pair | (k & 1));
-        if (i == k) y = y / u;
+        if (i == k) y = divp<!FULL64>(y, u);
         if (tid == 2 * k) sval[k & 1] = y;
         __syncthreads();
         const double xk = sval[k & 1];
@@ -553,6 +559,110 @@ __global__ void __launch_bounds__(128, 3) batched64_kernel(int n, double* __rest
   }
 }
 
+
+// 33 <= n <= 64 with at most one right-hand side: the same CTA-per-system
+// scheme with the forward substitution riding in the factor (row k's owner
+// publishes y_k with its U row; rows i > k apply y_i <- fma(-l_ik, y_k, y_i)
+// at step k — the separate sweep's ascending chain, bitwise), which removes
+// the forward sweep's 64 barrier steps; the backward sweep's quotients are
+// Markstein steps from the reciprocal of each row's diagonal (captured as
+// the pivot of its step), tested after the sweep, the sweep redone with true
+// division if any test fails.
+template <bool FULL64>
+__global__ void __launch_bounds__(128, 3) batched64f_kernel(int n, double* __restrict__ A, int64_t lda,
+                                                         int64_t strideA, int64_t batch, double* __restrict__ B,
+                                                         int64_t strideB, int tau_default, double tau_value,
+                                                         int32_t* __restrict__ info) {
+  __shared__ double urow[2][N64 + 2];   // U row k (entries j >= k) and, at [N64], y_k
+  __shared__ double sval[2];
+  __shared__ double snorm[4];
+  const int64_t sys = blockIdx.x;
+  if (sys >= batch) return;
+  const int tid = threadIdx.x, i = tid >> 1, j = tid & 1, lane = tid & 31;
+  const int pair = lane & ~1;
+  double* As = A + sys * strideA;
+  double* Bs = B ? B + sys * strideB : nullptr;
+  const bool rv = i < n;
+  double a[QB];
+#pragma unroll
+  for (int q = 0; q < QB; q++) {
+    const int c = j + 2 * q;
+    a[q] = (rv && c < n) ? As[i + (int64_t)c * lda] : (i == c ? 1.0 : 0.0);
+  }
+  double y = (Bs && rv) ? Bs[i] : 0.0;
+  double tv = tau_value;
+  if (tau_default) {   // n * eps * ||A_s||_inf
+    double rs = 0.0;
+#pragma unroll
+    for (int q = 0; q < QB; q++)
+      if (j + 2 * q < n) rs += fabs(a[q]);
+    rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+    double m = rv ? rs : 0.0;
+#pragma unroll
+    for (int o = 16; o >= 2; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) snorm[tid >> 5] = m;
+    __syncthreads();
+    m = fmax(fmax(snorm[0], snorm[1]), fmax(snorm[2], snorm[3]));
+    tv = (double)n * 2.220446049250313e-16 * m;
+  }
+  int inf = 0;
+  double d = 1.0;                            // this row's diagonal u_ii
+#pragma unroll
+  for (int k = 0; k < N64; k++) {
+    double* ur = urow[k & 1];
+    if (i == k) {
+#pragma unroll
+      for (int q = 0; q < QB; q++)
+        if (j + 2 * q >= k) ur[j + 2 * q] = a[q];
+      if (j == 0) ur[N64] = y;                // y_k is final at step k
+    }
+    __syncthreads();
+    const double piv = ur[k];
+    d = i == k ? piv : d;
+    if (k < n && inf == 0 && fabs(piv) <= tv) inf = k + 1;
+    const int qk = k >> 1;
+    if (i > k && j == (k & 1)) a[qk] = divp<!FULL64>(a[qk], piv);                       // Eq 6-a
+    const double l = __shfl_sync(0xffffffffu, a[qk], pair | (k & 1));
+    if (i > k) {
+#pragma unroll
+      for (int q = qk; q < QB; q++)
+        if (j + 2 * q > k) a[q] = fma(-l, ur[j + 2 * q], a[q]);             // Eq 6-c
+      y = fma(-l, ur[N64], y);                                             // Eq 1, L y = b
+    }
+  }
+  if (tid == 0 && info) info[sys] = inf;
+  if (Bs) {   // backward: U x = y
+    const double yf = y, rd = rcp_approx(d);
+    double yo = 0.0, qo = 0.0;
+    auto sweep = [&](auto mk_tag) {
+      constexpr bool MK = decltype(mk_tag)::value;
+#pragma unroll
+      for (int k = N64 - 1; k >= 0; k--) {
+        const double u = __shfl_sync(0xffffffffu, a[k >> 1], pair | (k & 1));
+        if (i == k) {
+          if (MK) { yo = y; y = quot_mk(y, d, rd); qo = y; }
+          else y = divp<!FULL64>(y, u);
+        }
+        if (tid == 2 * k) sval[k & 1] = y;
+        __syncthreads();
+        const double xk = sval[k & 1];
+        if (i < k) y = fma(-u, xk, y);
+      }
+    };
+    sweep(std::true_type{});
+    if (__syncthreads_or(!quot_exact(yo, d, qo))) {   // rare: the sweep again with true division
+      y = yf;
+      sweep(std::false_type{});
+    }
+    if (rv && j == 0) Bs[i] = y;
+  }
+#pragma unroll
+  for (int q = 0; q < QB; q++) {
+    const int c = j + 2 * q;
+    if (rv && c < n) As[i + (int64_t)c * lda] = a[q];
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_batched(int64_t n, double* A, int64_t lda, int64_t strideA, int64_t batch, double* B,
@@ -560,9 +670,16 @@ cudaError_t launch_batched(int64_t n, double* A, int64_t lda, int64_t strideA, i
                            double tau_value, int32_t* info, cudaStream_t s, bool solve_only) {
   if (batch <= 0 || n <= 0) return cudaSuccess;
   if (n > N64 || nrhs > MAXRHS) return cudaErrorInvalidValue;
+  if (n > NP && nrhs <= 1 && !solve_only) {
+    auto k = n == N64 ? batched64f_kernel<true> : batched64f_kernel<false>;
+    k<<<(unsigned)batch, 128, 0, s>>>((int)n, A, lda, strideA, batch, nrhs == 1 ? B : nullptr, strideB,
+                                     tau_default ? 1 : 0, tau_value, info);
+    return cudaGetLastError();
+  }
   if (n > NP) {
-    batched64_kernel<<<(unsigned)batch, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, ldb, strideB, (int)nrhs,
-                                                     tau_default ? 1 : 0, tau_value, info, solve_only ? 1 : 0);
+    auto k = n == N64 ? batched64_kernel<true> : batched64_kernel<false>;
+    k<<<(unsigned)batch, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, ldb, strideB, (int)nrhs,
+                                     tau_default ? 1 : 0, tau_value, info, solve_only ? 1 : 0);
     return cudaGetLastError();
   }
   const int64_t warps = (batch + 1) / 2;
