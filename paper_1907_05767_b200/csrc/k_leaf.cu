@@ -100,6 +100,20 @@ __global__ void __launch_bounds__(W * GD) leaf_lu_kernel(int w, double* __restri
   }
 }
 
+// Stage a 64 x 64 block in shared memory with all of a thread's loads in
+// flight at once.  (The rolled grid-stride form — load, store, next — waited
+// one L2 round trip per iteration: 16 x ~600 cycles at 256 threads, ~5 us of
+// every TRSM leaf launch, probes/trsm_trace.cu.)  NTHR = blockDim.x.
+template <int NTHR, typename Load, typename Store>
+__device__ __forceinline__ void stage64(Load load, Store store) {
+  constexpr int IT = W * W / NTHR;
+  double v[IT];
+#pragma unroll
+  for (int it = 0; it < IT; it++) v[it] = load((int)threadIdx.x + it * NTHR);
+#pragma unroll
+  for (int it = 0; it < IT; it++) store((int)threadIdx.x + it * NTHR, v[it]);
+}
+
 // ---------------------------------------------------------------- L21 = A21 U11^-1
 // Group per row: step p, the owner lane forms x_p / u_pp, broadcasts it, every
 // lane applies x_c = fma(-x_p, u_pc, x_c) to its entries c > p.  The quotient
@@ -120,6 +134,19 @@ __device__ __forceinline__ bool quot_ok(double y, double u, double q) { return d
 // Each block of 8 steps is checkpointed; if any quotient of the block is
 // unverified the warp redoes that block with true division.
 constexpr int RR = 2;
+#ifdef EBV_LEAF_TRACE
+// probes/trsm_trace.cu: %clock64 stamps of CTA 0, thread 0 (slot 0 entry,
+// 1 U staged, 2 reciprocals, 3 X loaded, 4 + qk end of block qk)
+__device__ long long g_ltrace[16];
+#define EBV_LTR(slot)                                                  \
+  do {                                                                 \
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_ltrace[slot] = clock64(); \
+  } while (0)
+#else
+#define EBV_LTR(slot) \
+  do {                \
+  } while (0)
+#endif
 #ifndef EBV_LEAF_G
 #define EBV_LEAF_G 4
 #endif
@@ -129,15 +156,20 @@ __global__ void __launch_bounds__(256, 2) trsm_ru_kernel(int64_t m, int k, doubl
                                                          const double* __restrict__ U, int64_t ldu) {
   __shared__ __align__(16) double sU[W * S + W];   // sU[p*S + c] = u(p, c), identity padded (+ overrun pad)
   __shared__ double srcp[W];
-  for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
-    const int p = idx % W, c = idx / W;
-    sU[p * S + c] = (p < k && c < k) ? (p <= c ? U[p + (int64_t)c * ldu] : 0.0) : (p == c ? 1.0 : 0.0);
-  }
+  EBV_LTR(0);
+  stage64<256>(
+      [&](int idx) {
+        const int p = idx % W, c = idx / W;
+        return (p < k && c < k) ? (p <= c ? U[p + (int64_t)c * ldu] : 0.0) : (p == c ? 1.0 : 0.0);
+      },
+      [&](int idx, double v) { sU[(idx % W) * S + idx / W] = v; });
   for (int idx = threadIdx.x; idx < W * (S - W) + W; idx += blockDim.x)   // the pad columns of each row + tail
     if (idx < W * (S - W)) sU[(idx / (S - W)) * S + W + idx % (S - W)] = 0.0; else sU[W * S + idx - W * (S - W)] = 0.0;
   __syncthreads();
+  EBV_LTR(1);
   if (threadIdx.x < W) srcp[threadIdx.x] = 1.0 / sU[threadIdx.x * S + threadIdx.x];
   __syncthreads();
+  EBV_LTR(2);
   const int tid = threadIdx.x, j = tid % G, lane = tid & 31, base = lane & ~(G - 1);
   const int64_t i0 = (int64_t)blockIdx.x * (32 * RR) + tid / G;   // rows i0 + 32 r
   double x[RR][Q];
@@ -149,6 +181,7 @@ __global__ void __launch_bounds__(256, 2) trsm_ru_kernel(int64_t m, int k, doubl
       const int64_t i = i0 + 32 * r;
       x[r][q] = (i < m && c < k) ? X[i + (int64_t)c * ldx] : 0.0;
     }
+  EBV_LTR(3);
 #pragma unroll 1
   for (int qk = 0; qk < Q; qk++) {
     double xs[RR][Q];
@@ -211,6 +244,7 @@ __global__ void __launch_bounds__(256, 2) trsm_ru_kernel(int64_t m, int k, doubl
       for (int q = 0; q < Q - 1; q++) x[r][q] = x[r][q + 1];
       x[r][Q - 1] = 0.0;
     }
+    EBV_LTR(4 + qk);
   }
 }
 
@@ -365,10 +399,12 @@ __global__ void __launch_bounds__(256) trsm_llu_kernel(int k, int64_t m, const d
   L += blockIdx.y * bsL;   // batched form: blockIdx.y = system
   X += blockIdx.y * bsX;
   __shared__ __align__(16) double sL[W * S];   // sL[p*S + r] = l(r, p), r > p
-  for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
-    const int r = idx % W, p = idx / W;
-    sL[p * S + r] = (r > p && r < k) ? L[r + (int64_t)p * ldl] : 0.0;
-  }
+  stage64<256>(
+      [&](int idx) {
+        const int r = idx % W, p = idx / W;
+        return (r > p && r < k) ? L[r + (int64_t)p * ldl] : 0.0;
+      },
+      [&](int idx, double v) { sL[(idx / W) * S + idx % W] = v; });
   __syncthreads();
   const int tid = threadIdx.x, j = tid % G, lane = tid & 31, base = lane & ~(G - 1);
   // grid-stride over chunks of 32*CC columns (the grid may be capped so the
@@ -428,10 +464,12 @@ __global__ void __launch_bounds__(128) trsm_luu_kernel(int k, int64_t m, const d
   U += blockIdx.y * bsU;   // batched form: blockIdx.y = system
   X += blockIdx.y * bsX;
   __shared__ __align__(16) double sU[W * S];   // sU[p*S + i] = u(i, p), i <= p (column p of U)
-  for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
-    const int i = idx % W, p = idx / W;
-    sU[p * S + i] = (i < k && p < k) ? (i <= p ? U[i + (int64_t)p * ldu] : 0.0) : (i == p ? 1.0 : 0.0);
-  }
+  stage64<128>(
+      [&](int idx) {
+        const int i = idx % W, p = idx / W;
+        return (i < k && p < k) ? (i <= p ? U[i + (int64_t)p * ldu] : 0.0) : (i == p ? 1.0 : 0.0);
+      },
+      [&](int idx, double v) { sU[(idx / W) * S + idx % W] = v; });
   __syncthreads();
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= m) return;

@@ -1,0 +1,32 @@
+// probes/trsm_trace.cu — %clock64 phases of trsm_ru_kernel (k_leaf.cu
+// compiled with EBV_LEAF_TRACE): U staging, reciprocals, X loads, and each
+// 8-step block of the row-parallel L21 = A21 U11^-1 solve, for one CTA
+// (m = 64) and a full grid (m = 8192).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1907_05767_b200/csrc \
+//     probes/trsm_trace.cu -o probes/trsm_trace -Lpaper_1907_05767_b200 -lebv \
+//     -Xlinker -rpath,\$ORIGIN/../paper_1907_05767_b200
+#define EBV_LEAF_TRACE 1
+#include "k_leaf.cu"
+#include <cstdio>
+#include <vector>
+int main() {
+  const int64_t ld = 8192 + 64;
+  std::vector<double> h(ld * 64);
+  for (int64_t c = 0; c < 64; c++)
+    for (int64_t r = 0; r < ld; r++) h[r + c * ld] = (r == c) ? 65.0 : ((r * 7 + c * 13) % 17 - 8) * 1e-2;
+  double* d;
+  cudaMalloc(&d, ld * 64 * 8);
+  for (int64_t m : {64, 1024, 8192}) {
+    for (int rep = 0; rep < 3; rep++) {
+      cudaMemcpy(d, h.data(), ld * 64 * 8, cudaMemcpyHostToDevice);
+      ebv::launch_trsm_right_upper(m, 64, d + 64, ld, d, ld, 0);
+      cudaDeviceSynchronize();
+    }
+    long long t[16];
+    cudaMemcpyFromSymbol(t, ebv::g_ltrace, sizeof(t));
+    printf("m %5lld: stage U %lld, rcp %lld, X load %lld, blocks:", (long long)m, t[1] - t[0], t[2] - t[1], t[3] - t[2]);
+    for (int b = 0; b < 8; b++) printf(" %lld", t[4 + b] - (b ? t[3 + b] : t[3]));
+    printf("  total %lld cycles\n", t[11] - t[0]);
+  }
+  return 0;
+}
