@@ -114,8 +114,23 @@ __global__ void __launch_bounds__(VT, 1)
   }
   __syncthreads();
   const int ncols = ncols_s;
-  for (int c = 0; c < ncols; c++)
-    for (int i = tid; i < n; i += VT) scol[(size_t)c * n + i] = A[i + (int64_t)cols[c] * lda];
+  {   // owned columns into shared memory, eight loads in flight per thread
+      // (a load -> store loop waits one memory round trip per iteration)
+    const int total = ncols * n;
+    for (int e0 = tid; e0 < total; e0 += 8 * VT) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int e = e0 + u * VT;
+        v[u] = e < total ? A[e % n + (int64_t)cols[e / n] * lda] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int e = e0 + u * VT;
+        if (e < total) scol[e] = v[u];
+      }
+    }
+  }
   __syncthreads();
   const double tv = *tau;
 

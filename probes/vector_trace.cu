@@ -1,6 +1,8 @@
 // Probe: timeline of the vector path (per block J, on the CTA owning J:
 // flag J-1 seen, apply done, diagonal block done, rows below done, released)
 // via %globaltimer.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 probes/vector_trace.cu -o probes/vector_trace \
+//     -Lpaper_1907_05767_b200 -lebv -Xlinker -rpath,\$ORIGIN/../paper_1907_05767_b200
 #define EBV_VECTOR_TRACE 1
 #include "../paper_1907_05767_b200/csrc/k_vector.cu"
 #include <cstdio>
@@ -29,7 +31,7 @@ int main(int argc, char** argv) {
   for (int rep = 1; rep <= 3; rep++) {
     cudaMemcpy(dA, hA.data(), (size_t)n * n * 8, cudaMemcpyHostToDevice);
     cudaEventRecord(e0);
-    cudaError_t e = ebv::launch_vector_lu(n, dA, n, tau, info, flags, lbuf, ctas, 0);
+    cudaError_t e = ebv::launch_vector_lu(n, dA, n, tau, info, flags, lbuf, ctas, rep, 0);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
