@@ -16,6 +16,7 @@
 #include "ebv_internal.cuh"
 #include "ebv_device.cuh"
 #include <cstdlib>
+#include <type_traits>
 
 namespace ebv {
 namespace {
@@ -279,6 +280,7 @@ __global__ void __launch_bounds__(W * GD) panel_leaf_kernel(int64_t M, int w, do
   __shared__ double srcp[W];
   __shared__ int smin, slast;
   const int tid = threadIdx.x, i = tid / GD, j = tid % GD, lane = tid & 31, base = lane & ~(GD - 1);
+  EBV_LTR(0);
   for (int idx = tid; idx < W * RS; idx += W * GD) sUp[idx] = 0.0;
   double a[QD];
 #pragma unroll
@@ -300,6 +302,7 @@ __global__ void __launch_bounds__(W * GD) panel_leaf_kernel(int64_t M, int w, do
   }
   __syncthreads();
   const bool store = slast != 0;
+  EBV_LTR(1);
   // ---- diagonal block (leaf_lu, publishing into the full U copy)
 #pragma unroll 1
   for (int qk = 0; qk < QD; qk++) {
@@ -337,9 +340,11 @@ __global__ void __launch_bounds__(W * GD) panel_leaf_kernel(int64_t M, int w, do
     volatile int64_t* vi = info;
     if (*vi == 0) *vi = koff + smin;
   }
+  EBV_LTR(2);
   if (M <= w) return;
   if (tid < W) srcp[tid] = 1.0 / sUp[tid * RS + (tid % GD) * PS];
   __syncthreads();
+  EBV_LTR(3);
   // ---- rows below (trsm_ru): this CTA's 64 rows, a group of 8 lanes each
   const int64_t r = (int64_t)w + (int64_t)blockIdx.x * W + i;
   const bool rv = r < M;
@@ -349,6 +354,7 @@ __global__ void __launch_bounds__(W * GD) panel_leaf_kernel(int64_t M, int w, do
     const int c = j + GD * q;
     x0[q] = (rv && c < w) ? P[r + (int64_t)c * lda] : 0.0;
   }
+  EBV_LTR(4);
   for (int pass = 0; pass < 2; pass++) {
     const bool exact = pass == 1;
     bool ok = true;
@@ -384,6 +390,213 @@ __global__ void __launch_bounds__(W * GD) panel_leaf_kernel(int64_t M, int w, do
       x[QD - 1] = 0.0;
     }
     if (!__any_sync(0xffffffffu, !ok)) break;
+  }
+  EBV_LTR(5);
+}
+
+// ---------------------------------------------------------------- blocked panel leaf
+// The panel leaf (w <= 64 columns, the diagonal block in every CTA plus the
+// CTA's 64 rows below) as four 16-column sub-panels, each in four phases
+// separated by CTA barriers — instead of one barrier round per column:
+//   A  warp 0 factors the 16 x 16 diagonal sub-block in registers (a row
+//      per lane, the pivot row by shuffles; Eq 6-a..c on the sub-block);
+//   B  threads 0..47: the sub-block rows' entries to the right (U12 of the
+//      sub-panel: a forward substitution with its unit L, one column per
+//      thread); threads 64..: every row below the sub-block — the rest of
+//      the diagonal block and the rows below — forms its 16 multipliers
+//      (x = a U^-1, Markstein quotients from published reciprocals of the
+//      pivots, tested after the row, the phase redone with true division
+//      if any test in the CTA fails);
+//   C  the same threads apply the rank-16 update (Eq 6-c for the sub-panel's
+//      16 steps) to their row's entries right of the sub-panel.
+// Per entry these are exactly the step-by-step operations in ascending k
+// (previous sub-panels' updates first, then this sub-panel's in order, the
+// division last), so the factors are bitwise the oracle's.  Shared memory
+// holds the 64 x 64 block and the 64 rows below (column-major, stride 65).
+constexpr int PB_LD = W + 1;
+constexpr size_t kPanelBlkSmem = (size_t)(2 * W * PB_LD + W) * sizeof(double);
+
+// phase A of panel_blk_kernel: LU of the 16 x 16 diagonal sub-block at
+// (c0, c0) in registers, lane l holding row c0 + l (a separate, fully
+// unrolled function: inside the sub-panel loop the step loop stayed rolled
+// and its row array went to local memory)
+__device__ __forceinline__ void pb_factor16(double* D, double* rc, int c0, int l, int tid, int w, double tv,
+                                            int& binf) {
+  double d[16];
+#pragma unroll
+  for (int t = 0; t < 16; t++) d[t] = D[(c0 + t) * PB_LD + c0 + l];
+#pragma unroll
+  for (int k = 0; k < 16; k++) {
+    const double piv = __shfl_sync(0xffffffffu, d[k], k);
+    if (tid == 0 && c0 + k < w && binf == 0 && fabs(piv) <= tv) binf = c0 + k + 1;
+    double u[16];
+#pragma unroll
+    for (int t = k + 1; t < 16; t++) u[t] = __shfl_sync(0xffffffffu, d[t], k);   // Eq 6-b (before the division)
+    const bool below = l > k;
+    const double lk = dev::div_z(d[k], piv);                                      // Eq 6-a
+    d[k] = below ? lk : d[k];
+#pragma unroll
+    for (int t = k + 1; t < 16; t++) {
+      const double nv = fma(-lk, u[t], d[t]);                                     // Eq 6-c
+      d[t] = below ? nv : d[t];
+    }
+  }
+  if (tid < 16) {
+    double dl = d[0];
+#pragma unroll
+    for (int t = 1; t < 16; t++) dl = t == l ? d[t] : dl;
+#pragma unroll
+    for (int t = 0; t < 16; t++) D[(c0 + t) * PB_LD + c0 + l] = d[t];
+    rc[c0 + l] = dev::rcp_approx(dl);
+  }
+}
+
+__global__ void __launch_bounds__(256) panel_blk_kernel(int64_t M, int w, double* __restrict__ P, int64_t lda,
+                                                        const double* __restrict__ tau, int64_t* info, int64_t koff,
+                                                        int* count, int64_t bsP, int64_t bsInfo, int64_t bsTau) {
+  P += blockIdx.y * bsP;
+  info += blockIdx.y * bsInfo;
+  tau += blockIdx.y * bsTau;
+  count += blockIdx.y;
+  extern __shared__ __align__(16) double pbs[];
+  double* D = pbs;                     // diagonal block: D[c * PB_LD + r]
+  double* R = pbs + W * PB_LD;         // the CTA's rows below: R[c * PB_LD + r]
+  double* rc = R + W * PB_LD;          // rcp_approx(u_cc)
+  __shared__ int slast;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t rb0 = (int64_t)w + (int64_t)blockIdx.x * W;   // first row below of this CTA
+  const int nrb = M > rb0 ? (int)(M - rb0 < W ? M - rb0 : W) : 0;
+  EBV_LTR(0);
+  {   // load (identity-padded diagonal block, zero-padded rows below), all loads in flight
+    const int r = tid & (W - 1), c4 = tid >> 6;
+    double vd[W / 4], vr[W / 4];
+#pragma unroll
+    for (int it = 0; it < W / 4; it++) {
+      const int c = c4 + 4 * it;
+      vd[it] = (r < w && c < w) ? P[r + (int64_t)c * lda] : (r == c ? 1.0 : 0.0);
+      vr[it] = (r < nrb && c < w) ? P[rb0 + r + (int64_t)c * lda] : 0.0;
+    }
+#pragma unroll
+    for (int it = 0; it < W / 4; it++) {
+      const int c = c4 + 4 * it;
+      D[c * PB_LD + r] = vd[it];
+      R[c * PB_LD + r] = vr[it];
+    }
+  }
+  const double tv = *tau;
+  __syncthreads();   // every CTA has read the unfactored diagonal block
+  if (tid == 0) {
+    __threadfence();
+    const int old = atomicAdd(count, 1);
+    slast = old == (int)gridDim.x - 1;
+    if (slast) {
+      *count = 0;
+      __threadfence();
+    }
+  }
+  int binf = 0;
+  EBV_LTR(1);
+#pragma unroll 1
+  for (int c0 = 0; c0 < W; c0 += 16) {
+    // ---- A: the 16 x 16 diagonal sub-block, one row per lane (lanes 16..31 mirror 0..15)
+    if (tid < 32) pb_factor16(D, rc, c0, lane & 15, tid, w, tv, binf);
+    __syncthreads();
+    EBV_LTR(2 + 3 * (c0 / 16));
+    const int ncol = W - c0 - 16;                 // columns right of the sub-panel
+    const int ndr = W - c0 - 16;                  // diagonal-block rows below the sub-block
+    // ---- B1: U12 of the sub-panel rows, one column per thread
+    if (tid < ncol) {
+      const int j = c0 + 16 + tid;
+      double u[16];
+#pragma unroll
+      for (int r = 0; r < 16; r++) u[r] = D[j * PB_LD + c0 + r];
+#pragma unroll
+      for (int p = 0; p < 15; p++)
+#pragma unroll
+        for (int r = p + 1; r < 16; r++) u[r] = fma(-D[(c0 + p) * PB_LD + c0 + r], u[p], u[r]);
+#pragma unroll
+      for (int r = 0; r < 16; r++) D[j * PB_LD + c0 + r] = u[r];
+    }
+    // ---- B2: the multipliers of every row below the sub-block (one row per thread)
+    const int ri = tid - 64;
+    const bool brow = ri >= 0 && ri < ndr + nrb;
+    double* base = nullptr;
+    int row = 0;
+    if (brow) {
+      if (ri < ndr) { base = D; row = c0 + 16 + ri; }
+      else { base = R; row = ri - ndr; }
+    }
+    double x[16], xin[16], ys[16];
+    if (brow) {
+#pragma unroll
+      for (int t = 0; t < 16; t++) xin[t] = base[(c0 + t) * PB_LD + row];
+    }
+    auto solve_row = [&](auto exact_tag) -> bool {
+      constexpr bool EXACT = decltype(exact_tag)::value;
+      bool ok = true;
+#pragma unroll
+      for (int t = 0; t < 16; t++) x[t] = xin[t];
+#pragma unroll
+      for (int t = 0; t < 16; t++) {
+        const double utt = D[(c0 + t) * PB_LD + c0 + t];
+        if (EXACT) {
+          x[t] = dev::div_z(x[t], utt);                                             // Eq 6-a
+        } else {
+          ys[t] = x[t];
+          x[t] = dev::quot_mk(x[t], utt, rc[c0 + t]);
+        }
+#pragma unroll
+        for (int t2 = t + 1; t2 < 16; t2++) x[t2] = fma(-x[t], D[(c0 + t2) * PB_LD + c0 + t], x[t2]);
+      }
+      if (!EXACT) {
+#pragma unroll
+        for (int t = 0; t < 16; t++) ok &= dev::quot_is_rn(ys[t], D[(c0 + t) * PB_LD + c0 + t], x[t]);
+      }
+      return ok;
+    };
+    bool ok = true;
+    if (brow) ok = solve_row(std::false_type{});
+    if (__syncthreads_or(!ok)) {   // rare: the phase again with true division
+      if (brow) solve_row(std::true_type{});
+    }
+    if (brow) {
+#pragma unroll
+      for (int t = 0; t < 16; t++) base[(c0 + t) * PB_LD + row] = x[t];
+    }
+    __syncthreads();   // U12 of the sub-panel (B1) is complete
+    EBV_LTR(3 + 3 * (c0 / 16));
+    // ---- C: the rank-16 update of the row's entries right of the sub-panel
+    if (brow) {   // four columns at a time: four independent fma chains
+#pragma unroll 1
+      for (int j = c0 + 16; j < W; j += 4) {
+        double v[4];
+#pragma unroll
+        for (int e = 0; e < 4; e++) v[e] = base[(j + e) * PB_LD + row];
+#pragma unroll
+        for (int t = 0; t < 16; t++)
+#pragma unroll
+          for (int e = 0; e < 4; e++) v[e] = fma(-x[t], D[(j + e) * PB_LD + c0 + t], v[e]);   // Eq 6-c
+#pragma unroll
+        for (int e = 0; e < 4; e++) base[(j + e) * PB_LD + row] = v[e];
+      }
+    }
+    __syncthreads();
+    EBV_LTR(4 + 3 * (c0 / 16));
+  }
+  // ---- store: the diagonal block by the last CTA to arrive, every CTA its rows below
+  const bool store = slast != 0;
+  {
+    const int r = tid & (W - 1), c4 = tid >> 6;
+#pragma unroll
+    for (int it = 0; it < W / 4; it++) {
+      const int c = c4 + 4 * it;
+      if (store && r < w && c < w) P[r + (int64_t)c * lda] = D[c * PB_LD + r];
+      if (r < nrb && c < w) P[rb0 + r + (int64_t)c * lda] = R[c * PB_LD + r];
+    }
+  }
+  if (store && tid == 0 && binf) {
+    volatile int64_t* vi = info;
+    if (*vi == 0) *vi = koff + binf;
   }
 }
 
@@ -507,6 +720,15 @@ cudaError_t launch_leaf_lu(int64_t n, double* A, int64_t lda, const double* tau,
   return cudaGetLastError();
 }
 
+// EBV_PANEL_BLK=0: the column-step panel leaf instead of the blocked one
+static bool panel_blocked() {
+  static const bool v = [] {
+    const char* e = getenv("EBV_PANEL_BLK");
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
+
 static cudaError_t panel_leaf_attr(size_t smem) {
   return ensure_max_dyn_smem(reinterpret_cast<const void*>(panel_leaf_kernel<kLeafG>), (int)smem);
 }
@@ -515,12 +737,18 @@ cudaError_t launch_panel_leaf(int64_t M, int64_t w, double* P, int64_t lda, cons
                               int64_t koff, int* count, cudaStream_t s) {
   if (w <= 0 || M <= 0) return cudaSuccess;
   if (w > W || M < w) return cudaErrorInvalidValue;
+  const int64_t grid = M > w ? (M - w + W - 1) / W : 1;
+  if (panel_blocked()) {
+    cudaError_t e = ensure_max_dyn_smem(reinterpret_cast<const void*>(panel_blk_kernel), (int)kPanelBlkSmem);
+    if (e != cudaSuccess) return e;
+    panel_blk_kernel<<<(unsigned)grid, 256, kPanelBlkSmem, s>>>(M, (int)w, P, lda, tau, info, koff, count, 0, 0, 0);
+    return cudaGetLastError();
+  }
   const size_t smem = (size_t)W * kLeafG * (W / kLeafG + 2) * sizeof(double);
   {
     cudaError_t e = panel_leaf_attr(smem);
     if (e != cudaSuccess) return e;
   }
-  const int64_t grid = M > w ? (M - w + W - 1) / W : 1;
   panel_leaf_kernel<kLeafG><<<(unsigned)grid, W * kLeafG, smem, s>>>(M, (int)w, P, lda, tau, info, koff, count, 0, 0,
                                                                       0);
   return cudaGetLastError();
@@ -563,14 +791,20 @@ cudaError_t launch_panel_leaf_batched(int64_t M, int64_t w, double* P, int64_t l
                                       int64_t batch, cudaStream_t s) {
   if (w <= 0 || M <= 0 || batch <= 0) return cudaSuccess;
   if (w > W || M < w) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)W * kLeafG * (W / kLeafG + 2) * sizeof(double);
-  cudaError_t e = panel_leaf_attr(smem);
+  const bool blk = panel_blocked();
+  const size_t smem = blk ? kPanelBlkSmem : (size_t)W * kLeafG * (W / kLeafG + 2) * sizeof(double);
+  cudaError_t e = blk ? ensure_max_dyn_smem(reinterpret_cast<const void*>(panel_blk_kernel), (int)smem)
+                      : panel_leaf_attr(smem);
   if (e != cudaSuccess) return e;
   const int64_t grid = M > w ? (M - w + W - 1) / W : 1;
   for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
     const int64_t nb = batch - b0 < 65535 ? batch - b0 : 65535;
-    panel_leaf_kernel<kLeafG><<<dim3((unsigned)grid, (unsigned)nb), W * kLeafG, smem, s>>>(
-        M, (int)w, P + b0 * bsP, lda, tau + b0 * bsTau, info + b0 * bsInfo, koff, count + b0, bsP, bsInfo, bsTau);
+    if (blk)
+      panel_blk_kernel<<<dim3((unsigned)grid, (unsigned)nb), 256, smem, s>>>(
+          M, (int)w, P + b0 * bsP, lda, tau + b0 * bsTau, info + b0 * bsInfo, koff, count + b0, bsP, bsInfo, bsTau);
+    else
+      panel_leaf_kernel<kLeafG><<<dim3((unsigned)grid, (unsigned)nb), W * kLeafG, smem, s>>>(
+          M, (int)w, P + b0 * bsP, lda, tau + b0 * bsTau, info + b0 * bsInfo, koff, count + b0, bsP, bsInfo, bsTau);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

@@ -9,6 +9,14 @@
 #include "k_leaf.cu"
 #include <cstdio>
 #include <vector>
+#include <cstdlib>
+// this executable's own kernels need their attribute set through its own
+// runtime (libebv.so carries a separate static cudart)
+namespace ebv {
+cudaError_t ensure_max_dyn_smem(const void* fn, int bytes) {
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+}  // namespace ebv
 int main() {
   const int64_t ld = 8192 + 64;
   std::vector<double> h(ld * 64);
@@ -27,6 +35,30 @@ int main() {
     printf("m %5lld: stage U %lld, rcp %lld, X load %lld, blocks:", (long long)m, t[1] - t[0], t[2] - t[1], t[3] - t[2]);
     for (int b = 0; b < 8; b++) printf(" %lld", t[4 + b] - (b ? t[3 + b] : t[3]));
     printf("  total %lld cycles\n", t[11] - t[0]);
+  }
+  // the fused panel leaf (diagonal block in every CTA, then its 64 rows below)
+  int* cnt; cudaMalloc(&cnt, 4); cudaMemset(cnt, 0, 4);
+  double* tau; cudaMalloc(&tau, 8); cudaMemset(tau, 0, 8);
+  int64_t* info; cudaMalloc(&info, 8); cudaMemset(info, 0, 8);
+  for (int64_t M : {64, 1024, 4096}) {
+    for (int rep = 0; rep < 3; rep++) {
+      cudaMemcpy(d, h.data(), ld * 64 * 8, cudaMemcpyHostToDevice);
+      cudaError_t e = ebv::launch_panel_leaf(M, 64, d, ld, tau, info, 0, cnt, 0);
+      cudaError_t e2 = cudaDeviceSynchronize();
+      if (e != cudaSuccess || e2 != cudaSuccess) printf("launch %s / %s\n", cudaGetErrorString(e), cudaGetErrorString(e2));
+    }
+    long long t[16];
+    cudaMemcpyFromSymbol(t, ebv::g_ltrace, sizeof(t));
+    if (getenv("EBV_PANEL_BLK") && atoi(getenv("EBV_PANEL_BLK")) == 0) {
+      printf("panel_leaf M %5lld: load+arrive %lld, diag %lld, rcp %lld, x0 load %lld, rows below %lld, total %lld cycles\n",
+             (long long)M, t[1] - t[0], t[2] - t[1], t[3] - t[2], t[4] - t[3], t[5] - t[4], t[5] - t[0]);
+    } else {
+      printf("panel_blk M %5lld: load %lld;", (long long)M, t[1] - t[0]);
+      for (int sp = 0; sp < 4; sp++)
+        printf(" [A %lld B %lld C %lld]", t[2 + 3 * sp] - (sp ? t[1 + 3 * sp] : t[1]), t[3 + 3 * sp] - t[2 + 3 * sp],
+               t[4 + 3 * sp] - t[3 + 3 * sp]);
+      printf(" total %lld cycles\n", t[13] - t[0]);
+    }
   }
   return 0;
 }
