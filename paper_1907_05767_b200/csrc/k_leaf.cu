@@ -457,7 +457,7 @@ __global__ void __launch_bounds__(256) panel_blk_kernel(int64_t M, int w, double
   P += blockIdx.y * bsP;
   info += blockIdx.y * bsInfo;
   tau += blockIdx.y * bsTau;
-  count += blockIdx.y;
+  if (count) count += blockIdx.y;   // (nullptr: a single CTA, the diagonal block only)
   extern __shared__ __align__(16) double pbs[];
   double* D = pbs;                     // diagonal block: D[c * PB_LD + r]
   double* R = pbs + W * PB_LD;         // the CTA's rows below: R[c * PB_LD + r]
@@ -486,12 +486,16 @@ __global__ void __launch_bounds__(256) panel_blk_kernel(int64_t M, int w, double
   const double tv = *tau;
   __syncthreads();   // every CTA has read the unfactored diagonal block
   if (tid == 0) {
-    __threadfence();
-    const int old = atomicAdd(count, 1);
-    slast = old == (int)gridDim.x - 1;
-    if (slast) {
-      *count = 0;
+    if (!count) {
+      slast = 1;
+    } else {
       __threadfence();
+      const int old = atomicAdd(count, 1);
+      slast = old == (int)gridDim.x - 1;
+      if (slast) {
+        *count = 0;
+        __threadfence();
+      }
     }
   }
   int binf = 0;
@@ -712,14 +716,6 @@ cudaError_t launch_trsm_left_upper(int64_t k, int64_t m, const double* U, int64_
   return cudaGetLastError();
 }
 
-cudaError_t launch_leaf_lu(int64_t n, double* A, int64_t lda, const double* tau, int64_t* info, int64_t koff,
-                           cudaStream_t s) {
-  if (n <= 0) return cudaSuccess;
-  if (n > W) return cudaErrorInvalidValue;
-  leaf_lu_kernel<kLeafG><<<1, W * kLeafG, 0, s>>>((int)n, A, lda, tau, info, koff);
-  return cudaGetLastError();
-}
-
 // EBV_PANEL_BLK=0: the column-step panel leaf instead of the blocked one
 static bool panel_blocked() {
   static const bool v = [] {
@@ -727,6 +723,20 @@ static bool panel_blocked() {
     return !(e && atoi(e) == 0);
   }();
   return v;
+}
+
+cudaError_t launch_leaf_lu(int64_t n, double* A, int64_t lda, const double* tau, int64_t* info, int64_t koff,
+                           cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  if (n > W) return cudaErrorInvalidValue;
+  if (panel_blocked()) {   // the blocked panel leaf with no rows below
+    cudaError_t e = ensure_max_dyn_smem(reinterpret_cast<const void*>(panel_blk_kernel), (int)kPanelBlkSmem);
+    if (e != cudaSuccess) return e;
+    panel_blk_kernel<<<1, 256, kPanelBlkSmem, s>>>(n, (int)n, A, lda, tau, info, koff, nullptr, 0, 0, 0);
+    return cudaGetLastError();
+  }
+  leaf_lu_kernel<kLeafG><<<1, W * kLeafG, 0, s>>>((int)n, A, lda, tau, info, koff);
+  return cudaGetLastError();
 }
 
 static cudaError_t panel_leaf_attr(size_t smem) {
