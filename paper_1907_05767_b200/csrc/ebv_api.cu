@@ -184,9 +184,11 @@ static int kU12La = [] {
   return e ? atoi(e) : -1;
 }();
 
+// round 2 (with the blocked panel leaf): 6144 — n = 16384 96.7 -> 95.7 ms,
+// n = 32768 703.2 -> 701.4 ms (4096: 96.1 / 702.1; 12288 no gain)
 static int64_t kTailRows = [] {
   const char* e = getenv("EBV_TAIL_ROWS");
-  return e ? (int64_t)atoll(e) : (int64_t)0;
+  return e ? (int64_t)atoll(e) : (int64_t)6144;
 }();
 
 // panels up to this many rows take the fused panel-leaf kernel (round 2,
@@ -242,12 +244,12 @@ int64_t block_width(const ebv_context* c, int64_t n) {
   return ((nb + c->leaf - 1) / c->leaf) * c->leaf;
 }
 
-// Width of the column block starting at c0.  EBV_TAIL_ROWS=t (experiment
-// knob, off by default) narrows the panels to 128 once fewer than t rows
-// remain; measured at n = 32768: t = 2048..8192 within 0.4% of fixed nb
-// (box-to-box noise ~2%), and widths adapted to the whole remaining order
-// were 1% slower.  Any sequence of widths keeps every entry's operation
-// order (bitwise the same factors).
+// Width of the column block starting at c0.  EBV_TAIL_ROWS=t narrows the
+// panels to 128 once fewer than t rows remain (the tail, where the panel
+// chain is exposed); round 1 measured no gain with the column-step leaf,
+// round 2 with the blocked leaf 0.3-1% (default 6144); widths adapted to
+// the whole remaining order were 1% slower.  Any sequence of widths keeps
+// every entry's operation order (bitwise the same factors).
 static int64_t step_width(const ebv_context* c, int64_t n, int64_t c0) {
   const int64_t nb = block_width(c, n);
   const int64_t w = (c->nb > 0 || n - c0 > kTailRows) ? nb : (nb < 128 ? nb : 128);
