@@ -175,7 +175,8 @@ static int64_t kU12SplitRows = [] {
 // streamed host factor plan: PCIe copy rate and DMMA update rate (B200)
 static const double kHostCopyBps = 55e9, kUpdateFlops = 33e12;
 
-// U12 lookahead (EBV_U12_LA: -1 auto = n >= 16384, 0 off, 1 on): step K
+// U12 lookahead (EBV_U12_LA: -1 auto = n >= 8192 here, n >= 16384 in the
+// distributed schedule; 0 off, 1 on): step K
 // updates block row K+1 first, and the side stream computes U12 of step K+1
 // (after panel K+1) while the main stream updates the rows below; see
 // lu_blocked.
