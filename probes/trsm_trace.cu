@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <vector>
 #include <cstdlib>
+#include <cmath>
+#include <cstdint>
 // this executable's own kernels need their attribute set through its own
 // runtime (libebv.so carries a separate static cudart)
 namespace ebv {
@@ -22,6 +24,15 @@ int main() {
   std::vector<double> h(ld * 64);
   for (int64_t c = 0; c < 64; c++)
     for (int64_t r = 0; r < ld; r++) h[r + c * ld] = (r == c) ? 65.0 : ((r * 7 + c * 13) % 17 - 8) * 1e-2;
+  if (getenv("EBV_PROBE_REAL")) {   // generator-like values: k * 2^-30, diag = row sum + 1
+    uint64_t st = 88172645463325252ull;
+    for (int64_t c = 0; c < 64; c++)
+      for (int64_t r = 0; r < ld; r++) {
+        st ^= st << 13; st ^= st >> 7; st ^= st << 17;
+        h[r + c * ld] = (double)((int64_t)(st % (1ull << 31)) - (1ll << 30)) * 9.313225746154785e-10;
+      }
+    for (int64_t r = 0; r < 64; r++) { double sum = 1.0; for (int64_t c = 0; c < 64; c++) if (c != r) sum += fabs(h[r + c * ld]); h[r + r * ld] = sum; }
+  }
   double* d;
   cudaMalloc(&d, ld * 64 * 8);
   for (int64_t m : {64, 1024, 8192}) {
@@ -58,6 +69,28 @@ int main() {
         printf(" [A %lld B %lld C %lld]", t[2 + 3 * sp] - (sp ? t[1 + 3 * sp] : t[1]), t[3 + 3 * sp] - t[2 + 3 * sp],
                t[4 + 3 * sp] - t[3 + 3 * sp]);
       printf(" total %lld cycles\n", t[13] - t[0]);
+    }
+  }
+  {   // schedule-like: a 1024 x 1024 matrix, lda 1024, panels at c0 = 0, 64, ... (events)
+    const int64_t n = 1024;
+    std::vector<double> hm(n * n);
+    for (int64_t c = 0; c < n; c++)
+      for (int64_t r = 0; r < n; r++) hm[r + c * n] = (r == c) ? 600.0 : ((r * 7 + c * 13) % 17 - 8) * 1e-2;
+    double* dm; cudaMalloc(&dm, n * n * 8);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    for (int64_t c0 : {0, 64, 512, 896}) {
+      float best = 1e9;
+      for (int rep = 0; rep < 5; rep++) {
+        cudaMemcpy(dm, hm.data(), n * n * 8, cudaMemcpyHostToDevice);
+        cudaEventRecord(e0);
+        ebv::launch_panel_leaf(n - c0, 64, dm + c0 + c0 * n, n, tau, info, c0, cnt, 0);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+      }
+      printf("schedule-like panel c0 %4lld M %4lld: %.2f us (%s)\n", (long long)c0, (long long)(n - c0), best * 1e3,
+             cudaGetErrorString(cudaGetLastError()));
     }
   }
   return 0;
