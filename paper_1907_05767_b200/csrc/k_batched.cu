@@ -455,6 +455,100 @@ __global__ void __launch_bounds__(128) batched1_kernel(int n, double* __restrict
   }
 }
 
+// ---------------------------------------------------------------- plain lane map (comparison)
+// The lane-level comparison SURVEY §8(a') asks for: one system per warp,
+// lane i owns row i (no first-with-last pairing), otherwise the scheme of
+// batched1_kernel (forward fused into the factor, the first U-row chunk
+// shuffled before the divisions, Markstein backward with the deferred
+// test).  Selected with EBV_BATCHED_PLAIN=1; bitwise the same results.
+template <bool FULL, bool HASB>
+__global__ void __launch_bounds__(128) batched_plain_kernel(int n, double* __restrict__ A, int64_t lda,
+                                                            int64_t strideA, int64_t batch, double* __restrict__ B,
+                                                            int64_t strideB, const double* __restrict__ tau_ptr,
+                                                            int tau_default, double tau_value,
+                                                            int32_t* __restrict__ info) {
+  const int i = threadIdx.x & 31;
+  const int64_t sys = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const bool act = sys < batch;
+  const bool v = act && (FULL || i < n);
+  double* As = A + (act ? sys : 0) * strideA;
+  double* Bs = HASB ? B + (act ? sys : 0) * strideB : nullptr;
+  double a[NP], y = 0.0;
+#pragma unroll
+  for (int j = 0; j < NP; j++)
+    a[j] = (v && (FULL || j < n)) ? As[i + (int64_t)j * lda] : (i == j ? 1.0 : 0.0);
+  if (HASB) y = v ? Bs[i] : 0.0;
+  double tv = tau_value;
+  if (tau_default) {
+    double sr = 0.0;
+#pragma unroll
+    for (int j = 0; j < NP; j++)
+      if (FULL || j < n) sr += fabs(a[j]);
+    double nm = v ? sr : 0.0;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) nm = fmax(nm, __shfl_xor_sync(0xffffffffu, nm, o));
+    tv = (double)n * 2.220446049250313e-16 * nm;
+  } else if (tau_ptr) {
+    tv = *tau_ptr;
+  }
+  int inf = 0;
+  double d = 1.0;
+#pragma unroll
+  for (int k = 0; k < NP; k++) {
+    const double piv = __shfl_sync(0xffffffffu, a[k], k);
+    d = i == k ? piv : d;
+    if ((FULL || k < n) && inf == 0 && fabs(piv) <= tv) inf = k + 1;
+    double u0[CH], yk = 0.0;
+    const int j1 = k + 1;
+#pragma unroll
+    for (int q = 0; q < CH; q++)
+      if (j1 + q < NP) u0[q] = __shfl_sync(0xffffffffu, a[j1 + q], k);
+    if (HASB) yk = __shfl_sync(0xffffffffu, y, k);
+    const bool below = i > k;
+    if (below) a[k] = divp<!FULL>(a[k], piv);                                   // Eq 6-a
+    const double nl = -a[k];
+#pragma unroll
+    for (int j0 = j1; j0 < NP; j0 += CH) {
+      double u[CH];
+#pragma unroll
+      for (int q = 0; q < CH; q++)
+        if (j0 + q < NP) u[q] = j0 == j1 ? u0[q] : __shfl_sync(0xffffffffu, a[j0 + q], k);
+      if (below) {
+#pragma unroll
+        for (int q = 0; q < CH; q++)
+          if (j0 + q < NP) a[j0 + q] = fma(nl, u[q], a[j0 + q]);                   // Eq 6-c
+      }
+    }
+    if (HASB && below) y = fma(nl, yk, y);                                        // Eq 1, L y = b
+  }
+  if (act && i == 0 && info) info[sys] = inf;
+  if (HASB) {
+    const double yf = y, rd = dev::rcp_approx(d);
+    double yo = 0.0, qo = 0.0;
+    auto sweep = [&](auto mk_tag) {
+      constexpr bool MK = decltype(mk_tag)::value;
+#pragma unroll
+      for (int k = NP - 1; k >= 0; k--) {
+        if (i == k) {
+          if (MK) { yo = y; y = quot_mk(y, d, rd); qo = y; }
+          else y = divp<!FULL>(y, a[k]);
+        }
+        const double xk = __shfl_sync(0xffffffffu, y, k);
+        if (i < k) y = fma(-a[k], xk, y);
+      }
+    };
+    sweep(std::true_type{});
+    if (__any_sync(0xffffffffu, !quot_exact(yo, d, qo))) {
+      y = yf;
+      sweep(std::false_type{});
+    }
+    if (v) Bs[i] = y;
+  }
+#pragma unroll
+  for (int j = 0; j < NP; j++)
+    if (v && (FULL || j < n)) As[i + (int64_t)j * lda] = a[j];
+}
+
 // ---------------------------------------------------------------- 33 <= n <= 64
 // SURVEY §8f f2 (batched medium systems, CTA per system).  One CTA of 128
 // threads per system: row i is owned by the lane pair (2i, 2i+1), lane j of
@@ -690,6 +784,18 @@ cudaError_t launch_batched(int64_t n, double* A, int64_t lda, int64_t strideA, i
     const char* e = getenv("EBV_BATCHED_V1");
     return !(e && atoi(e) == 0);
   }();
+  static const bool plain = [] {   // EBV_BATCHED_PLAIN=1: one system per warp, lane = row (comparison)
+    const char* e = getenv("EBV_BATCHED_PLAIN");
+    return e && atoi(e) == 1;
+  }();
+  if (plain && !solve_only && nrhs <= 1) {
+    const bool hasb = B && nrhs == 1;
+    const unsigned gp = (unsigned)((batch * 32 + 127) / 128);
+    auto k = n == NP ? (hasb ? batched_plain_kernel<true, true> : batched_plain_kernel<true, false>)
+                     : (hasb ? batched_plain_kernel<false, true> : batched_plain_kernel<false, false>);
+    k<<<gp, 128, 0, s>>>((int)n, A, lda, strideA, batch, B, strideB, tau, td, tau_value, info);
+    return cudaGetLastError();
+  }
   if (v1 && !solve_only && nrhs <= 1) {
     const bool hasb = B && nrhs == 1;
     if (n == NP && hasb)
