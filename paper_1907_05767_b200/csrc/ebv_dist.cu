@@ -84,6 +84,18 @@ NcclApi& nccl() {
   return api;
 }
 
+// EBV_DIST_FORCE_NCCL=1: a one-rank communicator still takes the NCCL data
+// path (panel broadcasts, info / row-sum all-reduces, the ring solve and its
+// final broadcast) — a one-rank collective is a local copy, so the calls,
+// their streams and the event protocol around them run on one GPU (tests)
+bool force_nccl() {
+  static const bool v = [] {
+    const char* e = getenv("EBV_DIST_FORCE_NCCL");
+    return e && atoi(e) == 1;
+  }();
+  return v;
+}
+
 ebv_status_t nccl_fail(ncclResult_t r, const char* where) {
   const char* m = nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error";
   set_error(std::string(where) + ": " + m);
@@ -207,7 +219,7 @@ ebv_status_t dist_factor(ebv_context* c, ebv_dist_state* d, std::vector<View>& v
   const size_t half = (size_t)n * nb;
   ebv_status_t st = ensure_pbuf(c, d, half);
   if (st != EBV_SUCCESS) return st;
-  const bool real = d->comm && d->nranks > 1;
+  const bool real = d->comm && (d->nranks > 1 || force_nccl());
   cudaStream_t side = c->side;
   cudaError_t e = cudaEventRecord(d->ev_side, s);                  // side starts after the caller's work
   if (e == cudaSuccess) e = cudaStreamWaitEvent(side, d->ev_side, 0);
@@ -359,10 +371,10 @@ ebv_status_t dist_solve(ebv_context* c, ebv_dist_state* d, std::vector<View>& vi
                         int64_t ldb, int64_t nrhs, cudaStream_t s) {
   const Plan& p0 = views[0].plan;
   const int64_t nb = p0.nb, N = p0.N;
-  const bool real = d->comm && d->nranks > 1;
+  const bool real = d->comm && (d->nranks > 1 || force_nccl());
   const size_t cnt = (size_t)(ldb * (nrhs - 1) + n);
   if (n <= 0 || nrhs <= 0) return EBV_SUCCESS;
-  if (d->nranks == 1 && views.size() == 1) {
+  if (d->nranks == 1 && views.size() == 1 && !(d->comm && force_nccl())) {
     // one rank: its slab is the whole matrix (blocks in ascending order),
     // so the ring has no hop — the single-GPU solve, same per-entry order
     return solve_full(c, n, views[0].A, views[0].lda, B, ldb, nrhs, s);
@@ -463,7 +475,7 @@ ebv_status_t dist_tau(ebv_context* c, ebv_dist_state* d, std::vector<View>& view
     c->launches += 1;
     first = false;
   }
-  if (d->comm && d->nranks > 1) {
+  if (d->comm && (d->nranks > 1 || force_nccl())) {
     ncclResult_t r = nccl().AllReduce(c->d_vec, c->d_vec, (size_t)n, ncclFloat64, ncclSum, d->comm, s);
     if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce(row sums)");
     c->launches += 1;

@@ -187,3 +187,49 @@ def test_emulated_dist_default_pivot_floor(dev, ctx, P, nb, n):
     torch.cuda.synchronize()
     assert int(info) == int(info1) > 0
     assert bits_eq(assemble(slabs, colmaps, n), LU1.cpu().numpy())
+
+
+_FORCED_SNIPPET = r"""
+import sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch, ebv_inputs, oracle
+import paper_1907_05767_b200 as ebv
+dev = torch.device("cuda:0")
+ebv.load_nccl()
+for n, nb, tau in ((900, 128, -1.0), (1536, 256, 0.0)):
+    uid = ebv.ebv_get_unique_id()
+    h = ebv.ebv_create_dist(0, uid, 0, 1, nb, 0)
+    d = ebv_inputs.generate(n, seed=5 + n, nrhs=2, device=dev)
+    slab = d["At"].clone()
+    info = torch.zeros((), dtype=torch.int64, device=dev)
+    sh = torch.cuda.current_stream().cuda_stream
+    assert ebv.ebv_lu_factor_dist(h, n, slab.data_ptr(), n, tau, info.data_ptr(), sh) == 0, ebv.ebv_last_error()
+    B = d["B"].T.clone(memory_format=torch.contiguous_format)
+    assert ebv.ebv_lu_solve_dist(h, n, slab.data_ptr(), n, B.data_ptr(), n, 2, sh) == 0, ebv.ebv_last_error()
+    torch.cuda.synchronize()
+    lu_o, info_o = oracle.lu_factor(d["At"].T.cpu().numpy())
+    assert np.array_equal(slab.T.cpu().numpy().view(np.uint64), lu_o.view(np.uint64))
+    x_o = oracle.lu_solve(lu_o, d["B"].cpu().numpy())
+    assert np.array_equal(B.T.cpu().numpy().view(np.uint64), x_o.view(np.uint64))
+    assert int(info) == info_o == 0
+    ebv.ebv_destroy(h)
+print("forced NCCL data path bitwise ok")
+"""
+
+
+def test_real_nccl_single_rank_data_path():
+    """The NCCL data path itself on one GPU: with EBV_DIST_FORCE_NCCL=1 a
+    one-rank communicator still broadcasts every panel, all-reduces info and
+    (tau < 0) the row sums, and runs the ring solve with its final
+    broadcast — a one-rank collective is a local copy, so the calls, streams
+    and event protocol of the multi-rank schedule execute and must leave the
+    results bitwise the oracle's.  (The switch is read once per process.)"""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, EBV_DIST_FORCE_NCCL="1")
+    r = subprocess.run([sys.executable, "-c", _FORCED_SNIPPET, root], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "bitwise ok" in r.stdout
