@@ -33,6 +33,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -573,12 +574,69 @@ ebv_status_t ebv_lu_factor_dist(ebv_context_t c, int64_t n, double* A_local, int
   if (views[0].plan.cols > 0 && !A_local) return invalid("ebv_lu_factor_dist: A_local NULL");
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
-  cudaError_t e = launch_set_info0(d_info, s);
-  if (e != cudaSuccess) return cuda_fail(e, "dist init");
-  c->launches += 1;
-  st = dist_tau(c, d, views, n, tau, s);
-  if (st != EBV_SUCCESS || n == 0) return st;
-  return dist_factor(c, d, views, n, d_info, s);
+  // CUDA-graph replay, as ebv_lu_factor: the second call with the same
+  // arguments captures the schedule (kernels, events and the NCCL
+  // collectives, which NCCL supports in captured streams; every rank
+  // captures and replays the same collective sequence), later calls replay
+  // it (EBV_DIST_GRAPHS=0: launch directly every time)
+  static const bool kDistGraphs = [] {
+    const char* ev = getenv("EBV_DIST_GRAPHS");
+    return !(ev && atoi(ev) == 0);
+  }();
+  ebv_context::GraphEntry* ge = nullptr;
+  const bool use_graph = kDistGraphs && c->graphs && !c->stats && s != nullptr && n > 0;
+  if (use_graph) {
+    for (auto& en : c->gcache)
+      if (en.n == n && en.lda == lda && en.A == A_local && en.info == d_info && en.tau == tau && en.nb == d->nb &&
+          en.leaf == c->leaf && en.la == c->lookahead) {
+        ge = &en;
+        break;
+      }
+    if (ge && ge->exec) {
+      cudaError_t e = cudaGraphLaunch(ge->exec, s);
+      if (e != cudaSuccess) return cuda_fail(e, "dist graph launch");
+      c->launches += ge->launches;
+      return EBV_SUCCESS;
+    }
+    if (!ge) {
+      if (c->gcache.size() >= 8) {
+        if (c->gcache.front().exec) cudaGraphExecDestroy(c->gcache.front().exec);
+        c->gcache.erase(c->gcache.begin());
+      }
+      c->gcache.push_back({n, lda, d->nb, c->leaf, A_local, d_info, tau, c->lookahead, 0, 0, nullptr});
+      ge = &c->gcache.back();
+    }
+    ge->hits++;
+  }
+  auto run = [&]() -> ebv_status_t {
+    cudaError_t e = launch_set_info0(d_info, s);
+    if (e != cudaSuccess) return cuda_fail(e, "dist init");
+    c->launches += 1;
+    ebv_status_t r = dist_tau(c, d, views, n, tau, s);
+    if (r == EBV_SUCCESS && n > 0) r = dist_factor(c, d, views, n, d_info, s);
+    return r;
+  };
+  const bool capture = use_graph && ge && ge->hits >= 2;
+  if (!capture) return run();
+  const int64_t l0 = c->launches;
+  bool ok = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  st = ok ? run() : EBV_ERR_CUDA;
+  cudaGraph_t graph = nullptr;
+  if (ok) ok = cudaStreamEndCapture(s, &graph) == cudaSuccess && st == EBV_SUCCESS;
+  if (ok) ok = cudaGraphInstantiateWithFlags(&ge->exec, graph, cudaGraphInstantiateFlagUseNodePriority) == cudaSuccess;
+  if (graph) cudaGraphDestroy(graph);
+  if (!ok) {
+    // the capture failed (nothing of it ran): never capture these arguments
+    // again and run the schedule directly
+    (void)cudaGetLastError();
+    ge->exec = nullptr;
+    ge->hits = INT32_MIN / 2;
+    return run();
+  }
+  ge->launches = c->launches - l0;
+  cudaError_t ec = cudaGraphLaunch(ge->exec, s);
+  if (ec != cudaSuccess) return cuda_fail(ec, "dist graph launch");
+  return EBV_SUCCESS;
 }
 
 ebv_status_t ebv_lu_solve_dist(ebv_context_t c, int64_t n, const double* LU_local, int64_t lda, double* B, int64_t ldb,

@@ -200,18 +200,22 @@ for n, nb, tau in ((900, 128, -1.0), (1536, 256, 0.0)):
     uid = ebv.ebv_get_unique_id()
     h = ebv.ebv_create_dist(0, uid, 0, 1, nb, 0)
     d = ebv_inputs.generate(n, seed=5 + n, nrhs=2, device=dev)
-    slab = d["At"].clone()
-    info = torch.zeros((), dtype=torch.int64, device=dev)
-    sh = torch.cuda.current_stream().cuda_stream
-    assert ebv.ebv_lu_factor_dist(h, n, slab.data_ptr(), n, tau, info.data_ptr(), sh) == 0, ebv.ebv_last_error()
-    B = d["B"].T.clone(memory_format=torch.contiguous_format)
-    assert ebv.ebv_lu_solve_dist(h, n, slab.data_ptr(), n, B.data_ptr(), n, 2, sh) == 0, ebv.ebv_last_error()
-    torch.cuda.synchronize()
     lu_o, info_o = oracle.lu_factor(d["At"].T.cpu().numpy())
-    assert np.array_equal(slab.T.cpu().numpy().view(np.uint64), lu_o.view(np.uint64))
     x_o = oracle.lu_solve(lu_o, d["B"].cpu().numpy())
-    assert np.array_equal(B.T.cpu().numpy().view(np.uint64), x_o.view(np.uint64))
-    assert int(info) == info_o == 0
+    slab = torch.empty_like(d["At"])
+    info = torch.zeros((), dtype=torch.int64, device=dev)
+    s = torch.cuda.Stream(dev)   # a created stream: the second call captures a graph, later calls replay it
+    sh = s.cuda_stream
+    for rep in range(4):
+        with torch.cuda.stream(s):
+            slab.copy_(d["At"])
+            assert ebv.ebv_lu_factor_dist(h, n, slab.data_ptr(), n, tau, info.data_ptr(), sh) == 0, ebv.ebv_last_error()
+            B = d["B"].T.clone(memory_format=torch.contiguous_format)
+            assert ebv.ebv_lu_solve_dist(h, n, slab.data_ptr(), n, B.data_ptr(), n, 2, sh) == 0, ebv.ebv_last_error()
+        torch.cuda.synchronize()
+        assert np.array_equal(slab.T.cpu().numpy().view(np.uint64), lu_o.view(np.uint64)), rep
+        assert np.array_equal(B.T.cpu().numpy().view(np.uint64), x_o.view(np.uint64)), rep
+        assert int(info) == info_o == 0
     ebv.ebv_destroy(h)
 print("forced NCCL data path bitwise ok")
 """
@@ -223,7 +227,9 @@ def test_real_nccl_single_rank_data_path():
     (tau < 0) the row sums, and runs the ring solve with its final
     broadcast — a one-rank collective is a local copy, so the calls, streams
     and event protocol of the multi-rank schedule execute and must leave the
-    results bitwise the oracle's.  (The switch is read once per process.)"""
+    results bitwise the oracle's, also when the schedule is captured into a
+    CUDA graph (second call) and replayed (later calls).  (The switch is read
+    once per process.)"""
     import os
     import subprocess
     import sys
