@@ -24,7 +24,10 @@ namespace {
 constexpr int NP = 32;   // padded order
 constexpr int MAXRHS = 16;
 
-constexpr int CH = 8;     // columns per shuffle chunk
+#ifndef EBV_BATCHED_CH
+#define EBV_BATCHED_CH 8
+#endif
+constexpr int CH = EBV_BATCHED_CH;   // columns per shuffle chunk
 
 // Markstein quotient from an approximate reciprocal, and the exact test that
 // it is RN(y / u) (remainder y - q u exact by fma, inside half an ulp of q
