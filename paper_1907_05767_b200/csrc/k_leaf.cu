@@ -1,7 +1,10 @@
 // k_leaf.cu — the small dense pieces of the blocked EbV LU (all <= 64 wide):
 //   leaf_lu          LU of a diagonal block (w <= 64) in one CTA
-//   trsm_right_upper L21 = A21 U11^-1, one thread per row (row-parallel)
-//   trsm_left_lower  U12 = L11^-1 A12, one thread per column (column-parallel)
+//   panel_leaf       the diagonal block and the rows below in one launch
+//                    (column steps); panel_blk: the same in 16-column
+//                    sub-panels (round 2, the default when rows below exist)
+//   trsm_right_upper L21 = A21 U11^-1, a lane group per row (row-parallel)
+//   trsm_left_lower  U12 = L11^-1 A12, a lane group per column (column-parallel)
 //
 // Paper: Eq 6-a l_ik = a_ik / a_kk; Eq 6-b the U_(k) row; Eq 6-c
 // the rank-1 update.  Per entry, updates are applied as
@@ -9,8 +12,8 @@
 // canonical order of DESIGN.md — so each kernel is bitwise equal to the
 // corresponding part of the serial oracle.
 //
-// Every kernel works on a fixed 64-wide block held in registers (fully
-// unrolled, no runtime guards); a narrower block (a ragged tail) is padded
+// Every kernel works on a fixed 64-wide block (in registers, or for
+// panel_blk in shared memory); a narrower block (a ragged tail) is padded
 // with an identity: padded multipliers are exactly 0 and fma(-0, u, a) == a,
 // so the real entries see exactly the same operation sequence.
 #include "ebv_internal.cuh"
