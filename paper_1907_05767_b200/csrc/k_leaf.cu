@@ -800,7 +800,10 @@ cudaError_t launch_panel_leaf_batched(int64_t M, int64_t w, double* P, int64_t l
                                       int64_t batch, cudaStream_t s) {
   if (w <= 0 || M <= 0 || batch <= 0) return cudaSuccess;
   if (w > W || M < w) return cudaErrorInvalidValue;
-  const bool blk = panel_blocked();
+  // the batched form keeps the column-step kernel: with many independent
+  // panels per launch throughput wins, and the blocked kernel's one CTA per
+  // SM (255 registers, 67 KB) lost there (20000 x n = 128: 12.46 -> 13.40 ms)
+  const bool blk = false;
   const size_t smem = blk ? kPanelBlkSmem : (size_t)W * kLeafG * (W / kLeafG + 2) * sizeof(double);
   cudaError_t e = blk ? ensure_max_dyn_smem(reinterpret_cast<const void*>(panel_blk_kernel), (int)smem)
                       : panel_leaf_attr(smem);
